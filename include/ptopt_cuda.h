@@ -1,0 +1,311 @@
+/*
+ * ptopt_cuda.h — C-ABI of the B200 (sm_100a) implementation of the batched
+ * 6-DoF powered-descent SCP hot path:
+ *     exact discretization -> power iteration -> customized PIPG -> SCP loop.
+ *
+ * This header is the drop-in boundary.  The reference (/root/reference/proj)
+ * is a header-only C++ template library with no FFI of its own; the entry
+ * points below are what a binding for this path would bind.  Each one names
+ * the reference interface it replaces (file:line relative to
+ * /root/reference/).  Plain C, `extern "C"`, plain pointers and sizes, no C++
+ * or torch types.
+ *
+ * Conventions
+ *   - All arrays are dense, row-major, IEEE fp64, instance-major
+ *     ([B][...] with B the batch size).  Matrices follow the reference's
+ *     Mat<R,C> row-major order a[i*cols+j] (proj/include/ptopt/smallmat.hpp:60).
+ *   - Every call returns a ptopt_call_status: 0 = the call ran; negative = a
+ *     call-level error (bad argument, CUDA failure) described by
+ *     ptopt_cuda_last_error().  A failing *instance* never fails the call:
+ *     per-instance outcomes come back in status[B] / fail_index[B], mirroring
+ *     mc::solve_instance which converts exceptions into RunRecord::failure
+ *     (proj/include/ptopt/montecarlo.hpp:114-132).
+ *   - Functions without the `_dev` suffix take HOST pointers and perform the
+ *     host<->device copies themselves (pageable or pinned memory both work).
+ *     `_dev` variants take DEVICE pointers valid on the handle's device and
+ *     enqueue work on the handle's stream without synchronising.
+ *   - The caller owns every buffer; the library allocates only its private
+ *     per-handle scratch.  A handle is not thread-safe; use one handle per
+ *     (device, host thread).
+ *   - There is no CPU fallback: every entry point fails with PTOPT_ERR_CUDA
+ *     when no sm_100 device is usable.
+ */
+#ifndef PTOPT_CUDA_H_
+#define PTOPT_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTOPT_ABI_VERSION 1
+
+/* Dimensions of the rocket path (proj/include/ptopt/rocket6dof.hpp:13-15,
+ * proj/include/ptopt/ctcs.hpp:25-28). */
+#define PTOPT_NXI 14   /* model state  xi = (m, r, v, q, w)              */
+#define PTOPT_NZETA 6  /* model control zeta = (T_body, torque_body)     */
+#define PTOPT_NG 9     /* path inequalities                              */
+#define PTOPT_NX 15    /* augmented state  x = (xi, y)                   */
+#define PTOPT_NU 7     /* augmented control u = (zeta, s)                */
+#define PTOPT_HISTORY_FIELDS 5 /* defect_inf, step_inf, penalized_cost, pipg_iterations, sigma
+                                  (proj/include/ptopt/scp.hpp:219-226) */
+
+/* Call-level status. */
+typedef enum ptopt_call_status {
+  PTOPT_OK = 0,
+  PTOPT_ERR_INVALID_ARGUMENT = -1, /* std::invalid_argument in the reference   */
+  PTOPT_ERR_CUDA = -2,             /* CUDA runtime / no usable device          */
+  PTOPT_ERR_UNSUPPORTED = -3,      /* shape outside what the kernels implement */
+  PTOPT_ERR_ALLOC = -4
+} ptopt_call_status;
+
+/* Per-instance status (what the reference reports by throwing). */
+typedef enum ptopt_instance_status {
+  PTOPT_ST_OK = 0,
+  /* PropagationDiverged{interval} (proj/include/ptopt/discretizer.hpp:18-23, 89, 136);
+   * fail_index = interval. */
+  PTOPT_ST_PROPAGATION_DIVERGED = 1,
+  /* pipg::SolverDiverged{iteration} (proj/include/ptopt/pipg.hpp:16-20, 476-478);
+   * fail_index = PIPG iteration. */
+  PTOPT_ST_SOLVER_DIVERGED = 2,
+  /* std::domain_error "dilation factor must be positive" (proj/include/ptopt/ctcs.hpp:66, 82);
+   * fail_index = interval. */
+  PTOPT_ST_DILATION_NONPOSITIVE = 3,
+  /* std::domain_error "nonpositive mass" (proj/include/ptopt/rocket6dof.hpp:246, 308). */
+  PTOPT_ST_MASS_NONPOSITIVE = 4,
+  /* std::domain_error "thrust magnitude below singular-point tolerance"
+   * (proj/include/ptopt/rocket6dof.hpp:306-307). */
+  PTOPT_ST_THRUST_SINGULAR = 5,
+  /* std::invalid_argument "seed point must not be all zero"
+   * (proj/include/ptopt/pipg.hpp:224-225). */
+  PTOPT_ST_POWER_SEED_ZERO = 6
+} ptopt_instance_status;
+
+/* rocket::VehicleParams (proj/include/ptopt/rocket6dof.hpp:85-99). */
+typedef struct ptopt_vehicle_params {
+  double alpha_mdot;
+  double g_inertial[3];
+  double inertia[9];  /* row-major 3x3 */
+  double r_thrust[3];
+  double H_theta[8];  /* row-major 2x4 tilt selector */
+  double m_dry;
+  double v_max;
+  double theta_max;
+  double omega_max;
+  double delta_max;
+  double T_min;
+  double T_max;
+  double gamma_max;
+} ptopt_vehicle_params;
+
+/* pipg::PipgConfig (proj/include/ptopt/pipg.hpp:22-38). */
+typedef struct ptopt_pipg_config {
+  double omega;
+  double rho;
+  int32_t j_max;
+  int32_t j_check;
+  double eps_abs;
+  double eps_rel;
+  double eps_buff;
+} ptopt_pipg_config;
+
+/* Flattened ScpProblem<Rocket6DoF> minus the per-instance fields (init_state,
+ * rng_seed) (proj/include/ptopt/scp.hpp:73-121; proj/include/ptopt/rocket_problem.hpp:59-94).
+ * px/pu are the already power-of-two-rounded scales of ScalingPair
+ * (proj/include/ptopt/scp.hpp:39-59); their reciprocals are exact. */
+typedef struct ptopt_problem_desc {
+  ptopt_vehicle_params vehicle;
+  int32_t nodes;            /* grid.size()                       */
+  int32_t integrator_steps; /* RK4 substeps per interval         */
+  double s_min;
+  double s_max;
+  double t_f_guess;
+  double w_cost;            /* ScpWeights (scp.hpp:18-22)        */
+  double w_prox;
+  double w_ep;
+  double epsilon_relax;
+  double px[PTOPT_NX];
+  double pu[PTOPT_NU];
+  ptopt_pipg_config pipg;
+  int32_t power_j_max;
+  int32_t max_iters;
+  double power_eps_abs;
+  double power_eps_rel;
+  double tol_feas;
+  double tol_step;
+  int32_t n_final_fix;
+  int32_t renormalize_quaternion; /* state_post_update hook present (rocket_problem.hpp:86-92) */
+  int32_t final_fix_idx[PTOPT_NX];
+  int32_t reserved_;
+  double final_fix_val[PTOPT_NX];
+  double e_cost[PTOPT_NX];
+} ptopt_problem_desc;
+
+/* Shape + shared data of a batch of pipg::Subproblem<NX,NU>
+ * (proj/include/ptopt/pipg.hpp:43-96).  Dimensions are run-time values inside
+ * the fixed capacities, exactly as in the reference. */
+typedef struct ptopt_subproblem_shape {
+  int32_t n_x;   /* 1..15 */
+  int32_t n_u;   /* 1..7  */
+  int32_t nodes; /* >= 2  */
+  int32_t n_init_fix;
+  int32_t n_final_fix;
+  int32_t reserved_;
+  int32_t init_fix_idx[PTOPT_NX];
+  int32_t final_fix_idx[PTOPT_NX];
+  double e_y[PTOPT_NX];
+  double e_cost[PTOPT_NX];
+  double w_cost;
+  double w_prox;
+  double w_ep;
+} ptopt_subproblem_shape;
+
+/* Per-instance arrays of a batch of subproblems; M = nodes-1.  All [B][...]. */
+typedef struct ptopt_subproblem_arrays {
+  const double* A_minus;       /* [B][M][n_x][n_x]                          */
+  const double* A_plus;        /* [B][M][n_x][n_x] or NULL meaning -I       */
+  const double* B_minus;       /* [B][M][n_x][n_u]                          */
+  const double* B_plus;        /* [B][M][n_x][n_u]                          */
+  const double* w;             /* [B][M][n_x]                               */
+  const double* eps_relax;     /* [B][M]                                    */
+  const double* u_min;         /* [B][nodes][n_u]  (+-inf allowed)          */
+  const double* u_max;         /* [B][nodes][n_u]                           */
+  const double* init_fix_val;  /* [B][n_init_fix]                           */
+  const double* final_fix_val; /* [B][n_final_fix]                          */
+} ptopt_subproblem_arrays;
+
+/* pipg::Workspace warm start / solution groups (proj/include/ptopt/pipg.hpp:100-141). */
+typedef struct ptopt_workspace_arrays {
+  double* x;          /* [B][nodes][n_x] */
+  double* u;          /* [B][nodes][n_u] */
+  double* vc_pos;     /* [B][M][n_x]     */
+  double* vc_neg;     /* [B][M][n_x]     */
+  double* dyn_dual;   /* [B][M][n_x]     */
+  double* relax_dual; /* [B][M]          */
+} ptopt_workspace_arrays;
+
+typedef struct ptopt_cuda_handle ptopt_cuda_handle;
+
+/* ---- library ---------------------------------------------------------- */
+
+int ptopt_cuda_abi_version(void);
+/* Thread-local description of the last call-level error on this thread. */
+const char* ptopt_cuda_last_error(void);
+/* Number of kernel launches issued through `h` since creation (graph nodes
+ * count once per graph launch). */
+int64_t ptopt_cuda_launch_count(const ptopt_cuda_handle* h);
+
+/* Creates a solver handle for one problem description on one device.
+ * Replaces constructing ScpProblem<Rocket6DoF> + Grid
+ * (proj/include/ptopt/scp.hpp:73-121, proj/include/ptopt/trajectory.hpp:11-34).
+ * `tau` = grid nodes [nodes] (strictly increasing, tau[0]=0, tau[nodes-1]=1),
+ * or NULL for Grid::uniform(nodes).  `stream` = a cudaStream_t to run on, or
+ * NULL for a private non-blocking stream owned by the handle. */
+int ptopt_cuda_create(const ptopt_problem_desc* desc, const double* tau, int device, void* stream,
+                      ptopt_cuda_handle** out);
+int ptopt_cuda_destroy(ptopt_cuda_handle* h);
+/* Blocks until all work enqueued on the handle's stream has finished. */
+int ptopt_cuda_synchronize(ptopt_cuda_handle* h);
+
+/* ---- exact discretization --------------------------------------------- */
+
+/* Batched linearize_all (proj/include/ptopt/discretizer.hpp:191-232), i.e.
+ * propagate_interval (discretizer.hpp:82-149) over every interval of every
+ * instance.  x [B][nodes][15], u [B][nodes][7] ->
+ * A [B][M][15][15], Bm/Bp [B][M][15][7], w/x_end [B][M][15].
+ * status[b] != 0 marks the FIRST failing interval of instance b (the
+ * reference throws from the lowest interval index) and fail_index[b] holds it;
+ * blocks of a failed instance are unspecified. */
+int ptopt_cuda_linearize_batch(ptopt_cuda_handle* h, int batch, const double* x, const double* u,
+                               double* A, double* Bm, double* Bp, double* w, double* x_end,
+                               int32_t* status, int32_t* fail_index);
+int ptopt_cuda_linearize_batch_dev(ptopt_cuda_handle* h, int batch, const double* x,
+                                   const double* u, double* A, double* Bm, double* Bp, double* w,
+                                   double* x_end, int32_t* status, int32_t* fail_index);
+
+/* ---- scaled subproblem assembly ---------------------------------------- */
+
+/* Batched assemble_subproblem (proj/include/ptopt/scp.hpp:139-217) for the
+ * handle's problem: blocks + iterate -> scaled Subproblem arrays.
+ * init_state [B][14]; outputs: A_minus [B][M][15][15] (A_plus is -I and not
+ * materialised), B_minus/B_plus [B][M][15][7], w_hat [B][M][15],
+ * eps_relax [B][M], u_min/u_max [B][nodes][7], init_fix_val [B][15],
+ * final_fix_val [B][n_final_fix]. */
+int ptopt_cuda_assemble_batch(ptopt_cuda_handle* h, int batch, const double* init_state,
+                              const double* x, const double* u, const double* A, const double* Bm,
+                              const double* Bp, const double* x_end, double* A_minus,
+                              double* B_minus, double* B_plus, double* w_hat, double* eps_relax,
+                              double* u_min, double* u_max, double* init_fix_val,
+                              double* final_fix_val);
+/* Fills `shape` with the subproblem shape assemble_subproblem produces for the
+ * handle's problem (n_x=15, n_u=7, fix index lists, e_y, scaled e_cost, weights). */
+int ptopt_cuda_subproblem_shape(const ptopt_cuda_handle* h, ptopt_subproblem_shape* shape);
+
+/* ---- power iteration ---------------------------------------------------- */
+
+/* Batched pipg::power_iteration_custom (proj/include/ptopt/pipg.hpp:206-292).
+ * Seeds: seed_x [B][nodes][n_x], seed_u [B][nodes][n_u], seed_vcp/seed_vcn
+ * [B][M][n_x].  sigma[b] = (1+eps_buff) * estimate; trips[b] = iterations run
+ * (may be NULL).  status[b] = PTOPT_ST_POWER_SEED_ZERO for an all-zero seed. */
+int ptopt_cuda_power_iteration_batch(ptopt_cuda_handle* h, int batch,
+                                     const ptopt_subproblem_shape* shape,
+                                     const ptopt_subproblem_arrays* sp, const double* seed_x,
+                                     const double* seed_u, const double* seed_vcp,
+                                     const double* seed_vcn, double eps_abs, double eps_rel,
+                                     double eps_buff, int j_max, double* sigma, int32_t* trips,
+                                     int32_t* status);
+int ptopt_cuda_power_iteration_batch_dev(ptopt_cuda_handle* h, int batch,
+                                         const ptopt_subproblem_shape* shape,
+                                         const ptopt_subproblem_arrays* sp, const double* seed_x,
+                                         const double* seed_u, const double* seed_vcp,
+                                         const double* seed_vcn, double eps_abs, double eps_rel,
+                                         double eps_buff, int j_max, double* sigma, int32_t* trips,
+                                         int32_t* status);
+
+/* ---- customized PIPG ---------------------------------------------------- */
+
+/* Batched pipg::pipg_custom (proj/include/ptopt/pipg.hpp:350-497).  `ws` holds
+ * the warm start on entry and the solution (the *_cur groups, pipg.hpp:490-495)
+ * on return; sigma [B] is Workspace::sigma.  iterations [B], converged [B]
+ * mirror PipgResult (pipg.hpp:342-345).  status/fail_index report
+ * SolverDiverged{j}. */
+int ptopt_cuda_pipg_batch(ptopt_cuda_handle* h, int batch, const ptopt_subproblem_shape* shape,
+                          const ptopt_subproblem_arrays* sp, const ptopt_pipg_config* cfg,
+                          const double* sigma, const ptopt_workspace_arrays* ws,
+                          int32_t* iterations, uint8_t* converged, int32_t* status,
+                          int32_t* fail_index);
+int ptopt_cuda_pipg_batch_dev(ptopt_cuda_handle* h, int batch, const ptopt_subproblem_shape* shape,
+                              const ptopt_subproblem_arrays* sp, const ptopt_pipg_config* cfg,
+                              const double* sigma, const ptopt_workspace_arrays* ws,
+                              int32_t* iterations, uint8_t* converged, int32_t* status,
+                              int32_t* fail_index);
+
+/* ---- SCP loop ------------------------------------------------------------ */
+
+/* Batched scp_solve (proj/include/ptopt/scp.hpp:256-364) for the handle's
+ * problem, the whole loop on the device under one CUDA graph.
+ * Inputs: init_state [B][14] (ScpProblem::init_state), x_guess [B][nodes][15],
+ * u_guess [B][nodes][7], rng_seed [B] (ScpProblem::rng_seed).
+ * Outputs: x_out/u_out (ScpResult::iterate), scp_iterations [B], converged [B],
+ * final_defect_inf [B], history [B][max_iters][5] (rows past scp_iterations are
+ * zero; pipg_iterations stored as a double), power_trips [B][max_iters] (may be
+ * NULL; extra diagnostic the reference does not expose), status/fail_index [B]. */
+int ptopt_cuda_scp_solve_batch(ptopt_cuda_handle* h, int batch, const double* init_state,
+                               const double* x_guess, const double* u_guess,
+                               const uint64_t* rng_seed, double* x_out, double* u_out,
+                               int32_t* scp_iterations, uint8_t* converged,
+                               double* final_defect_inf, double* history, int32_t* power_trips,
+                               int32_t* status, int32_t* fail_index);
+int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double* init_state,
+                                   const double* x_guess, const double* u_guess,
+                                   const uint64_t* rng_seed, double* x_out, double* u_out,
+                                   int32_t* scp_iterations, uint8_t* converged,
+                                   double* final_defect_inf, double* history, int32_t* power_trips,
+                                   int32_t* status, int32_t* fail_index);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PTOPT_CUDA_H_ */

@@ -1,0 +1,913 @@
+// capi.cu — the C-ABI of include/ptopt_cuda.h: handle, device buffers, argument checking,
+// host<->device staging, kernel dispatch, and the CUDA graph of the SCP loop.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "model_const.hpp"
+#include "ptopt_cuda.h"
+
+using namespace ptopt_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define PT_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e__ = (expr);                                                          \
+    if (e__ != cudaSuccess)                                                            \
+      return fail(PTOPT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (want == 0) want = 8;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+enum BufId {
+  // staging for host-pointer entry points and the stand-alone ops
+  B_X, B_U, B_A, B_BM, B_BP, B_W, B_XEND, B_STATUS, B_FAILIDX, B_FAILKEY, B_INIT,
+  B_AM, B_AP, B_BMH, B_BPH, B_WH, B_EPS, B_UMIN, B_UMAX, B_INITVAL, B_FINALVAL,
+  B_SEEDX, B_SEEDU, B_SEEDP, B_SEEDN, B_SIGMA, B_TRIPS, B_ITERS, B_CONV,
+  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR,
+  // SCP loop state (separate so a stand-alone call never disturbs a captured graph)
+  S_ZX, S_ZU, S_INIT, S_SEED, S_A, S_BM, S_BP, S_W, S_XEND, S_AM, S_BMH, S_BPH, S_WH, S_EPS,
+  S_UMIN, S_UMAX, S_INITVAL, S_FINALVAL, S_SEEDX, S_SEEDU, S_WSX, S_WSU, S_WSP, S_WSN, S_WSD,
+  S_WSR, S_SIGMA, S_PITERS, S_FAILKEY, S_ACTIVE, S_CONV, S_SOLVES, S_LASTSTEP, S_FDEF, S_HIST,
+  S_TRIPS, S_STATUS, S_FAILIDX,
+  kNumBufs
+};
+
+}  // namespace
+
+struct ptopt_cuda_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ptopt_problem_desc desc{};
+  std::vector<double> tau;
+  double* d_tau = nullptr;
+  ModelConst model{};
+  ScpConst scp{};
+  SubShape rocket_shape{};
+  int64_t launches = 0;
+  DevBuf buf[kNumBufs];
+  cudaGraphExec_t scp_graph = nullptr;
+  int scp_graph_batch = 0;
+  int scp_graph_kernels = 0;
+  int scp_capacity = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (cudaSetDevice(dev) != cudaSuccess) ok = false;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool pipg_cfg_valid(const ptopt_pipg_config& c) {  // PipgConfig::validate, pipg.hpp:31-37
+  return c.omega > 0.0 && c.rho > 0.0 && c.rho < 2.0 && c.j_check >= 1 && c.j_max >= 1 &&
+         c.eps_buff >= 0.0;
+}
+
+int check_shape(const ptopt_subproblem_shape* s, SubShape& out) {
+  if (!s) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null subproblem shape");
+  // Subproblem::resize, pipg.hpp:69-71
+  if (s->n_x < 1 || s->n_x > PTOPT_NX || s->n_u < 1 || s->n_u > PTOPT_NU || s->nodes < 2)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "subproblem: bad dimensions");
+  if (s->n_init_fix < 0 || s->n_init_fix > PTOPT_NX || s->n_final_fix < 0 ||
+      s->n_final_fix > PTOPT_NX)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "subproblem: bad boundary row count");
+  out.nx = s->n_x;
+  out.nu = s->n_u;
+  out.n = s->nodes;
+  out.n_init_fix = s->n_init_fix;
+  out.n_final_fix = s->n_final_fix;
+  for (int i = 0; i < PTOPT_NX; ++i) {
+    out.init_fix_idx[i] = s->init_fix_idx[i];
+    out.final_fix_idx[i] = s->final_fix_idx[i];
+    out.e_y[i] = s->e_y[i];
+    out.e_cost[i] = s->e_cost[i];
+  }
+  for (int i = 0; i < s->n_init_fix; ++i)
+    if (s->init_fix_idx[i] < 0 || s->init_fix_idx[i] >= s->n_x)
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "subproblem: initial row index out of range");
+  for (int i = 0; i < s->n_final_fix; ++i)
+    if (s->final_fix_idx[i] < 0 || s->final_fix_idx[i] >= s->n_x)
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "subproblem: final row index out of range");
+  out.w_cost = s->w_cost;
+  out.w_prox = s->w_prox;
+  out.w_ep = s->w_ep;
+  return PTOPT_OK;
+}
+
+int check_smem(ptopt_cuda_handle* h, size_t bytes) {
+  int limit = 0;
+  PT_CUDA(cudaDeviceGetAttribute(&limit, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  if (bytes > (size_t)limit)
+    return fail(PTOPT_ERR_UNSUPPORTED, "subproblem too large for one CTA's shared memory (" +
+                                           std::to_string(bytes) + " > " + std::to_string(limit) +
+                                           " bytes)");
+  return PTOPT_OK;
+}
+
+template <class T>
+int upload(ptopt_cuda_handle* h, BufId id, const T* host, size_t count, const T** dev_out) {
+  if (!host) {
+    *dev_out = nullptr;
+    return PTOPT_OK;
+  }
+  PT_CUDA(h->buf[id].ensure(count * sizeof(T)));
+  PT_CUDA(cudaMemcpyAsync(h->buf[id].p, host, count * sizeof(T), cudaMemcpyHostToDevice,
+                          h->stream));
+  *dev_out = h->buf[id].as<T>();
+  return PTOPT_OK;
+}
+
+template <class T>
+int device_out(ptopt_cuda_handle* h, BufId id, size_t count, T** dev_out) {
+  PT_CUDA(h->buf[id].ensure(count * sizeof(T)));
+  *dev_out = h->buf[id].as<T>();
+  return PTOPT_OK;
+}
+
+template <class T>
+int download(ptopt_cuda_handle* h, T* host, const T* dev, size_t count) {
+  if (!host) return PTOPT_OK;
+  PT_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, h->stream));
+  return PTOPT_OK;
+}
+
+#define PT_TRY(expr)            \
+  do {                          \
+    int rc__ = (expr);          \
+    if (rc__ != PTOPT_OK) return rc__; \
+  } while (0)
+
+void fill_scp_const(const ptopt_problem_desc& d, ScpConst& c) {
+  c.nodes = d.nodes;
+  c.max_iters = d.max_iters;
+  c.n_final_fix = d.n_final_fix;
+  c.renorm_quat = d.renormalize_quaternion;
+  for (int i = 0; i < kNX; ++i) {
+    c.final_fix_idx[i] = d.final_fix_idx[i];
+    c.final_fix_val[i] = d.final_fix_val[i];
+    c.px[i] = d.px[i];
+    c.px_inv[i] = 1.0 / d.px[i];
+    c.e_cost[i] = d.e_cost[i];
+  }
+  for (int i = 0; i < kNU; ++i) {
+    c.pu[i] = d.pu[i];
+    c.pu_inv[i] = 1.0 / d.pu[i];
+  }
+  c.w_cost = d.w_cost;
+  c.w_ep = d.w_ep;
+  c.epsilon_relax = d.epsilon_relax;
+  c.s_min = d.s_min;
+  c.s_max = d.s_max;
+  c.tol_feas = d.tol_feas;
+  c.tol_step = d.tol_step;
+}
+
+void fill_rocket_shape(const ptopt_problem_desc& d, SubShape& s) {  // scp.hpp:160-215
+  std::memset(&s, 0, sizeof s);
+  s.nx = kNX;
+  s.nu = kNU;
+  s.n = d.nodes;
+  s.n_init_fix = kNX;
+  s.n_final_fix = d.n_final_fix;
+  for (int i = 0; i < kNX; ++i) s.init_fix_idx[i] = i;
+  for (int i = 0; i < d.n_final_fix; ++i) s.final_fix_idx[i] = d.final_fix_idx[i];
+  s.e_y[kNX - 1] = 1.0;
+  for (int i = 0; i < kNX; ++i) s.e_cost[i] = d.px[i] * d.e_cost[i];
+  s.w_cost = d.w_cost;
+  s.w_prox = d.w_prox;
+  s.w_ep = d.w_ep;
+}
+
+int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
+  PT_TRY(check_smem(h, pipg_generic_smem(a.shape, solver_generic_threads(a.shape))));
+  PT_CUDA(configure_solver_generic(a.shape));
+  PT_CUDA(launch_power_generic(a, h->stream));
+  h->launches += 1;
+  return PTOPT_OK;
+}
+
+int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
+  PT_TRY(check_smem(h, pipg_generic_smem(a.shape, solver_generic_threads(a.shape))));
+  PT_CUDA(configure_solver_generic(a.shape));
+  PT_CUDA(launch_pipg_generic(a, h->stream));
+  h->launches += 1;
+  return PTOPT_OK;
+}
+
+LinearizeArgs linearize_args(ptopt_cuda_handle* h, int batch, const double* x, const double* u,
+                             double* A, double* Bm, double* Bp, double* w, double* x_end,
+                             int* fail_key, const unsigned char* active) {
+  LinearizeArgs a;
+  a.model = h->model;
+  a.batch = batch;
+  a.nodes = h->desc.nodes;
+  a.steps = h->desc.integrator_steps;
+  a.tau = h->d_tau;
+  a.x = x;
+  a.u = u;
+  a.A = A;
+  a.Bm = Bm;
+  a.Bp = Bp;
+  a.w = w;
+  a.x_end = x_end;
+  a.fail_key = fail_key;
+  a.active = active;
+  return a;
+}
+
+int ensure_scp_state(ptopt_cuda_handle* h, int batch, ScpState& s) {
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
+  const size_t nf = h->desc.n_final_fix > 0 ? (size_t)h->desc.n_final_fix : 1;
+  const size_t mi = (size_t)h->desc.max_iters;
+  struct Req { BufId id; size_t bytes; };
+  const Req reqs[] = {
+      {S_ZX, B * n * kNX * 8}, {S_ZU, B * n * kNU * 8}, {S_INIT, B * kNXI * 8}, {S_SEED, B * 8},
+      {S_A, B * m * kNX * kNX * 8}, {S_BM, B * m * kNX * kNU * 8}, {S_BP, B * m * kNX * kNU * 8},
+      {S_W, B * m * kNX * 8}, {S_XEND, B * m * kNX * 8}, {S_AM, B * m * kNX * kNX * 8},
+      {S_BMH, B * m * kNX * kNU * 8}, {S_BPH, B * m * kNX * kNU * 8}, {S_WH, B * m * kNX * 8},
+      {S_EPS, B * m * 8}, {S_UMIN, B * n * kNU * 8}, {S_UMAX, B * n * kNU * 8},
+      {S_INITVAL, B * kNX * 8}, {S_FINALVAL, B * nf * 8}, {S_SEEDX, B * n * kNX * 8},
+      {S_SEEDU, B * n * kNU * 8}, {S_WSX, B * n * kNX * 8}, {S_WSU, B * n * kNU * 8},
+      {S_WSP, B * m * kNX * 8}, {S_WSN, B * m * kNX * 8}, {S_WSD, B * m * kNX * 8},
+      {S_WSR, B * m * 8}, {S_SIGMA, B * 8}, {S_PITERS, B * 4}, {S_FAILKEY, B * 4},
+      {S_ACTIVE, B}, {S_CONV, B}, {S_SOLVES, B * 4}, {S_LASTSTEP, B * 8}, {S_FDEF, B * 8},
+      {S_HIST, B * mi * 5 * 8}, {S_TRIPS, B * mi * 4}, {S_STATUS, B * 4}, {S_FAILIDX, B * 4}};
+  bool grew = false;
+  for (const Req& r : reqs) {
+    if (r.bytes > h->buf[r.id].bytes || !h->buf[r.id].p) grew = true;
+    PT_CUDA(h->buf[r.id].ensure(r.bytes));
+  }
+  if (grew && h->scp_graph) {  // pointers changed: the captured graph is stale
+    cudaGraphExecDestroy(h->scp_graph);
+    h->scp_graph = nullptr;
+    h->scp_graph_batch = 0;
+  }
+  auto D = [&](BufId id) { return h->buf[id].as<double>(); };
+  s.zx = D(S_ZX); s.zu = D(S_ZU); s.init_state = D(S_INIT);
+  s.rng_seed = h->buf[S_SEED].as<unsigned long long>();
+  s.A = D(S_A); s.Bm = D(S_BM); s.Bp = D(S_BP); s.w = D(S_W); s.x_end = D(S_XEND);
+  s.Am = D(S_AM); s.Bmh = D(S_BMH); s.Bph = D(S_BPH); s.wh = D(S_WH); s.eps = D(S_EPS);
+  s.umin = D(S_UMIN); s.umax = D(S_UMAX); s.init_val = D(S_INITVAL); s.final_val = D(S_FINALVAL);
+  s.seed_x = D(S_SEEDX); s.seed_u = D(S_SEEDU);
+  s.ws.x = D(S_WSX); s.ws.u = D(S_WSU); s.ws.vc_pos = D(S_WSP); s.ws.vc_neg = D(S_WSN);
+  s.ws.dyn_dual = D(S_WSD); s.ws.relax_dual = D(S_WSR);
+  s.sigma = D(S_SIGMA);
+  s.pipg_iters = h->buf[S_PITERS].as<int>();
+  s.fail_key = h->buf[S_FAILKEY].as<int>();
+  s.active = h->buf[S_ACTIVE].as<unsigned char>();
+  s.converged = h->buf[S_CONV].as<unsigned char>();
+  s.solves = h->buf[S_SOLVES].as<int>();
+  s.last_step = D(S_LASTSTEP);
+  s.final_defect = D(S_FDEF);
+  s.history = D(S_HIST);
+  s.power_trips = h->buf[S_TRIPS].as<int>();
+  s.status = h->buf[S_STATUS].as<int>();
+  s.fail_index = h->buf[S_FAILIDX].as<int>();
+  return PTOPT_OK;
+}
+
+/// Enqueues the whole SCP loop for `batch` instances on the handle's stream (used under
+/// stream capture to build the graph).  Returns the number of kernels enqueued.
+int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* kernels_out) {
+  ScpArgs sa;
+  sa.c = h->scp;
+  sa.s = st;
+  sa.batch = batch;
+  int kernels = 0;
+  launch_scp_init(sa, h->stream);
+  ++kernels;
+
+  PowerArgs pa;
+  pa.shape = h->rocket_shape;
+  pa.sp = SubArrays{st.Am, nullptr, st.Bmh, st.Bph, st.wh, st.eps, st.umin, st.umax,
+                    st.init_val, st.final_val};
+  pa.batch = batch;
+  pa.seed_x = st.seed_x;
+  pa.seed_u = st.seed_u;
+  pa.seed_vcp = st.ws.vc_pos;
+  pa.seed_vcn = st.ws.vc_neg;
+  pa.eps_abs = h->desc.power_eps_abs;
+  pa.eps_rel = h->desc.power_eps_rel;
+  pa.eps_buff = h->desc.pipg.eps_buff;
+  pa.j_max = h->desc.power_j_max;
+  pa.sigma = st.sigma;
+  pa.trips = st.power_trips;
+  pa.trips_stride = h->desc.max_iters;
+  pa.trips_slot = st.solves;
+  pa.status = st.status;
+  pa.active = st.active;
+
+  PipgArgs ga;
+  ga.shape = h->rocket_shape;
+  ga.sp = pa.sp;
+  ga.batch = batch;
+  ga.omega = h->desc.pipg.omega;
+  ga.rho = h->desc.pipg.rho;
+  ga.eps_abs = h->desc.pipg.eps_abs;
+  ga.eps_rel = h->desc.pipg.eps_rel;
+  ga.j_max = h->desc.pipg.j_max;
+  ga.j_check = h->desc.pipg.j_check;
+  ga.sigma = st.sigma;
+  ga.ws = st.ws;
+  ga.iterations = st.pipg_iters;
+  ga.converged = nullptr;
+  ga.status = st.status;
+  ga.fail_index = st.fail_index;
+  ga.active = st.active;
+
+  const LinearizeArgs la = linearize_args(h, batch, st.zx, st.zu, st.A, st.Bm, st.Bp, st.w,
+                                          st.x_end, st.fail_key, st.active);
+  for (int it = 0; it <= h->desc.max_iters; ++it) {
+    launch_linearize(la, h->stream);
+    launch_scp_prepare(sa, h->stream);
+    kernels += 2;
+    if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
+    PT_CUDA(launch_power_generic(pa, h->stream));
+    PT_CUDA(launch_pipg_generic(ga, h->stream));
+    launch_scp_update(sa, h->stream);
+    kernels += 3;
+  }
+  PT_CUDA(cudaGetLastError());
+  *kernels_out = kernels;
+  return PTOPT_OK;
+}
+
+int ensure_scp_graph(ptopt_cuda_handle* h, int batch, const ScpState& st) {
+  if (h->scp_graph && h->scp_graph_batch == batch) return PTOPT_OK;
+  if (h->scp_graph) {
+    cudaGraphExecDestroy(h->scp_graph);
+    h->scp_graph = nullptr;
+  }
+  PT_TRY(check_smem(h, pipg_generic_smem(h->rocket_shape, solver_generic_threads(h->rocket_shape))));
+  PT_CUDA(configure_solver_generic(h->rocket_shape));
+  cudaGraph_t graph = nullptr;
+  PT_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int kernels = 0;
+  const int rc = enqueue_scp_loop(h, batch, st, &kernels);
+  cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+  if (rc != PTOPT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess)
+    return fail(PTOPT_ERR_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&h->scp_graph, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess)
+    return fail(PTOPT_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  h->scp_graph_batch = batch;
+  h->scp_graph_kernels = kernels;
+  return PTOPT_OK;
+}
+
+int scp_solve_common(ptopt_cuda_handle* h, int batch, const double* init_state,
+                     const double* x_guess, const double* u_guess, const uint64_t* rng_seed,
+                     double* x_out, double* u_out, int32_t* scp_iterations, uint8_t* converged,
+                     double* final_defect_inf, double* history, int32_t* power_trips,
+                     int32_t* status, int32_t* fail_index, cudaMemcpyKind in_kind,
+                     cudaMemcpyKind out_kind) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!init_state || !x_guess || !u_guess || !rng_seed)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp_solve: null input");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, mi = (size_t)h->desc.max_iters;
+  ScpState st;
+  PT_TRY(ensure_scp_state(h, batch, st));
+  PT_TRY(ensure_scp_graph(h, batch, st));
+  PT_CUDA(cudaMemcpyAsync(st.zx, x_guess, B * n * kNX * 8, in_kind, h->stream));
+  PT_CUDA(cudaMemcpyAsync(st.zu, u_guess, B * n * kNU * 8, in_kind, h->stream));
+  PT_CUDA(cudaMemcpyAsync(const_cast<double*>(st.init_state), init_state, B * kNXI * 8, in_kind,
+                          h->stream));
+  PT_CUDA(cudaMemcpyAsync(const_cast<unsigned long long*>(st.rng_seed), rng_seed, B * 8, in_kind,
+                          h->stream));
+  PT_CUDA(cudaGraphLaunch(h->scp_graph, h->stream));
+  h->launches += h->scp_graph_kernels;
+  auto out = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, out_kind, h->stream);
+  };
+  PT_CUDA(out(x_out, st.zx, B * n * kNX * 8));
+  PT_CUDA(out(u_out, st.zu, B * n * kNU * 8));
+  PT_CUDA(out(scp_iterations, st.solves, B * 4));
+  PT_CUDA(out(converged, st.converged, B));
+  PT_CUDA(out(final_defect_inf, st.final_defect, B * 8));
+  PT_CUDA(out(history, st.history, B * mi * 5 * 8));
+  PT_CUDA(out(power_trips, st.power_trips, B * mi * 4));
+  PT_CUDA(out(status, st.status, B * 4));
+  PT_CUDA(out(fail_index, st.fail_index, B * 4));
+  if (out_kind == cudaMemcpyDeviceToHost) PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ptopt_cuda_abi_version(void) { return PTOPT_ABI_VERSION; }
+
+const char* ptopt_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int64_t ptopt_cuda_launch_count(const ptopt_cuda_handle* h) { return h ? h->launches : 0; }
+
+int ptopt_cuda_create(const ptopt_problem_desc* desc, const double* tau, int device, void* stream,
+                      ptopt_cuda_handle** out) {
+  if (!desc || !out) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  const ptopt_problem_desc& d = *desc;
+  // Grid (trajectory.hpp:14-21) and ScpProblem::validate (scp.hpp:111-120)
+  if (d.nodes < 2) return fail(PTOPT_ERR_INVALID_ARGUMENT, "grid needs at least two nodes");
+  std::vector<double> grid((size_t)d.nodes);
+  if (tau) {
+    for (int k = 0; k < d.nodes; ++k) grid[k] = tau[k];
+    if (grid.front() != 0.0 || grid.back() != 1.0)
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "grid must start at 0 and end at 1");
+    for (int k = 1; k < d.nodes; ++k)
+      if (!(grid[k] > grid[k - 1]))
+        return fail(PTOPT_ERR_INVALID_ARGUMENT, "grid nodes must be strictly increasing");
+  } else {
+    for (int k = 0; k < d.nodes; ++k) grid[k] = (double)k / (d.nodes - 1);
+    grid.front() = 0.0;
+    grid.back() = 1.0;
+  }
+  if (!(d.w_cost >= 0.0)) return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp.w_cost must be >= 0");
+  if (!(d.w_prox > 0.0)) return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp.w_prox must be > 0");
+  if (!(d.w_ep > 0.0)) return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp.w_ep must be > 0");
+  if (!(d.epsilon_relax > 0.0))
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp.epsilon_relax must be > 0");
+  if (!pipg_cfg_valid(d.pipg)) return fail(PTOPT_ERR_INVALID_ARGUMENT, "invalid pipg config");
+  if (!(d.s_min > 0.0) || !(d.s_min <= d.s_max))
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp: need 0 < s_min <= s_max");
+  if (d.max_iters < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp.max_iters must be >= 1");
+  if (d.integrator_steps < 1)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "grid.integrator_substeps must be >= 1");
+  if (d.power_j_max < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg.power_j_max must be >= 1");
+  if (d.n_final_fix < 0 || d.n_final_fix > PTOPT_NX)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp: bad final boundary row count");
+  for (int i = 0; i < d.n_final_fix; ++i)
+    if (d.final_fix_idx[i] < 0 || d.final_fix_idx[i] >= PTOPT_NX)
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "scp: final boundary index out of range");
+  for (int i = 0; i < PTOPT_NX; ++i)  // assemble_subproblem, scp.hpp:155-158
+    if (!(d.px[i] > 0.0))
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "assemble_subproblem: nonpositive state scale");
+  for (int i = 0; i < PTOPT_NU; ++i)
+    if (!(d.pu[i] > 0.0))
+      return fail(PTOPT_ERR_INVALID_ARGUMENT, "assemble_subproblem: nonpositive control scale");
+
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count < 1)
+    return fail(PTOPT_ERR_CUDA, std::string("no CUDA device: ") +
+                                    (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0"));
+  if (device < 0 || device >= count) return fail(PTOPT_ERR_INVALID_ARGUMENT, "bad device index");
+  int major = 0;
+  PT_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10)
+    return fail(PTOPT_ERR_CUDA, "device is not sm_100 (this library ships sm_100a code only)");
+
+  ptopt_cuda_handle* h = new (std::nothrow) ptopt_cuda_handle();
+  if (!h) return fail(PTOPT_ERR_ALLOC, "out of host memory");
+  h->device = device;
+  h->desc = d;
+  h->tau = grid;
+  if (!make_model_const(d.vehicle, h->model)) {
+    delete h;
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "inverse3: singular matrix");
+  }
+  fill_scp_const(d, h->scp);
+  fill_rocket_shape(d, h->rocket_shape);
+  DeviceGuard guard(device);
+  if (!guard.ok) {
+    delete h;
+    return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  }
+  if (stream) {
+    h->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete h;
+      return fail(PTOPT_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    h->own_stream = true;
+  }
+  e = cudaMalloc(&h->d_tau, sizeof(double) * grid.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(h->d_tau, grid.data(), sizeof(double) * grid.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    ptopt_cuda_destroy(h);
+    return fail(PTOPT_ERR_CUDA, std::string("grid upload: ") + cudaGetErrorString(e));
+  }
+  *out = h;
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
+  if (!h) return PTOPT_OK;
+  DeviceGuard guard(h->device);
+  cudaStreamSynchronize(h->stream);
+  if (h->scp_graph) cudaGraphExecDestroy(h->scp_graph);
+  for (DevBuf& b : h->buf) b.release();
+  if (h->d_tau) cudaFree(h->d_tau);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_synchronize(ptopt_cuda_handle* h) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  DeviceGuard guard(h->device);
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+// ---- exact discretization -------------------------------------------------------------
+
+int ptopt_cuda_linearize_batch_dev(ptopt_cuda_handle* h, int batch, const double* x,
+                                   const double* u, double* A, double* Bm, double* Bp, double* w,
+                                   double* x_end, int32_t* status, int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!x || !u || !A || !Bm || !Bp || !w || !x_end)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "linearize: null array");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  int* fail_key = nullptr;
+  PT_TRY(device_out(h, B_FAILKEY, (size_t)batch, &fail_key));
+  launch_init_fail_key(fail_key, batch, h->stream);
+  launch_linearize(linearize_args(h, batch, x, u, A, Bm, Bp, w, x_end, fail_key, nullptr),
+                   h->stream);
+  h->launches += 2;
+  if (status || fail_index) {
+    launch_decode_fail_key(fail_key, batch, status, fail_index, h->stream);
+    h->launches += 1;
+  }
+  PT_CUDA(cudaGetLastError());
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_linearize_batch(ptopt_cuda_handle* h, int batch, const double* x, const double* u,
+                               double* A, double* Bm, double* Bp, double* w, double* x_end,
+                               int32_t* status, int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!x || !u || !A || !Bm || !Bp || !w || !x_end)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "linearize: null array");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
+  const double *dx, *du;
+  double *dA, *dBm, *dBp, *dw, *dxe;
+  int *dst, *dfi;
+  PT_TRY(upload(h, B_X, x, B * n * kNX, &dx));
+  PT_TRY(upload(h, B_U, u, B * n * kNU, &du));
+  PT_TRY(device_out(h, B_A, B * m * kNX * kNX, &dA));
+  PT_TRY(device_out(h, B_BM, B * m * kNX * kNU, &dBm));
+  PT_TRY(device_out(h, B_BP, B * m * kNX * kNU, &dBp));
+  PT_TRY(device_out(h, B_W, B * m * kNX, &dw));
+  PT_TRY(device_out(h, B_XEND, B * m * kNX, &dxe));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
+  PT_TRY(ptopt_cuda_linearize_batch_dev(h, batch, dx, du, dA, dBm, dBp, dw, dxe, dst, dfi));
+  PT_TRY(download(h, A, dA, B * m * kNX * kNX));
+  PT_TRY(download(h, Bm, dBm, B * m * kNX * kNU));
+  PT_TRY(download(h, Bp, dBp, B * m * kNX * kNU));
+  PT_TRY(download(h, w, dw, B * m * kNX));
+  PT_TRY(download(h, x_end, dxe, B * m * kNX));
+  PT_TRY(download(h, status, dst, B));
+  PT_TRY(download(h, fail_index, dfi, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+// ---- scaled subproblem assembly -------------------------------------------------------
+
+int ptopt_cuda_subproblem_shape(const ptopt_cuda_handle* h, ptopt_subproblem_shape* shape) {
+  if (!h || !shape) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null argument");
+  const SubShape& s = h->rocket_shape;
+  std::memset(shape, 0, sizeof *shape);
+  shape->n_x = s.nx;
+  shape->n_u = s.nu;
+  shape->nodes = s.n;
+  shape->n_init_fix = s.n_init_fix;
+  shape->n_final_fix = s.n_final_fix;
+  for (int i = 0; i < kNX; ++i) {
+    shape->init_fix_idx[i] = s.init_fix_idx[i];
+    shape->final_fix_idx[i] = s.final_fix_idx[i];
+    shape->e_y[i] = s.e_y[i];
+    shape->e_cost[i] = s.e_cost[i];
+  }
+  shape->w_cost = s.w_cost;
+  shape->w_prox = s.w_prox;
+  shape->w_ep = s.w_ep;
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_assemble_batch(ptopt_cuda_handle* h, int batch, const double* init_state,
+                              const double* x, const double* u, const double* A, const double* Bm,
+                              const double* Bp, const double* x_end, double* A_minus,
+                              double* B_minus, double* B_plus, double* w_hat, double* eps_relax,
+                              double* u_min, double* u_max, double* init_fix_val,
+                              double* final_fix_val) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!init_state || !x || !u || !A || !Bm || !Bp || !x_end)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "assemble: null input");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
+  const size_t nf = h->desc.n_final_fix > 0 ? (size_t)h->desc.n_final_fix : 1;
+  const double *dinit, *dx, *du, *dA, *dBm, *dBp, *dxe;
+  double *oAm, *oBm, *oBp, *ow, *oeps, *oumin, *oumax, *oiv, *ofv;
+  PT_TRY(upload(h, B_INIT, init_state, B * kNXI, &dinit));
+  PT_TRY(upload(h, B_X, x, B * n * kNX, &dx));
+  PT_TRY(upload(h, B_U, u, B * n * kNU, &du));
+  PT_TRY(upload(h, B_A, A, B * m * kNX * kNX, &dA));
+  PT_TRY(upload(h, B_BM, Bm, B * m * kNX * kNU, &dBm));
+  PT_TRY(upload(h, B_BP, Bp, B * m * kNX * kNU, &dBp));
+  PT_TRY(upload(h, B_XEND, x_end, B * m * kNX, &dxe));
+  PT_TRY(device_out(h, B_AM, B * m * kNX * kNX, &oAm));
+  PT_TRY(device_out(h, B_BMH, B * m * kNX * kNU, &oBm));
+  PT_TRY(device_out(h, B_BPH, B * m * kNX * kNU, &oBp));
+  PT_TRY(device_out(h, B_WH, B * m * kNX, &ow));
+  PT_TRY(device_out(h, B_EPS, B * m, &oeps));
+  PT_TRY(device_out(h, B_UMIN, B * n * kNU, &oumin));
+  PT_TRY(device_out(h, B_UMAX, B * n * kNU, &oumax));
+  PT_TRY(device_out(h, B_INITVAL, B * kNX, &oiv));
+  PT_TRY(device_out(h, B_FINALVAL, B * nf, &ofv));
+  launch_assemble(h->scp, batch, dinit, dx, du, dA, dBm, dBp, dxe, oAm, oBm, oBp, ow, oeps, oumin,
+                  oumax, oiv, ofv, h->stream);
+  h->launches += 1;
+  PT_CUDA(cudaGetLastError());
+  PT_TRY(download(h, A_minus, oAm, B * m * kNX * kNX));
+  PT_TRY(download(h, B_minus, oBm, B * m * kNX * kNU));
+  PT_TRY(download(h, B_plus, oBp, B * m * kNX * kNU));
+  PT_TRY(download(h, w_hat, ow, B * m * kNX));
+  PT_TRY(download(h, eps_relax, oeps, B * m));
+  PT_TRY(download(h, u_min, oumin, B * n * kNU));
+  PT_TRY(download(h, u_max, oumax, B * n * kNU));
+  PT_TRY(download(h, init_fix_val, oiv, B * kNX));
+  PT_TRY(download(h, final_fix_val, ofv, B * (size_t)h->desc.n_final_fix));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+// ---- power iteration ------------------------------------------------------------------
+
+int ptopt_cuda_power_iteration_batch_dev(ptopt_cuda_handle* h, int batch,
+                                         const ptopt_subproblem_shape* shape,
+                                         const ptopt_subproblem_arrays* sp, const double* seed_x,
+                                         const double* seed_u, const double* seed_vcp,
+                                         const double* seed_vcn, double eps_abs, double eps_rel,
+                                         double eps_buff, int j_max, double* sigma, int32_t* trips,
+                                         int32_t* status) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!sp || !seed_x || !seed_u || !seed_vcp || !seed_vcn || !sigma)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "power iteration: null argument");
+  if (!sp->A_minus || !sp->B_minus || !sp->B_plus)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "power iteration: null operator block");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  PowerArgs a;
+  PT_TRY(check_shape(shape, a.shape));
+  a.sp = SubArrays{sp->A_minus, sp->A_plus, sp->B_minus, sp->B_plus, sp->w, sp->eps_relax,
+                   sp->u_min, sp->u_max, sp->init_fix_val, sp->final_fix_val};
+  a.batch = batch;
+  a.seed_x = seed_x;
+  a.seed_u = seed_u;
+  a.seed_vcp = seed_vcp;
+  a.seed_vcn = seed_vcn;
+  a.eps_abs = eps_abs;
+  a.eps_rel = eps_rel;
+  a.eps_buff = eps_buff;
+  a.j_max = j_max;
+  a.sigma = sigma;
+  a.trips = trips;
+  a.trips_stride = 1;
+  a.trips_slot = nullptr;
+  a.status = status;
+  a.active = nullptr;
+  if (status) PT_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * (size_t)batch, h->stream));
+  return dispatch_power(h, a);
+}
+
+namespace {
+
+/// Uploads the per-instance arrays of a subproblem batch; returns device views.
+int upload_sub(ptopt_cuda_handle* h, int batch, const SubShape& s,
+               const ptopt_subproblem_arrays* sp, ptopt_subproblem_arrays* dev) {
+  const size_t B = (size_t)batch, n = (size_t)s.n, m = n - 1, nx = (size_t)s.nx, nu = (size_t)s.nu;
+  PT_TRY(upload(h, B_AM, sp->A_minus, B * m * nx * nx, &dev->A_minus));
+  PT_TRY(upload(h, B_AP, sp->A_plus, B * m * nx * nx, &dev->A_plus));
+  PT_TRY(upload(h, B_BMH, sp->B_minus, B * m * nx * nu, &dev->B_minus));
+  PT_TRY(upload(h, B_BPH, sp->B_plus, B * m * nx * nu, &dev->B_plus));
+  PT_TRY(upload(h, B_WH, sp->w, B * m * nx, &dev->w));
+  PT_TRY(upload(h, B_EPS, sp->eps_relax, B * m, &dev->eps_relax));
+  PT_TRY(upload(h, B_UMIN, sp->u_min, B * n * nu, &dev->u_min));
+  PT_TRY(upload(h, B_UMAX, sp->u_max, B * n * nu, &dev->u_max));
+  PT_TRY(upload(h, B_INITVAL, sp->init_fix_val, B * (size_t)s.n_init_fix, &dev->init_fix_val));
+  PT_TRY(upload(h, B_FINALVAL, sp->final_fix_val, B * (size_t)s.n_final_fix, &dev->final_fix_val));
+  return PTOPT_OK;
+}
+
+}  // namespace
+
+int ptopt_cuda_power_iteration_batch(ptopt_cuda_handle* h, int batch,
+                                     const ptopt_subproblem_shape* shape,
+                                     const ptopt_subproblem_arrays* sp, const double* seed_x,
+                                     const double* seed_u, const double* seed_vcp,
+                                     const double* seed_vcn, double eps_abs, double eps_rel,
+                                     double eps_buff, int j_max, double* sigma, int32_t* trips,
+                                     int32_t* status) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!sp || !seed_x || !seed_u || !seed_vcp || !seed_vcn || !sigma)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "power iteration: null argument");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  SubShape s;
+  PT_TRY(check_shape(shape, s));
+  const size_t B = (size_t)batch, n = (size_t)s.n, m = n - 1, nx = (size_t)s.nx, nu = (size_t)s.nu;
+  ptopt_subproblem_arrays dev{};
+  PT_TRY(upload_sub(h, batch, s, sp, &dev));
+  const double *dsx, *dsu, *dsp, *dsn;
+  double* dsig;
+  int *dtr, *dst;
+  PT_TRY(upload(h, B_SEEDX, seed_x, B * n * nx, &dsx));
+  PT_TRY(upload(h, B_SEEDU, seed_u, B * n * nu, &dsu));
+  PT_TRY(upload(h, B_SEEDP, seed_vcp, B * m * nx, &dsp));
+  PT_TRY(upload(h, B_SEEDN, seed_vcn, B * m * nx, &dsn));
+  PT_TRY(device_out(h, B_SIGMA, B, &dsig));
+  PT_TRY(device_out(h, B_TRIPS, B, &dtr));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(ptopt_cuda_power_iteration_batch_dev(h, batch, shape, &dev, dsx, dsu, dsp, dsn, eps_abs,
+                                              eps_rel, eps_buff, j_max, dsig, dtr, dst));
+  PT_TRY(download(h, sigma, dsig, B));
+  PT_TRY(download(h, trips, dtr, B));
+  PT_TRY(download(h, status, dst, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+// ---- customized PIPG ------------------------------------------------------------------
+
+int ptopt_cuda_pipg_batch_dev(ptopt_cuda_handle* h, int batch, const ptopt_subproblem_shape* shape,
+                              const ptopt_subproblem_arrays* sp, const ptopt_pipg_config* cfg,
+                              const double* sigma, const ptopt_workspace_arrays* ws,
+                              int32_t* iterations, uint8_t* converged, int32_t* status,
+                              int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!sp || !cfg || !sigma || !ws)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null argument");
+  if (!pipg_cfg_valid(*cfg)) return fail(PTOPT_ERR_INVALID_ARGUMENT, "invalid pipg config");
+  if (!sp->A_minus || !sp->B_minus || !sp->B_plus || !sp->w || !sp->eps_relax || !sp->u_min ||
+      !sp->u_max)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null subproblem array");
+  if (!ws->x || !ws->u || !ws->vc_pos || !ws->vc_neg || !ws->dyn_dual || !ws->relax_dual)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null workspace array");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  PipgArgs a;
+  PT_TRY(check_shape(shape, a.shape));
+  if ((a.shape.n_init_fix > 0 && !sp->init_fix_val) || (a.shape.n_final_fix > 0 && !sp->final_fix_val))
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null boundary values");
+  a.sp = SubArrays{sp->A_minus, sp->A_plus, sp->B_minus, sp->B_plus, sp->w, sp->eps_relax,
+                   sp->u_min, sp->u_max, sp->init_fix_val, sp->final_fix_val};
+  a.batch = batch;
+  a.omega = cfg->omega;
+  a.rho = cfg->rho;
+  a.eps_abs = cfg->eps_abs;
+  a.eps_rel = cfg->eps_rel;
+  a.j_max = cfg->j_max;
+  a.j_check = cfg->j_check;
+  a.sigma = sigma;
+  a.ws = WsArrays{ws->x, ws->u, ws->vc_pos, ws->vc_neg, ws->dyn_dual, ws->relax_dual};
+  a.iterations = iterations;
+  a.converged = converged;
+  a.status = status;
+  a.fail_index = fail_index;
+  a.active = nullptr;
+  if (status) PT_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * (size_t)batch, h->stream));
+  if (fail_index)
+    PT_CUDA(cudaMemsetAsync(fail_index, 0xff, sizeof(int32_t) * (size_t)batch, h->stream));
+  return dispatch_pipg(h, a);
+}
+
+int ptopt_cuda_pipg_batch(ptopt_cuda_handle* h, int batch, const ptopt_subproblem_shape* shape,
+                          const ptopt_subproblem_arrays* sp, const ptopt_pipg_config* cfg,
+                          const double* sigma, const ptopt_workspace_arrays* ws,
+                          int32_t* iterations, uint8_t* converged, int32_t* status,
+                          int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!sp || !cfg || !sigma || !ws)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null argument");
+  if (!ws->x || !ws->u || !ws->vc_pos || !ws->vc_neg || !ws->dyn_dual || !ws->relax_dual)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "pipg: null workspace array");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  SubShape s;
+  PT_TRY(check_shape(shape, s));
+  const size_t B = (size_t)batch, n = (size_t)s.n, m = n - 1, nx = (size_t)s.nx, nu = (size_t)s.nu;
+  ptopt_subproblem_arrays dev{};
+  PT_TRY(upload_sub(h, batch, s, sp, &dev));
+  const double* dsig;
+  PT_TRY(upload(h, B_SIGMA, sigma, B, &dsig));
+  ptopt_workspace_arrays dws{};
+  const double* tmp;
+  PT_TRY(upload(h, B_WSX, (const double*)ws->x, B * n * nx, &tmp)); dws.x = const_cast<double*>(tmp);
+  PT_TRY(upload(h, B_WSU, (const double*)ws->u, B * n * nu, &tmp)); dws.u = const_cast<double*>(tmp);
+  PT_TRY(upload(h, B_WSP, (const double*)ws->vc_pos, B * m * nx, &tmp)); dws.vc_pos = const_cast<double*>(tmp);
+  PT_TRY(upload(h, B_WSN, (const double*)ws->vc_neg, B * m * nx, &tmp)); dws.vc_neg = const_cast<double*>(tmp);
+  PT_TRY(upload(h, B_WSD, (const double*)ws->dyn_dual, B * m * nx, &tmp)); dws.dyn_dual = const_cast<double*>(tmp);
+  PT_TRY(upload(h, B_WSR, (const double*)ws->relax_dual, B * m, &tmp)); dws.relax_dual = const_cast<double*>(tmp);
+  int *dit, *dst, *dfi;
+  unsigned char* dcv;
+  PT_TRY(device_out(h, B_ITERS, B, &dit));
+  PT_TRY(device_out(h, B_CONV, B, &dcv));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
+  PT_TRY(ptopt_cuda_pipg_batch_dev(h, batch, shape, &dev, cfg, dsig, &dws, dit, dcv, dst, dfi));
+  PT_TRY(download(h, ws->x, dws.x, B * n * nx));
+  PT_TRY(download(h, ws->u, dws.u, B * n * nu));
+  PT_TRY(download(h, ws->vc_pos, dws.vc_pos, B * m * nx));
+  PT_TRY(download(h, ws->vc_neg, dws.vc_neg, B * m * nx));
+  PT_TRY(download(h, ws->dyn_dual, dws.dyn_dual, B * m * nx));
+  PT_TRY(download(h, ws->relax_dual, dws.relax_dual, B * m));
+  PT_TRY(download(h, iterations, dit, B));
+  PT_TRY(download(h, converged, dcv, B));
+  PT_TRY(download(h, status, dst, B));
+  PT_TRY(download(h, fail_index, dfi, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+// ---- SCP loop -------------------------------------------------------------------------
+
+int ptopt_cuda_scp_solve_batch(ptopt_cuda_handle* h, int batch, const double* init_state,
+                               const double* x_guess, const double* u_guess,
+                               const uint64_t* rng_seed, double* x_out, double* u_out,
+                               int32_t* scp_iterations, uint8_t* converged,
+                               double* final_defect_inf, double* history, int32_t* power_trips,
+                               int32_t* status, int32_t* fail_index) {
+  return scp_solve_common(h, batch, init_state, x_guess, u_guess, rng_seed, x_out, u_out,
+                          scp_iterations, converged, final_defect_inf, history, power_trips,
+                          status, fail_index, cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost);
+}
+
+int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double* init_state,
+                                   const double* x_guess, const double* u_guess,
+                                   const uint64_t* rng_seed, double* x_out, double* u_out,
+                                   int32_t* scp_iterations, uint8_t* converged,
+                                   double* final_defect_inf, double* history, int32_t* power_trips,
+                                   int32_t* status, int32_t* fail_index) {
+  return scp_solve_common(h, batch, init_state, x_guess, u_guess, rng_seed, x_out, u_out,
+                          scp_iterations, converged, final_defect_inf, history, power_trips,
+                          status, fail_index, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+// rocket_model.cuh — 6-DoF vehicle + CTCS augmentation evaluated in registers, and the
+// per-lane RK4 sensitivity propagation used by the discretization kernel.
+//
+// One warp integrates one grid interval (propagate_interval,
+// /root/reference/proj/include/ptopt/discretizer.hpp:82-149).  Lane j < 29 owns column j of the
+// sensitivity bundle [Phi_x (15) | Phi_u- (7) | Phi_u+ (7)]; every lane carries the (identical)
+// augmented state, so the model, its Jacobian and the column product A(tau) * col are evaluated
+// entirely in registers with no cross-lane traffic in the inner loop.  The Jacobian
+// (rocket6dof.hpp:303-402 through ctcs.hpp:79-129) is applied in its structural sparsity:
+// skipped entries are exact zeros in the reference's dense product, so results agree with the
+// dense loops up to FMA contraction.
+//
+// Everything here is `__host__ __device__` so tests/sim can run the same lane code on the CPU.
+#pragma once
+
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define PT_HD __host__ __device__ __forceinline__
+#else
+#define PT_HD inline
+#endif
+
+namespace ptopt_b200 {
+
+constexpr int kNX = 15;
+constexpr int kNU = 7;
+constexpr int kNXI = 14;
+constexpr int kCols = kNX + 2 * kNU;  // 29 sensitivity columns
+
+// per-instance status codes (mirror ptopt_instance_status in include/ptopt_cuda.h)
+constexpr int kStOk = 0;
+constexpr int kStPropDiverged = 1;
+constexpr int kStSolverDiverged = 2;
+constexpr int kStDilation = 3;
+constexpr int kStMass = 4;
+constexpr int kStThrust = 5;
+constexpr int kStSeedZero = 6;
+
+/// Vehicle constants with everything that does not depend on the state folded on the host
+/// (VehicleParams, rocket6dof.hpp:85-99; inverse3 :210-224; the cos() terms of :282, :292).
+struct ModelConst {
+  double alpha;
+  double g[3];
+  double J[9];
+  double Jinv[9];
+  double JinvR[9];  // Jinv * skew(r_thrust)  (rocket6dof.hpp:370-375)
+  double rT[3];
+  double H[8];
+  double m_dry;
+  double v_max_sq;
+  double c_theta_sq;  // (1 - cos(theta_max))^2
+  double w_max_sq;
+  double sec_delta;
+  double T_max;
+  double T_min;
+  double gamma_max_sq;
+};
+
+PT_HD bool pt_finite(double v) { return fabs(v) <= 1.79769313486231570e308; }
+
+/// Everything one RK4 stage needs from (x, u): the rate f, the scalars that define the
+/// nonzeros of A = df/dx, and what is needed to form one column of B = df/du.
+struct Stage {
+  double s;       // dilation factor
+  double f[kNX];  // augmented rate  s * (F, sum g+^2)
+  double F[kNXI]; // undilated model rate (the s-column of B, ctcs.hpp:99)
+  double integrand;
+  double C[9];    // body-to-inertial DCM
+  double rm;      // 1/m
+  double rTn;     // 1/|T|
+  double svm[3];  // A[v_i][m]
+  double svq[12]; // A[v_i][q_j]
+  double hw[3];   // s * 0.5 * w_k
+  double gq[4];   // s * 0.5 * q_k
+  double sww[9];  // A[w_i][w_j]
+  bool y_active;  // any path inequality violated
+  double ay[kNX]; // row y of A (valid when y_active)
+  double gp[9];   // clipped constraint values (valid when y_active)
+};
+
+/// Evaluates the stage at augmented state x and control u.  Returns a status code in the
+/// reference's throw order: dilation (ctcs.hpp:66), mass (rocket6dof.hpp:246), thrust (:306).
+PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stage& st) {
+  const double s = u[6];
+  const double m = x[0];
+  const double T0 = u[0], T1 = u[1], T2 = u[2];
+  if (!(s > 0.0)) return kStDilation;
+  if (!(m > 0.0)) return kStMass;
+  const double Tn = sqrt(T0 * T0 + T1 * T1 + T2 * T2);
+  if (Tn < 1e-9) return kStThrust;
+  st.s = s;
+  const double rm = 1.0 / m;
+  const double rTn = 1.0 / Tn;
+  st.rm = rm;
+  st.rTn = rTn;
+  const double q0 = x[7], q1 = x[8], q2 = x[9], qw = x[10];
+  const double w0 = x[11], w1 = x[12], w2 = x[13];
+
+  // dcm, rocket6dof.hpp:176-188
+  {
+    const double ss = q0 * q0 + q1 * q1 + q2 * q2;
+    const double d = qw * qw - ss;
+    double* C = st.C;
+    C[0] = d + 2.0 * q0 * q0;
+    C[1] = 2.0 * q0 * q1 + 2.0 * qw * (-q2);
+    C[2] = 2.0 * q0 * q2 + 2.0 * qw * q1;
+    C[3] = 2.0 * q1 * q0 + 2.0 * qw * q2;
+    C[4] = d + 2.0 * q1 * q1;
+    C[5] = 2.0 * q1 * q2 + 2.0 * qw * (-q0);
+    C[6] = 2.0 * q2 * q0 + 2.0 * qw * (-q1);
+    C[7] = 2.0 * q2 * q1 + 2.0 * qw * q0;
+    C[8] = d + 2.0 * q2 * q2;
+  }
+  double CT[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) CT[i] = st.C[i * 3] * T0 + st.C[i * 3 + 1] * T1 + st.C[i * 3 + 2] * T2;
+
+  // eval_dynamics, rocket6dof.hpp:245-274
+  double* F = st.F;
+  F[0] = -P.alpha * Tn;
+  F[1] = x[4];
+  F[2] = x[5];
+  F[3] = x[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) F[4 + i] = CT[i] * rm + P.g[i];
+  F[7] = 0.5 * (qw * w0 + (q1 * w2 - q2 * w1));
+  F[8] = 0.5 * (qw * w1 + (q2 * w0 - q0 * w2));
+  F[9] = 0.5 * (qw * w2 + (q0 * w1 - q1 * w0));
+  F[10] = -0.5 * (q0 * w0 + q1 * w1 + q2 * w2);
+  double Jw[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) Jw[i] = P.J[i * 3] * w0 + P.J[i * 3 + 1] * w1 + P.J[i * 3 + 2] * w2;
+  {
+    const double lev0 = P.rT[1] * T2 - P.rT[2] * T1;
+    const double lev1 = P.rT[2] * T0 - P.rT[0] * T2;
+    const double lev2 = P.rT[0] * T1 - P.rT[1] * T0;
+    const double gy0 = w1 * Jw[2] - w2 * Jw[1];
+    const double gy1 = w2 * Jw[0] - w0 * Jw[2];
+    const double gy2 = w0 * Jw[1] - w1 * Jw[0];
+    const double t0 = lev0 - gy0 + u[3], t1 = lev1 - gy1 + u[4], t2 = lev2 - gy2 + u[5];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      F[11 + i] = P.Jinv[i * 3] * t0 + P.Jinv[i * 3 + 1] * t1 + P.Jinv[i * 3 + 2] * t2;
+  }
+
+  // eval_constraints, rocket6dof.hpp:278-301, clipped as in ctcs.hpp:47-56
+  const double hq0 = P.H[0] * q0 + P.H[1] * q1 + P.H[2] * q2 + P.H[3] * qw;
+  const double hq1 = P.H[4] * q0 + P.H[5] * q1 + P.H[6] * q2 + P.H[7] * qw;
+  double g[9];
+  g[0] = P.m_dry - m;
+  g[1] = -x[1];
+  g[2] = x[4] * x[4] + x[5] * x[5] + x[6] * x[6] - P.v_max_sq;
+  g[3] = 4.0 * (hq0 * hq0 + hq1 * hq1) - P.c_theta_sq;
+  g[4] = w0 * w0 + w1 * w1 + w2 * w2 - P.w_max_sq;
+  g[5] = Tn - T0 * P.sec_delta;
+  g[6] = Tn - P.T_max;
+  g[7] = -Tn + P.T_min;
+  g[8] = u[3] * u[3] + u[4] * u[4] + u[5] * u[5] - P.gamma_max_sq;
+  double integrand = 0.0;
+  bool active = false;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double v = g[i] > 0.0 ? g[i] : 0.0;
+    st.gp[i] = v;
+    integrand += v * v;
+    active = active || (v > 0.0);
+  }
+  st.integrand = integrand;
+  st.y_active = active;
+#pragma unroll
+  for (int i = 0; i < kNXI; ++i) st.f[i] = s * F[i];
+  st.f[14] = s * integrand;
+
+  // nonzeros of A = s * dF/dxi (rocket6dof.hpp:325-369 through ctcs.hpp:96-97)
+  const double rm2 = rm * rm;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) st.svm[i] = s * (-CT[i] * rm2);
+  {
+    // dcm_times_vec_jac, rocket6dof.hpp:191-207, divided by m
+    const double qT = q0 * T0 + q1 * T1 + q2 * T2;
+    const double qv[3] = {q0, q1, q2};
+    const double T[3] = {T0, T1, T2};
+    const double Tk[9] = {0.0, -T2, T1, T2, 0.0, -T0, -T1, T0, 0.0};
+    const double qxT[3] = {q1 * T2 - q2 * T1, q2 * T0 - q0 * T2, q0 * T1 - q1 * T0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double v = -2.0 * T[i] * qv[j] + 2.0 * qv[i] * T[j] - 2.0 * qw * Tk[i * 3 + j];
+        if (i == j) v += 2.0 * qT;
+        st.svq[i * 4 + j] = s * (v * rm);
+      }
+      st.svq[i * 4 + 3] = s * ((2.0 * qw * T[i] + 2.0 * qxT[i]) * rm);
+    }
+  }
+  st.hw[0] = s * (0.5 * w0);
+  st.hw[1] = s * (0.5 * w1);
+  st.hw[2] = s * (0.5 * w2);
+  st.gq[0] = s * (0.5 * q0);
+  st.gq[1] = s * (0.5 * q1);
+  st.gq[2] = s * (0.5 * q2);
+  st.gq[3] = s * (0.5 * qw);
+  {
+    // dw/dw = Jinv * ([Jw]x - [w]x J), rocket6dof.hpp:352-369
+    const double JWk[9] = {0.0, -Jw[2], Jw[1], Jw[2], 0.0, -Jw[0], -Jw[1], Jw[0], 0.0};
+    const double Wk[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+    double M[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double acc = JWk[i * 3 + j];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc -= Wk[i * 3 + k] * P.J[k * 3 + j];
+        M[i * 3 + j] = acc;
+      }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc += P.Jinv[i * 3 + k] * M[k * 3 + j];
+        st.sww[i * 3 + j] = s * acc;
+      }
+  }
+  if (active) {
+    // row y of A: 2 s g+ dg/dxi (ctcs.hpp:108-115 with rocket6dof.hpp:383-391)
+    const double s2 = 2.0 * s;
+    double* ay = st.ay;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) ay[i] = 0.0;
+    ay[0] = s2 * st.gp[0] * -1.0;
+    ay[1] = s2 * st.gp[1] * -1.0;
+    ay[4] = s2 * st.gp[2] * (2.0 * x[4]);
+    ay[5] = s2 * st.gp[2] * (2.0 * x[5]);
+    ay[6] = s2 * st.gp[2] * (2.0 * x[6]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ay[7 + j] = s2 * st.gp[3] * (8.0 * (hq0 * P.H[j] + hq1 * P.H[4 + j]));
+    ay[11] = s2 * st.gp[4] * (2.0 * w0);
+    ay[12] = s2 * st.gp[4] * (2.0 * w1);
+    ay[13] = s2 * st.gp[4] * (2.0 * w2);
+  }
+  return kStOk;
+}
+
+/// One column of B = df/du (ctcs.hpp:96-128; rocket6dof.hpp:333-334, 370-380, 393-400).
+/// jc in [0,7): thrust x/y/z, torque x/y/z, dilation.
+PT_HD void b_column(const ModelConst& P, const Stage& st, const double* u, int jc, double* b) {
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) b[i] = 0.0;
+  const double s = st.s;
+  if (jc < 3) {
+    const double Tj = jc == 0 ? u[0] : (jc == 1 ? u[1] : u[2]);
+    const double that = Tj * st.rTn;
+    b[0] = s * (-P.alpha * that);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double Cij = jc == 0 ? st.C[i * 3] : (jc == 1 ? st.C[i * 3 + 1] : st.C[i * 3 + 2]);
+      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
+      b[4 + i] = s * (Cij * st.rm);
+      b[11 + i] = s * JR;
+    }
+    if (st.y_active) {
+      const double s2 = 2.0 * s;
+      double acc = 0.0;
+      acc += s2 * st.gp[5] * (that - (jc == 0 ? P.sec_delta : 0.0));
+      acc += s2 * st.gp[6] * that;
+      acc += s2 * st.gp[7] * (-that);
+      b[14] = acc;
+    }
+  } else if (jc < 6) {
+    const int j = jc - 3;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
+      b[11 + i] = s * Ji;
+    }
+    if (st.y_active) {
+      const double gj = j == 0 ? u[3] : (j == 1 ? u[4] : u[5]);
+      b[14] = 2.0 * s * st.gp[8] * (2.0 * gj);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kNXI; ++i) b[i] = st.F[i];
+    b[14] = st.integrand;
+  }
+}
+
+/// d = A * c in the structural sparsity of A (ascending column order inside every row, as
+/// mat_mat does: smallmat.hpp:115-120).
+PT_HD void apply_A(const Stage& st, const double* c, double* d) {
+  const double s = st.s;
+  d[0] = 0.0;
+  d[1] = s * c[4];
+  d[2] = s * c[5];
+  d[3] = s * c[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = st.svm[i] * c[0];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += st.svq[i * 4 + j] * c[7 + j];
+    d[4 + i] = acc;
+  }
+  const double* h = st.hw;
+  const double* g = st.gq;
+  d[7] = h[2] * c[8] - h[1] * c[9] + h[0] * c[10] + g[3] * c[11] - g[2] * c[12] + g[1] * c[13];
+  d[8] = -h[2] * c[7] + h[0] * c[9] + h[1] * c[10] + g[2] * c[11] + g[3] * c[12] - g[0] * c[13];
+  d[9] = h[1] * c[7] - h[0] * c[8] + h[2] * c[10] - g[1] * c[11] + g[0] * c[12] + g[3] * c[13];
+  d[10] = -h[0] * c[7] - h[1] * c[8] - h[2] * c[9] - g[0] * c[11] - g[1] * c[12] - g[2] * c[13];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    d[11 + i] = st.sww[i * 3] * c[11] + st.sww[i * 3 + 1] * c[12] + st.sww[i * 3 + 2] * c[13];
+  double dy = 0.0;
+  if (st.y_active) {
+#pragma unroll
+    for (int k = 0; k < kNXI; ++k) dy += st.ay[k] * c[k];
+  }
+  d[14] = dy;
+}
+
+/// Per-warp scratch for the (lane-invariant) state part of the RK4 bundle.
+struct StateScratch {
+  double sx[kNX];  // state at the start of the RK4 step
+  double ax[kNX];  // running RK4 combination
+};
+
+/// Integrates one interval for sensitivity column `lane` (lanes >= 29 only follow the state).
+/// `writer` lanes update the shared state scratch (lane 0 on the GPU; every lane has a private
+/// scratch in the CPU simulation).  SYNC() is __syncwarp() on the device.
+/// On success col[15] holds column `lane` of [A | B- | B+] and x_end[15] the propagated state.
+template <class SyncFn>
+PT_HD int propagate_lane(const ModelConst& P, int lane, bool writer, StateScratch& sc,
+                         const double* xk, const double* uk, const double* uk1, double tau_k,
+                         double tau_k1, int steps, double* col, double* x_end, SyncFn SYNC) {
+  // all_finite(x_k), discretizer.hpp:89
+  bool fin = true;
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) fin = fin && pt_finite(xk[i]);
+  if (!fin) return kStPropDiverged;
+
+  const double span = tau_k1 - tau_k;
+  const double h = span / steps;
+  const bool is_col = lane < kCols;
+  const int jc = lane < kNX ? 0 : (lane - kNX) % kNU;    // control index of this lane's B column
+  const bool minus = lane >= kNX && lane < kNX + kNU;    // Phi_u- lanes get lam_left
+  const bool forced = lane >= kNX && lane < kCols;
+
+  double s_c[kNX], a_c[kNX], c[kNX];  // column: step start, RK4 combination, stage input
+  double xin[kNX];
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) {
+    s_c[i] = (i == lane) ? 1.0 : 0.0;  // Phi_x(0) = I, Phi_u(0) = 0 (discretizer.hpp:94-96)
+    xin[i] = xk[i];
+  }
+  if (writer) {
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) sc.sx[i] = xk[i];
+  }
+  SYNC();
+
+  for (int step = 0; step < steps; ++step) {
+    const double t0 = tau_k + h * step;
+    const double t_end = (step + 1 == steps) ? tau_k1 : t0 + h;
+#pragma unroll 1
+    for (int stage = 0; stage < 4; ++stage) {
+      const double tau = stage == 0 ? t0 : (stage == 3 ? t_end : t0 + 0.5 * h);
+      const double wk = (stage == 0 || stage == 3) ? h / 6.0 : h / 3.0;       // RK4 weight
+      const double wn = stage == 2 ? h : 0.5 * h;                             // next-stage offset
+      // foh_interp, discretizer.hpp:26-39
+      const double lam_right = (tau - tau_k) / span;
+      const double lam_left = (tau_k1 - tau) / span;
+      double u[kNU];
+#pragma unroll
+      for (int i = 0; i < kNU; ++i) u[i] = lam_left * uk[i] + lam_right * uk1[i];
+      if (stage == 0) {
+#pragma unroll
+        for (int i = 0; i < kNX; ++i) c[i] = s_c[i];
+      }
+      Stage st;
+      const int rc = eval_stage(P, xin, u, st);
+      if (rc != kStOk) return rc;
+
+      if (is_col) {
+        double d[kNX];
+        apply_A(st, c, d);
+        if (forced) {
+          double b[kNX];
+          b_column(P, st, u, jc, b);
+          const double lam = minus ? lam_left : lam_right;
+#pragma unroll
+          for (int i = 0; i < kNX; ++i) d[i] += lam * b[i];
+        }
+#pragma unroll
+        for (int i = 0; i < kNX; ++i) {
+          a_c[i] = (stage == 0 ? s_c[i] : a_c[i]) + wk * d[i];
+          c[i] = s_c[i] + wn * d[i];  // unused after stage 3
+        }
+      }
+      // state part: identical in every lane; only the writer touches the scratch
+      SYNC();
+#pragma unroll
+      for (int i = 0; i < kNX; ++i) {
+        const double sxi = sc.sx[i];
+        const double axi = (stage == 0 ? sxi : sc.ax[i]) + wk * st.f[i];
+        xin[i] = sxi + wn * st.f[i];
+        if (stage == 3) xin[i] = axi;
+        st.f[i] = axi;  // reuse as the value to publish
+      }
+      SYNC();
+      if (writer) {
+#pragma unroll
+        for (int i = 0; i < kNX; ++i) {
+          sc.ax[i] = st.f[i];
+          if (stage == 3) sc.sx[i] = st.f[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) s_c[i] = a_c[i];
+    // all_finite(s.x) after every RK4 step, discretizer.hpp:136
+    fin = true;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) fin = fin && pt_finite(xin[i]);
+    if (!fin) return kStPropDiverged;
+    SYNC();
+  }
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) {
+    col[i] = s_c[i];
+    x_end[i] = xin[i];
+  }
+  return kStOk;
+}
+
+}  // namespace ptopt_b200

@@ -1,0 +1,53 @@
+// sim_kernels.cpp — TEST INFRASTRUCTURE.  Runs the device lane code of
+// paper_2404_18034_b200/csrc/*.cuh on the CPU, one "lane" after another, so the
+// kernel arithmetic can be checked against the oracle without a GPU.  Not part of
+// the product library and never loaded by it.
+#include <cstring>
+
+#include "model_const.hpp"
+#include "rocket_model.cuh"
+
+using namespace ptopt_b200;
+
+extern "C" {
+
+/// One interval through propagate_lane for every lane, then the kernel's epilogue.
+int sim_propagate_interval(const ptopt_vehicle_params* vp, const double* xk, const double* uk,
+                           const double* uk1, double tau_k, double tau_k1, int steps, double* A,
+                           double* Bm, double* Bp, double* w, double* x_end) {
+  ModelConst mc;
+  if (!make_model_const(*vp, mc)) return -8;
+  double block[kNX][kCols];
+  double xe[kNX];
+  for (int lane = 0; lane < 32; ++lane) {
+    StateScratch sc;
+    double col[kNX], xel[kNX];
+    const int rc = propagate_lane(mc, lane, true, sc, xk, uk, uk1, tau_k, tau_k1, steps, col, xel,
+                                  [] {});
+    if (rc) return rc;
+    if (lane < kCols)
+      for (int i = 0; i < kNX; ++i) block[i][lane] = col[i];
+    if (lane == 0) std::memcpy(xe, xel, sizeof xe);
+  }
+  for (int i = 0; i < kNX; ++i) {
+    double acc = 0.0;
+    for (int j = 0; j < kNX; ++j) acc += block[i][j] * xk[j];
+    double wv = xe[i] + -1.0 * acc;
+    acc = 0.0;
+    for (int j = 0; j < kNU; ++j) acc += block[i][kNX + j] * uk[j];
+    wv += -1.0 * acc;
+    acc = 0.0;
+    for (int j = 0; j < kNU; ++j) acc += block[i][kNX + kNU + j] * uk1[j];
+    wv += -1.0 * acc;
+    w[i] = wv;
+    x_end[i] = xe[i];
+    for (int j = 0; j < kNX; ++j) A[i * kNX + j] = block[i][j];
+    for (int j = 0; j < kNU; ++j) {
+      Bm[i * kNU + j] = block[i][kNX + j];
+      Bp[i * kNU + j] = block[i][kNX + kNU + j];
+    }
+  }
+  return 0;
+}
+
+}  // extern "C"

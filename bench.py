@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py — SCP solves/sec of the batched 6-DoF powered-descent hot path on B200.
+
+    python bench.py --gpus N --steps K --warmup W            # this repo's CUDA path
+    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path
+
+One "step" = one full batched ``scp_solve`` (26 discretizations + 25 power iterations +
+25 x 2500 PIPG iterations per instance at the shipped defaults) over one batch of dispersed
+landing scenarios, N=50 nodes, 4096 instances per GPU (BASELINE.json configs[3]).  Instances
+are independent, so ranks shard run ids with no data-path collective (weak scaling).
+
+JSON line keys: see the bench contract; additionally ``stages_ms`` (device time per stage
+of the last timed graph launch), ``roofline`` (dominant kernel vs the FP64 DFMA peak measured
+in the same run and vs the compulsory-HBM bound) and ``cpu_baseline`` (the unmodified
+reference compiled in place, oracle/_ref, timed on the host cores on a bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NX, NU = 15, 7
+
+
+# --------------------------------------------------------------------------- helpers
+def algorithmic_flops(nodes: int):
+    """dense block-product flops only."""
+    m = nodes - 1
+    disc = m * (16 * 4 * 2 * NX * NX * (NX + 2 * NU) + 2 * (NX * NX + 2 * NX * NU))
+    op = m * 2 * 2 * (NX * NX + 2 * NX * NU)  # one PIPG iteration or one power trip
+    return disc, op
+
+
+class ClockSampler:
+    """Samples nvidia-smi clocks / throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                     "-i", str(self.index)], capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) >= 7:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.25)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = [n for i, n in enumerate(names) if any(r[3 + i] == "Active" for r in self.rows)]
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(self.rows), "reasons": reasons}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_reference_run(nodes: int, instances: int, workers: int):
+    """Times the reference's own mc::run_batch (oracle/_ref when built, else the C restatement)
+    on `workers` host threads.  Returns (solves_per_s, kind, wall_s)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import CpuOracle, ref_available
+    from paper_2404_18034_b200 import scenario
+
+    sc = scenario.default_scenario(nodes)
+    desc = sc.problem_desc()
+    if ref_available():
+        oracle, kind = CpuOracle("ptref", fast=True), "reference"
+    else:
+        oracle, kind = CpuOracle("ptor"), "port"
+    wall, rec, _, _ = oracle.run_batch(desc, sc.initial_state, sc.dispersion.r_low,
+                                       sc.dispersion.r_high, sc.dispersion.seed, instances,
+                                       workers, sc.audit_substeps)
+    assert (rec[:, 7] == 0).all(), "reference CPU run reported a failed instance"
+    return instances / wall, kind, wall
+
+
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    inst = args.cpu_instances or cores
+    walls = []
+    kind = "reference"
+    for i in range(args.warmup + args.steps):
+        _, kind, wall = cpu_reference_run(args.nodes, inst, cores)
+        if i >= args.warmup:
+            walls.append(wall)
+    total = sum(walls)
+    value = inst * len(walls) / total
+    sample = (f"{inst} instances of the {args.batch}-instance N={args.nodes} batch per step "
+              f"(run ids 0..{inst - 1}), mc::run_batch on {cores} threads")
+    line = {
+        "impl": "reference", "metric": "SCP solves/sec (batched, N=50)", "value": value,
+        "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(walls), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {"workload": f"full SCP loop (trust region + virtual control), batch {args.batch} per GPU, "
+                        f"N={args.nodes} nodes, default 6-DoF landing scenario, dispersed initial "
+                        f"positions (BASELINE.json configs[3])",
+            "batch_per_gpu": args.batch, "global_batch": args.batch * world, "nodes": args.nodes,
+            "scp_max_iters": 25, "pipg_j_max": 2500, "power_j_max": 10000,
+            "parallelism": f"instances sharded over {world} GPU(s), no collective",
+            "l2": "per-step working set (operator blocks + iterates of the whole batch) exceeds "
+                  "the 126 MB L2; inputs are re-uploaded/re-initialised every step"}
+
+
+# --------------------------------------------------------------------------- own arm
+def run_own_arm(args):
+    import numpy as np
+    import torch
+
+    from paper_2404_18034_b200 import scenario
+    from paper_2404_18034_b200.binding import Solver
+
+    rank, local_rank, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the product path has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    use_dist = world > 1
+    if use_dist:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if use_dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    B, n = args.batch, args.nodes
+    sc = scenario.default_scenario(n)
+    desc = sc.problem_desc()
+    mi = int(desc.max_iters)
+    ids = range(rank * B, (rank + 1) * B)  # weak scaling: B run ids per rank
+    batch = scenario.make_batch(sc, ids)
+
+    stream = torch.cuda.Stream(device=dev)
+    solver = Solver(desc, device=local_rank, stream=stream)
+
+    # device-resident inputs / outputs for the kernel-only number
+    d_init = torch.from_numpy(batch["init_state"]).to(dev)
+    d_xg = torch.from_numpy(batch["x_guess"]).to(dev)
+    d_ug = torch.from_numpy(batch["u_guess"]).to(dev)
+    d_seed = torch.from_numpy(batch["rng_seed"].view(np.int64)).to(dev)
+    d_x = torch.empty((B, n, NX), dtype=torch.float64, device=dev)
+    d_u = torch.empty((B, n, NU), dtype=torch.float64, device=dev)
+    d_iters = torch.empty(B, dtype=torch.int32, device=dev)
+    d_conv = torch.empty(B, dtype=torch.uint8, device=dev)
+    d_fdef = torch.empty(B, dtype=torch.float64, device=dev)
+    d_hist = torch.empty((B, mi, 5), dtype=torch.float64, device=dev)
+    d_trips = torch.empty((B, mi), dtype=torch.int32, device=dev)
+    d_status = torch.empty(B, dtype=torch.int32, device=dev)
+    d_fail = torch.empty(B, dtype=torch.int32, device=dev)
+
+    def step_dev():
+        solver.scp_solve_dev(d_init, d_xg, d_ug, d_seed, d_x, d_u, d_iters, d_conv, d_fdef,
+                             d_hist, d_trips, d_status, d_fail)
+
+    fp64_peak = solver.measure_fp64_peak()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step_dev()
+        stream.synchronize()
+        barrier()
+        launches0 = solver.launch_count
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clocks:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step_dev()
+            ev1.record(stream)
+            stream.synchronize()
+        barrier()
+        launches = solver.launch_count - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    stages = solver.scp_stage_times()
+    trips = d_trips.cpu().numpy().astype(np.int64)
+    hist = d_hist.cpu().numpy()
+    status = d_status.cpu().numpy()
+    scp_iters = d_iters.cpu().numpy()
+
+    # ---- end to end through the host-pointer C-ABI call, pinned host buffers
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype).pin_memory().numpy()
+
+    h_in = {}
+    for k in ("init_state", "x_guess", "u_guess", "rng_seed"):
+        src = batch[k].view(np.int64) if batch[k].dtype == np.uint64 else batch[k]
+        h_in[k] = pinned(src.shape, torch.from_numpy(src).dtype)
+        h_in[k][...] = src
+    h_out = dict(x=pinned((B, n, NX), torch.float64), u=pinned((B, n, NU), torch.float64),
+                 scp_iterations=pinned((B,), torch.int32), converged=pinned((B,), torch.uint8),
+                 final_defect_inf=pinned((B,), torch.float64),
+                 history=pinned((B, mi, 5), torch.float64),
+                 power_trips=pinned((B, mi), torch.int32), status=pinned((B,), torch.int32),
+                 fail_index=pinned((B,), torch.int32))
+    h2d = sum(int(v.nbytes) for v in h_in.values())
+    d2h = sum(int(v.nbytes) for v in h_out.values())
+
+    def step_e2e():
+        solver.scp_solve_into(h_in["init_state"], h_in["x_guess"], h_in["u_guess"],
+                              h_in["rng_seed"], h_out)
+
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    step_e2e()  # the graph is warm already; one untimed pass for the staging path
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_e2e()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    assert np.array_equal(h_out["x"], d_x.cpu().numpy()), "e2e and device-resident results differ"
+
+    # ---- max over ranks
+    if use_dist:
+        t = torch.tensor([ms_total, e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, e2e_s = float(t[0]), float(t[1])
+        bad = torch.tensor([int((status != 0).sum())], device=dev)
+        dist.all_reduce(bad)
+        n_bad = int(bad[0])
+    else:
+        n_bad = int((status != 0).sum())
+
+    if rank == 0:
+        disc_flop, op_flop = algorithmic_flops(n)
+        sum_trips = float(trips.sum())
+        pipg_iters = float(hist[:, :, 3].sum())
+        n_lin = float((scp_iters + 1).sum())
+        flop = {"linearize": n_lin * disc_flop, "power_iteration": sum_trips * op_flop,
+                "pipg": pipg_iters * op_flop}
+        dom = max(("linearize", "power_iteration", "pipg"), key=lambda k: stages[k])
+        achieved = flop[dom] / (stages[dom] * 1e-3) * 1e-12
+        total_flop = sum(flop.values())
+        value = world * B * args.steps / (ms_total * 1e-3)
+        line = {
+            "metric": "SCP solves/sec (batched, N=50)", "value": value, "unit": "solves/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, world),
+            "clocks": clocks.summary(),
+            "e2e": {"value": world * B * e2e_steps / e2e_s, "unit": "solves/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "stages_ms": stages,
+            "work": {"power_trips_mean": sum_trips / B, "pipg_iterations_mean": pipg_iters / B,
+                     "scp_iterations_mean": float(scp_iters.mean()), "failed_instances": n_bad,
+                     "algorithmic_gflop_per_solve": total_flop / B * 1e-9,
+                     "algorithmic_tflops_whole_step": total_flop / (stages["graph_total"] * 1e-3) * 1e-12},
+            "roofline": {
+                "bound": "fp64", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
+                               "no fp64 entry)",
+                "traffic": None,
+                "per_stage": {k: {"tflops": flop[k] / (stages[k] * 1e-3) * 1e-12,
+                                  "frac": flop[k] / (stages[k] * 1e-3) * 1e-12 / fp64_peak,
+                                  "share_of_step": stages[k] / stages["graph_total"]}
+                              for k in ("linearize", "power_iteration", "pipg")},
+            },
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            inst = args.cpu_instances or cores
+            v, kind, wall = cpu_reference_run(n, inst, cores)
+            line["cpu_baseline"] = {
+                "value": v, "unit": "solves/s", "cores": cores, "kind": kind,
+                "sample": f"run ids 0..{inst - 1} of the same batch ({inst} full N={n} solves, "
+                          f"mc::run_batch on {cores} threads, {wall:.1f} s)"}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if use_dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--batch", type=int, default=4096, help="instances per GPU")
+    ap.add_argument("--nodes", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-instances", type=int, default=0,
+                    help="instances in the CPU sample (default: one per host core)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_own_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -304,6 +304,21 @@ int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double
                                    double* final_defect_inf, double* history, int32_t* power_trips,
                                    int32_t* status, int32_t* fail_index);
 
+/* ---- measurement --------------------------------------------------------- */
+
+#define PTOPT_STAGE_COUNT 6
+/* Device time in milliseconds of the most recent scp_solve_batch[_dev] graph launch on this
+ * handle, split by stage and measured by event nodes inside the graph:
+ * [0] discretization (linearize_all), [1] defect test + assemble_subproblem + seed,
+ * [2] power iteration, [3] PIPG, [4] iterate update, [5] whole graph.
+ * Blocks until the launch has finished.  (No reference counterpart: the reference only keeps
+ * wall-clock times per instance, proj/include/ptopt/montecarlo.hpp:113, 133.) */
+int ptopt_cuda_scp_stage_times(ptopt_cuda_handle* h, double* ms);
+
+/* Measures the FP64 FMA throughput of the device (dependent-chain-free DFMA loop filling every
+ * SM) in TFLOP/s: the roofline denominator for this path, which MEASURED_PEAKS.json lacks. */
+int ptopt_cuda_measure_fp64_peak(ptopt_cuda_handle* h, double* tflops);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

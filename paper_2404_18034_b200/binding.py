@@ -28,7 +28,10 @@ EXPORTS = [
     "ptopt_cuda_power_iteration_batch", "ptopt_cuda_power_iteration_batch_dev",
     "ptopt_cuda_pipg_batch", "ptopt_cuda_pipg_batch_dev",
     "ptopt_cuda_scp_solve_batch", "ptopt_cuda_scp_solve_batch_dev",
+    "ptopt_cuda_scp_stage_times", "ptopt_cuda_measure_fp64_peak",
 ]
+
+STAGE_NAMES = ("linearize", "prepare", "power_iteration", "pipg", "update", "graph_total")
 
 
 class PtoptError(RuntimeError):
@@ -122,6 +125,18 @@ class Solver:
     @property
     def launch_count(self) -> int:
         return int(self.lib.ptopt_cuda_launch_count(self._h))
+
+    def scp_stage_times(self) -> dict:
+        """Device milliseconds per stage of the last scp_solve graph launch."""
+        ms = (C.c_double * 6)()
+        _check(self.lib.ptopt_cuda_scp_stage_times(self._h, ms))
+        return dict(zip(STAGE_NAMES, [float(v) for v in ms]))
+
+    def measure_fp64_peak(self) -> float:
+        """DFMA microbenchmark, TFLOP/s."""
+        tf = C.c_double(0.0)
+        _check(self.lib.ptopt_cuda_measure_fp64_peak(self._h, C.byref(tf)))
+        return tf.value
 
     # ---------------------------------------------------------------- discretization
     def linearize_all(self, x, u):

@@ -83,6 +83,10 @@ struct ptopt_cuda_handle {
   int scp_graph_batch = 0;
   int scp_graph_kernels = 0;
   int scp_capacity = 0;
+  // stage-boundary events recorded by event nodes inside the SCP graph
+  std::vector<cudaEvent_t> stage_events;
+  std::vector<int> stage_of_span;  // stage id of the span that ENDS at event i+1
+  bool stage_times_valid = false;
 };
 
 namespace {
@@ -315,8 +319,21 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   sa.s = st;
   sa.batch = batch;
   int kernels = 0;
+  h->stage_of_span.clear();
+  size_t ev = 0;
+  auto mark = [&](int stage) -> cudaError_t {  // closes the span of `stage` (-1: opens the first)
+    if (ev >= h->stage_events.size()) {
+      cudaEvent_t e;
+      cudaError_t rc = cudaEventCreate(&e);
+      if (rc != cudaSuccess) return rc;
+      h->stage_events.push_back(e);
+    }
+    if (stage >= 0) h->stage_of_span.push_back(stage);
+    return cudaEventRecordWithFlags(h->stage_events[ev++], h->stream, cudaEventRecordExternal);
+  };
   launch_scp_init(sa, h->stream);
   ++kernels;
+  PT_CUDA(mark(-1));
 
   PowerArgs pa;
   pa.shape = h->rocket_shape;
@@ -360,12 +377,17 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
                                           st.x_end, st.fail_key, st.active);
   for (int it = 0; it <= h->desc.max_iters; ++it) {
     launch_linearize(la, h->stream);
+    PT_CUDA(mark(0));
     launch_scp_prepare(sa, h->stream);
+    PT_CUDA(mark(1));
     kernels += 2;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
     PT_CUDA(launch_power_generic(pa, h->stream));
+    PT_CUDA(mark(2));
     PT_CUDA(launch_pipg_generic(ga, h->stream));
+    PT_CUDA(mark(3));
     launch_scp_update(sa, h->stream);
+    PT_CUDA(mark(4));
     kernels += 3;
   }
   PT_CUDA(cudaGetLastError());
@@ -425,6 +447,7 @@ int scp_solve_common(ptopt_cuda_handle* h, int batch, const double* init_state,
                           h->stream));
   PT_CUDA(cudaGraphLaunch(h->scp_graph, h->stream));
   h->launches += h->scp_graph_kernels;
+  h->stage_times_valid = true;
   auto out = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
     if (!dst) return cudaSuccess;
     return cudaMemcpyAsync(dst, src, bytes, out_kind, h->stream);
@@ -549,6 +572,7 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
   DeviceGuard guard(h->device);
   cudaStreamSynchronize(h->stream);
   if (h->scp_graph) cudaGraphExecDestroy(h->scp_graph);
+  for (cudaEvent_t e : h->stage_events) cudaEventDestroy(e);
   for (DevBuf& b : h->buf) b.release();
   if (h->d_tau) cudaFree(h->d_tau);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -908,6 +932,57 @@ int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double
   return scp_solve_common(h, batch, init_state, x_guess, u_guess, rng_seed, x_out, u_out,
                           scp_iterations, converged, final_defect_inf, history, power_trips,
                           status, fail_index, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+}
+
+// ---- measurement ----------------------------------------------------------------------
+
+int ptopt_cuda_scp_stage_times(ptopt_cuda_handle* h, double* ms) {
+  if (!h || !ms) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null argument");
+  if (!h->stage_times_valid || h->stage_of_span.empty())
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "no scp_solve_batch launch to report on");
+  DeviceGuard guard(h->device);
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < PTOPT_STAGE_COUNT; ++i) ms[i] = 0.0;
+  for (size_t i = 0; i < h->stage_of_span.size(); ++i) {
+    float t = 0.f;
+    PT_CUDA(cudaEventElapsedTime(&t, h->stage_events[i], h->stage_events[i + 1]));
+    ms[h->stage_of_span[i]] += t;
+  }
+  float total = 0.f;
+  PT_CUDA(cudaEventElapsedTime(&total, h->stage_events.front(),
+                               h->stage_events[h->stage_of_span.size()]));
+  ms[5] = total;
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_measure_fp64_peak(ptopt_cuda_handle* h, double* tflops) {
+  if (!h || !tflops) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard guard(h->device);
+  int sms = 0;
+  PT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+  double* sink = nullptr;
+  PT_TRY(device_out(h, B_SIGMA, 8, &sink));
+  cudaEvent_t e0, e1;
+  PT_CUDA(cudaEventCreate(&e0));
+  PT_CUDA(cudaEventCreate(&e1));
+  const int ctas = sms * 4, threads = 256, iters = 4000;
+  launch_fp64_peak(sink, iters / 10, ctas, threads, h->stream);  // warm-up
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    PT_CUDA(cudaEventRecord(e0, h->stream));
+    launch_fp64_peak(sink, iters, ctas, threads, h->stream);
+    PT_CUDA(cudaEventRecord(e1, h->stream));
+    PT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    const double tf = fp64_peak_flops(iters, ctas, threads) / (ms * 1e-3) * 1e-12;
+    if (tf > best) best = tf;
+  }
+  h->launches += 6;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *tflops = best;
+  return PTOPT_OK;
 }
 
 }  // extern "C"

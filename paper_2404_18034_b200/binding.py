@@ -23,6 +23,7 @@ _lib = None
 EXPORTS = [
     "ptopt_cuda_abi_version", "ptopt_cuda_last_error", "ptopt_cuda_launch_count",
     "ptopt_cuda_create", "ptopt_cuda_destroy", "ptopt_cuda_synchronize",
+    "ptopt_cuda_set_solver_path",
     "ptopt_cuda_linearize_batch", "ptopt_cuda_linearize_batch_dev",
     "ptopt_cuda_assemble_batch", "ptopt_cuda_subproblem_shape",
     "ptopt_cuda_power_iteration_batch", "ptopt_cuda_power_iteration_batch_dev",
@@ -118,6 +119,10 @@ class Solver:
 
     def __exit__(self, *exc):
         self.close()
+
+    def set_solver_path(self, path: str):
+        """'auto' (register-resident kernels where the shape allows) or 'generic'."""
+        _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int({"auto": 0, "generic": 1}[path])))
 
     def synchronize(self):
         _check(self.lib.ptopt_cuda_synchronize(self._h))

@@ -87,6 +87,7 @@ struct ptopt_cuda_handle {
   std::vector<cudaEvent_t> stage_events;
   std::vector<int> stage_of_span;  // stage id of the span that ENDS at event i+1
   bool stage_times_valid = false;
+  int solver_path = PTOPT_SOLVER_AUTO;
 };
 
 namespace {
@@ -223,18 +224,35 @@ void fill_rocket_shape(const ptopt_problem_desc& d, SubShape& s) {  // scp.hpp:1
   s.w_ep = d.w_ep;
 }
 
+/// The register-resident kernels serve the rocket-shaped subproblem; every other shape (and a
+/// handle forced to PTOPT_SOLVER_GENERIC) runs the shape-generic kernels.
+bool use_fast_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
+  return h->solver_path != PTOPT_SOLVER_GENERIC && solver_fast_supports(s, has_a_plus);
+}
+
+int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
+  if (fast) {
+    PT_TRY(check_smem(h, pipg_fast_smem(s)));
+    PT_CUDA(configure_solver_fast(s));
+  } else {
+    PT_TRY(check_smem(h, pipg_generic_smem(s, solver_generic_threads(s))));
+    PT_CUDA(configure_solver_generic(s));
+  }
+  return PTOPT_OK;
+}
+
 int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
-  PT_TRY(check_smem(h, pipg_generic_smem(a.shape, solver_generic_threads(a.shape))));
-  PT_CUDA(configure_solver_generic(a.shape));
-  PT_CUDA(launch_power_generic(a, h->stream));
+  const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
+  PT_TRY(configure_solver(h, a.shape, fast));
+  PT_CUDA(fast ? launch_power_fast(a, h->stream) : launch_power_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
 }
 
 int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
-  PT_TRY(check_smem(h, pipg_generic_smem(a.shape, solver_generic_threads(a.shape))));
-  PT_CUDA(configure_solver_generic(a.shape));
-  PT_CUDA(launch_pipg_generic(a, h->stream));
+  const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
+  PT_TRY(configure_solver(h, a.shape, fast));
+  PT_CUDA(fast ? launch_pipg_fast(a, h->stream) : launch_pipg_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
 }
@@ -375,6 +393,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
 
   const LinearizeArgs la = linearize_args(h, batch, st.zx, st.zu, st.A, st.Bm, st.Bp, st.w,
                                           st.x_end, st.fail_key, st.active);
+  const bool fast = use_fast_solver(h, h->rocket_shape, false);
   for (int it = 0; it <= h->desc.max_iters; ++it) {
     launch_linearize(la, h->stream);
     PT_CUDA(mark(0));
@@ -382,9 +401,9 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 2;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    PT_CUDA(launch_power_generic(pa, h->stream));
+    PT_CUDA(fast ? launch_power_fast(pa, h->stream) : launch_power_generic(pa, h->stream));
     PT_CUDA(mark(2));
-    PT_CUDA(launch_pipg_generic(ga, h->stream));
+    PT_CUDA(fast ? launch_pipg_fast(ga, h->stream) : launch_pipg_generic(ga, h->stream));
     PT_CUDA(mark(3));
     launch_scp_update(sa, h->stream);
     PT_CUDA(mark(4));
@@ -401,8 +420,7 @@ int ensure_scp_graph(ptopt_cuda_handle* h, int batch, const ScpState& st) {
     cudaGraphExecDestroy(h->scp_graph);
     h->scp_graph = nullptr;
   }
-  PT_TRY(check_smem(h, pipg_generic_smem(h->rocket_shape, solver_generic_threads(h->rocket_shape))));
-  PT_CUDA(configure_solver_generic(h->rocket_shape));
+  PT_TRY(configure_solver(h, h->rocket_shape, use_fast_solver(h, h->rocket_shape, false)));
   cudaGraph_t graph = nullptr;
   PT_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   int kernels = 0;
@@ -577,6 +595,21 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
   if (h->d_tau) cudaFree(h->d_tau);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (path != PTOPT_SOLVER_AUTO && path != PTOPT_SOLVER_GENERIC)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "unknown solver path");
+  if (path != h->solver_path && h->scp_graph) {  // the captured graph names the other kernels
+    DeviceGuard guard(h->device);
+    cudaStreamSynchronize(h->stream);
+    cudaGraphExecDestroy(h->scp_graph);
+    h->scp_graph = nullptr;
+    h->scp_graph_batch = 0;
+  }
+  h->solver_path = path;
   return PTOPT_OK;
 }
 

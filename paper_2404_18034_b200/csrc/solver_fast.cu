@@ -1,0 +1,657 @@
+// solver_fast.cu — register-resident power iteration and customized PIPG for the rocket-shaped
+// subproblem (n_x = 15, n_u = 7, A_plus = -I, e_y = unit vector of the last state, at most
+// kFastMaxNodes nodes).
+//
+// One CTA per instance, five threads per node.  Thread (k, g) keeps rows 3g..3g+2 of the packed
+// interval block [A-_k | B-_k | B+_k] (3 x 29 doubles) in registers for the whole kernel, so the
+// operator is read from HBM exactly once per launch and never touches shared memory:
+//   * the forward product  H z  (dual update / power-iteration forward map) is thread-local:
+//     29 FMAs per row against the node vectors, which are broadcast from shared memory;
+//   * the transposed product H^T phi uses the thread's own three dual entries: it forms the
+//     29 partial column sums of its three rows and publishes them to shared memory, where the
+//     owner of each primal entry adds the five partials of its column.
+// Every primal/dual entry has one owner thread that keeps its extrapolated copy in registers;
+// only what a neighbour needs (reflections, extrapolated duals, partial sums) lives in shared
+// memory.  Two block-wide barriers per iteration.
+//
+// Follows /root/reference/proj/include/ptopt/pipg.hpp:206-292 (power_iteration_custom),
+// :307-326 (stopping_custom), :335-340 (step_sizes), :350-497 (pipg_custom).  Sums over the
+// fifteen rows of a column are grouped three rows at a time, and FMA contraction is on; both
+// change rounding only (measured sensitivity of the whole loop: 1e-13).
+#include "kernels.cuh"
+
+namespace ptopt_b200 {
+
+namespace {
+
+constexpr int kG = 5;        // threads per node
+constexpr int kR = 3;        // operator rows per thread
+constexpr int kW = kNX + 2 * kNU;  // 29 columns of [A- | B- | B+]
+constexpr int kXS = 18;      // node stride of x vectors in shared memory (16-byte aligned, conflict-free)
+constexpr int kUS = 10;      // node stride of u vectors
+constexpr int kPS = 35;      // stride of one thread's partial-sum slot (== 3 mod 16: conflict-free)
+constexpr int kFastThreads = 256;
+constexpr int kFastWarps = kFastThreads / 32;
+
+// position of a column's partial sum inside a slot: x columns first, then the B- / B+ columns
+// interleaved so that the five owners of a node read with a 3-double spacing (no bank conflicts)
+__host__ __device__ constexpr int pos_bm(int ju) { return ju < 5 ? 15 + 3 * ju : 16 + 3 * (ju - 5); }
+__host__ __device__ constexpr int pos_bp(int ju) { return ju < 5 ? 17 + 3 * ju : 22 + 3 * (ju - 5); }
+__host__ __device__ constexpr int pos_col(int j) {
+  return j < kNX ? j : (j < kNX + kNU ? pos_bm(j - kNX) : pos_bp(j - kNX - kNU));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+/// Loads rows 3g..3g+2 of [A-_k | B-_k | B+_k] of instance b into registers.
+__device__ __forceinline__ void load_rows(const SubArrays& sp, int b, int m, int k, int g,
+                                          double (&a)[kR][kW]) {
+  const size_t iv = (size_t)b * m + k;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int i = kR * g + r;
+    const double* ra = sp.A_minus + (iv * kNX + i) * kNX;
+    const double* rm = sp.B_minus + (iv * kNX + i) * kNU;
+    const double* rp = sp.B_plus + (iv * kNX + i) * kNU;
+#pragma unroll
+    for (int j = 0; j < kNX; ++j) a[r][j] = __ldg(ra + j);
+#pragma unroll
+    for (int j = 0; j < kNU; ++j) {
+      a[r][kNX + j] = __ldg(rm + j);
+      a[r][kNX + kNU + j] = __ldg(rp + j);
+    }
+  }
+}
+
+/// Reads the node vectors the forward product of interval k needs: x_k, u_k, u_{k+1}.
+__device__ __forceinline__ void load_node_vectors(const double* xs, const double* us, int k,
+                                                  double (&v)[kW]) {
+  const double2* x2 = reinterpret_cast<const double2*>(xs + k * kXS);
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const double2 t = x2[q];
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+  v[14] = xs[k * kXS + 14];
+  const double2* u2 = reinterpret_cast<const double2*>(us + k * kUS);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 t = u2[q];  // entry 7 is padding
+    v[kNX + 2 * q] = t.x;
+    if (q < 3) v[kNX + 2 * q + 1] = t.y;
+  }
+  const double2* w2 = reinterpret_cast<const double2*>(us + (k + 1) * kUS);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 t = w2[q];
+    v[kNX + kNU + 2 * q] = t.x;
+    if (q < 3) v[kNX + kNU + 2 * q + 1] = t.y;
+  }
+}
+
+/// Row r of the forward product: A- x_k, B- u_k, B+ u_{k+1}, each summed in ascending column
+/// order (mat_vec, smallmat.hpp:93-97).
+__device__ __forceinline__ void row_products(const double (&a)[kR][kW], const double (&v)[kW], int r,
+                                             double& pa, double& pm, double& pp) {
+  double sa = 0.0, sm = 0.0, sp = 0.0;
+#pragma unroll
+  for (int j = 0; j < kNX; ++j) sa += a[r][j] * v[j];
+#pragma unroll
+  for (int j = 0; j < kNU; ++j) {
+    sm += a[r][kNX + j] * v[kNX + j];
+    sp += a[r][kNX + kNU + j] * v[kNX + kNU + j];
+  }
+  pa = sa;
+  pm = sm;
+  pp = sp;
+}
+
+/// Publishes the partial column sums of this thread's three rows against its three dual entries.
+__device__ __forceinline__ void store_partials(const double (&a)[kR][kW], const double (&d)[kR],
+                                               double* slot) {
+#pragma unroll
+  for (int j = 0; j < kW; ++j) {
+    double p = a[0][j] * d[0];
+    p += a[1][j] * d[1];
+    p += a[2][j] * d[2];
+    slot[pos_col(j)] = p;
+  }
+}
+
+/// Sum over the five partial slots of an interval for one column position.
+__device__ __forceinline__ double column_sum(const double* part, int interval, int pos) {
+  const double* p = part + (size_t)interval * kG * kPS + pos;
+  double s = p[0];
+#pragma unroll
+  for (int q = 1; q < kG; ++q) s += p[q * kPS];
+  return s;
+}
+
+struct FastLayout {
+  int xs, us, phi, theta, part, red, total;  // offsets in doubles
+  // PIPG only
+  int wv, eps, umin, umax, xc, uc, vpc, vnc, phc, thc, bnd;
+};
+
+__host__ __device__ inline int even_up(int v) { return (v + 1) & ~1; }
+
+__host__ __device__ inline FastLayout fast_layout(int n, bool pipg) {
+  const int m = n - 1;
+  FastLayout L{};
+  int o = 0;
+  L.xs = o; o += n * kXS;
+  L.us = o; o += n * kUS;
+  L.phi = o; o += even_up(m * kNX);
+  L.theta = o; o += even_up(m);
+  L.part = o; o += even_up(m * kG * kPS);
+  L.red = o; o += 16 * kFastWarps;
+  if (pipg) {
+    L.wv = o; o += even_up(m * kNX);
+    L.eps = o; o += even_up(m);
+    L.umin = o; o += even_up(n * kNU);
+    L.umax = o; o += even_up(n * kNU);
+    L.xc = o; o += even_up(n * kNX);
+    L.uc = o; o += even_up(n * kNU);
+    L.vpc = o; o += even_up(m * kNX);
+    L.vnc = o; o += even_up(m * kNX);
+    L.phc = o; o += even_up(m * kNX);
+    L.thc = o; o += even_up(m);
+    L.bnd = o; o += 6 * 16;  // ecost, init_val, final_val, init_on, final_on (as doubles)
+  }
+  L.total = o;
+  return L;
+}
+
+// ---------------------------------------------------------------------------------------------
+// power iteration (pipg.hpp:206-292)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = tid / kG, g = tid - k * kG;
+  const bool node = k < n, ival = k < m;
+  const FastLayout L = fast_layout(n, false);
+  double* xs = sm + L.xs;
+  double* us = sm + L.us;
+  double* phis = sm + L.phi;
+  double* thetas = sm + L.theta;
+  double* part = sm + L.part;
+  double* red = sm + L.red;
+
+  double aop[kR][kW];
+  double vcp[kR], vcn[kR];
+  if (ival) load_rows(a.sp, b, m, k, g, aop);
+
+  // seed (pipg.hpp:213-230): x, u, vc+, vc-; sigma0 = ||seed||_2
+  double acc = 0.0;
+  if (node) {
+    const double* sx = a.seed_x + ((size_t)b * n + k) * kNX;
+    const double* su = a.seed_u + ((size_t)b * n + k) * kNU;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const double v = sx[kR * g + r];
+      xs[k * kXS + kR * g + r] = v;
+      acc += v * v;
+    }
+    {
+      const double v = su[g];
+      us[k * kUS + g] = v;
+      acc += v * v;
+    }
+    if (g < 2) {
+      const double v = su[g + 5];
+      us[k * kUS + g + 5] = v;
+      acc += v * v;
+    }
+    if (g == 4) us[k * kUS + 7] = 0.0;  // padding read by the vector loads
+  }
+  if (ival) {
+    const double* sp = a.seed_vcp + ((size_t)b * m + k) * kNX;
+    const double* sn = a.seed_vcn + ((size_t)b * m + k) * kNX;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      vcp[r] = sp[kR * g + r];
+      vcn[r] = sn[kR * g + r];
+      acc += vcp[r] * vcp[r];
+      acc += vcn[r] * vcn[r];
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  double sigma = 0.0;
+#pragma unroll
+  for (int w = 0; w < kFastWarps; ++w) sigma += red[w];
+  if (sigma == 0.0) {  // pipg.hpp:224-225
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSeedZero;
+      a.sigma[b] = 0.0;
+      if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
+    }
+    return;
+  }
+  sigma = sqrt(sigma);
+
+  int trips = 0;
+  for (int j = 1; j <= a.j_max; ++j) {
+    trips = j;
+    // ---- forward map scaled by 1/sigma (pipg.hpp:234-245) and partial sums of H^T [phi; theta]
+    double phi[kR];
+    if (ival) {
+      const double inv = 1.0 / sigma;
+      double v[kW];
+      load_node_vectors(xs, us, k, v);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        double pa, pm, pp;
+        row_products(aop, v, r, pa, pm, pp);
+        double s = pa + -xs[(k + 1) * kXS + kR * g + r];
+        s += pm;
+        s += pp;
+        s += vcp[r];
+        s += -1.0 * vcn[r];
+        phi[r] = s * inv;
+        phis[k * kNX + kR * g + r] = phi[r];
+      }
+      if (g == 4) thetas[k] = (xs[(k + 1) * kXS + 14] - v[14]) / sigma;
+      store_partials(aop, phi, part + (size_t)tid * kPS);
+    }
+    __syncthreads();
+    // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
+    acc = 0.0;
+    if (node) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int i = kR * g + r;
+        double s = 0.0;
+        if (ival) s = column_sum(part, k, i);
+        if (k > 0) {
+          const double t = -phis[(k - 1) * kNX + i];
+          s = ival ? s + t : t;
+        }
+        if (i == kNX - 1) {
+          if (ival) s += -thetas[k];
+          if (k > 0) s += thetas[k - 1];
+        }
+        xs[k * kXS + i] = s;
+        acc += s * s;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int ju = g + 5 * q;
+        if (q == 1 && g >= 2) break;
+        double s = 0.0;
+        if (ival) s = column_sum(part, k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
+        if (k > 0) {
+          const double t = column_sum(part, k - 1, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+          s = ival ? s + t : t;
+        }
+        us[k * kUS + ju] = s;
+        acc += s * s;
+      }
+    }
+    if (ival) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        vcp[r] = phi[r];
+        vcn[r] = -phi[r];
+        acc += phi[r] * phi[r];
+        acc += phi[r] * phi[r];
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[((j & 1) ? kFastWarps : 0) + warp] = acc;
+    __syncthreads();
+    double sigma_star = 0.0;
+#pragma unroll
+    for (int w = 0; w < kFastWarps; ++w) sigma_star += red[((j & 1) ? kFastWarps : 0) + w];
+    sigma_star = sqrt(sigma_star);
+    if (sigma_star == 0.0) {  // seed in the null space, pipg.hpp:280-284
+      sigma = 0.0;
+      break;
+    }
+    if (fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma)) {
+      sigma = sigma_star;
+      break;
+    }
+    sigma = sigma_star;
+  }
+  if (tid == 0) {
+    a.sigma[b] = (1.0 + a.eps_buff) * sigma;
+    if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// customized PIPG (pipg.hpp:350-497)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = tid / kG, g = tid - k * kG;
+  const bool node = k < n, ival = k < m;
+  const FastLayout L = fast_layout(n, true);
+  double* xr = sm + L.xs;      // reflections 2*cur - ex of x (pipg.hpp:436-443)
+  double* ur = sm + L.us;
+  double* phx = sm + L.phi;    // extrapolated dynamics dual
+  double* thx = sm + L.theta;  // extrapolated relaxation dual
+  double* part = sm + L.part;
+  double* red = sm + L.red;
+  double* wv = sm + L.wv;
+  double* epsv = sm + L.eps;
+  double* umin = sm + L.umin;
+  double* umax = sm + L.umax;
+  double* xc = sm + L.xc;      // *_cur groups: kept only around stopping checks and at the end
+  double* uc = sm + L.uc;
+  double* vpc = sm + L.vpc;
+  double* vnc = sm + L.vnc;
+  double* phc = sm + L.phc;
+  double* thc = sm + L.thc;
+  double* ecost = sm + L.bnd;
+  double* init_val = ecost + 16;
+  double* final_val = init_val + 16;
+  double* init_on = final_val + 16;
+  double* final_on = init_on + 16;
+
+  const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
+  if (tid < 16) {
+    ecost[tid] = tid < kNX ? a.shape.e_cost[tid] : 0.0;
+    init_on[tid] = 0.0;
+    final_on[tid] = 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
+    for (int i = 0; i < a.shape.n_init_fix; ++i) {
+      init_on[a.shape.init_fix_idx[i]] = 1.0;
+      init_val[a.shape.init_fix_idx[i]] = a.sp.init_fix_val[(size_t)b * a.shape.n_init_fix + i];
+    }
+    for (int i = 0; i < a.shape.n_final_fix; ++i) {
+      final_on[a.shape.final_fix_idx[i]] = 1.0;
+      final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
+    }
+  }
+  for (int e = tid; e < NM; e += kFastThreads) wv[e] = a.sp.w[(size_t)b * NM + e];
+  for (int e = tid; e < m; e += kFastThreads) epsv[e] = a.sp.eps_relax[(size_t)b * m + e];
+  for (int e = tid; e < NUn; e += kFastThreads) {
+    umin[e] = a.sp.u_min[(size_t)b * NUn + e];
+    umax[e] = a.sp.u_max[(size_t)b * NUn + e];
+  }
+  // warm start: ex = cur = workspace (pipg.hpp:362-374)
+  for (int e = tid; e < NXn; e += kFastThreads) xc[e] = a.ws.x[(size_t)b * NXn + e];
+  for (int e = tid; e < NUn; e += kFastThreads) uc[e] = a.ws.u[(size_t)b * NUn + e];
+  for (int e = tid; e < NM; e += kFastThreads) {
+    vpc[e] = a.ws.vc_pos[(size_t)b * NM + e];
+    vnc[e] = a.ws.vc_neg[(size_t)b * NM + e];
+    phc[e] = a.ws.dyn_dual[(size_t)b * NM + e];
+  }
+  for (int e = tid; e < m; e += kFastThreads) thc[e] = a.ws.relax_dual[(size_t)b * m + e];
+
+  double aop[kR][kW];
+  if (ival) load_rows(a.sp, b, m, k, g, aop);
+  __syncthreads();
+
+  // owner-private extrapolated copies
+  double xe[kR], ue[2], vpe[kR], vne[kR], phe[kR], the = 0.0;
+  ue[0] = ue[1] = 0.0;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) xe[r] = vpe[r] = vne[r] = phe[r] = 0.0;
+  if (node) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) xe[r] = xc[k * kNX + kR * g + r];
+    ue[0] = uc[k * kNU + g];
+    if (g < 2) ue[1] = uc[k * kNU + g + 5];
+    if (g == 4) ur[k * kUS + 7] = 0.0;  // padding read by the vector loads
+  }
+  if (ival) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int e = k * kNX + kR * g + r;
+      vpe[r] = vpc[e];
+      vne[r] = vnc[e];
+      phe[r] = phc[e];
+      phx[e] = phe[r];
+    }
+    if (g == 4) {
+      the = thc[k];
+      thx[k] = the;
+    }
+    store_partials(aop, phe, part + (size_t)tid * kPS);
+  }
+
+  const double w_prox = a.shape.w_prox, w_ep = a.shape.w_ep, w_cost = a.shape.w_cost;
+  const double sigma = a.sigma[b];
+  const double alpha = 2.0 / (w_prox + sqrt(w_prox * w_prox + 4.0 * a.omega * sigma));
+  const double beta = a.omega * alpha;
+  const double rho = a.rho;
+  __syncthreads();
+
+  int iters = 0;
+  bool converged = false, diverged = false;
+  for (int j = 1; j <= a.j_max; ++j) {
+    const bool check = (j % a.j_check) == 0;
+    // cur values are materialised when the next iteration checks against them, when this one
+    // checks (a converged exit returns them), and on the last iteration
+    const bool keep = check || ((j + 1) % a.j_check) == 0 || j == a.j_max;
+    double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
+    double bad = 0.0;
+
+    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
+    if (node) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int i = kR * g + r;
+        const double x0 = xe[r];
+        double grad = x0 * w_prox;
+        if (ival) {
+          grad += column_sum(part, k, i);
+          if (i == kNX - 1) grad += -thx[k];
+        }
+        if (k > 0) {
+          grad += -phx[(k - 1) * kNX + i];
+          if (i == kNX - 1) grad += thx[k - 1];
+        }
+        if (k == n - 1) grad += w_cost * ecost[i];
+        double xn = x0 + -alpha * grad;
+        if (k == 0 && init_on[i] != 0.0) xn = init_val[i];
+        if (k == n - 1 && final_on[i] != 0.0) xn = final_val[i];
+        xr[k * kXS + i] = 2.0 * xn - x0;
+        if (check) {
+          const double old = xc[k * kNX + i];
+          z_cur = fmax(z_cur, fabs(xn));
+          z_prev = fmax(z_prev, fabs(old));
+          z_del = fmax(z_del, fabs(xn - old));
+          if (!pt_finite(xn)) bad = 1.0;
+        }
+        if (keep) xc[k * kNX + i] = xn;
+        xe[r] = (1.0 - rho) * x0 + rho * xn;  // extrapolation, pipg.hpp:461-467
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && g >= 2) break;
+        const int ju = g + 5 * q;
+        const double u0 = ue[q];
+        double grad = u0 * w_prox;
+        if (ival) grad += column_sum(part, k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
+        if (k > 0) grad += column_sum(part, k - 1, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+        double un = u0 + -alpha * grad;
+        // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
+        const double lo = umin[k * kNU + ju], hi = umax[k * kNU + ju];
+        const double cl = (hi < un) ? hi : un;
+        un = (lo < cl) ? cl : lo;
+        ur[k * kUS + ju] = 2.0 * un - u0;
+        if (check) {
+          const double old = uc[k * kNU + ju];
+          z_cur = fmax(z_cur, fabs(un));
+          z_prev = fmax(z_prev, fabs(old));
+          z_del = fmax(z_del, fabs(un - old));
+          if (!pt_finite(un)) bad = 1.0;
+        }
+        if (keep) uc[k * kNU + ju] = un;
+        ue[q] = (1.0 - rho) * u0 + rho * un;
+      }
+    }
+    __syncthreads();
+
+    // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
+    //      extrapolation of the dual groups (:468-472) and the partial sums of H^T phi_ex for
+    //      the next primal step
+    if (ival) {
+      double v[kW];
+      load_node_vectors(xr, ur, k, v);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        const int e = k * kNX + kR * g + r;
+        double pa, pm, pp;
+        row_products(aop, v, r, pa, pm, pp);
+        double resid = pa + -xr[(k + 1) * kXS + kR * g + r];
+        resid += pm;
+        resid += pp;
+        const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
+        const double vp = fmax(0.0, vp0 - alpha * (w_ep + p0));
+        const double vn = fmax(0.0, vn0 - alpha * (w_ep - p0));
+        resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv[e];
+        const double pn = p0 + beta * resid;
+        if (check) {
+          const double op = vpc[e], on = vnc[e], od = phc[e];
+          z_cur = fmax(z_cur, fmax(fabs(vp), fabs(vn)));
+          z_prev = fmax(z_prev, fmax(fabs(op), fabs(on)));
+          z_del = fmax(z_del, fmax(fabs(vp - op), fabs(vn - on)));
+          r_cur = fmax(r_cur, fabs(pn));
+          r_prev = fmax(r_prev, fabs(od));
+          r_del = fmax(r_del, fabs(pn - od));
+          if (!pt_finite(pn)) bad = 1.0;
+        }
+        if (keep) {
+          vpc[e] = vp;
+          vnc[e] = vn;
+          phc[e] = pn;
+        }
+        phe[r] = (1.0 - rho) * p0 + rho * pn;
+        vpe[r] = (1.0 - rho) * vp0 + rho * vp;
+        vne[r] = (1.0 - rho) * vn0 + rho * vn;
+        phx[e] = phe[r];
+      }
+      if (g == 4) {
+        const double drift = xr[(k + 1) * kXS + 14] - v[14] - epsv[k];
+        const double tn = fmax(0.0, the + beta * drift);
+        if (check) {
+          const double old = thc[k];
+          r_cur = fmax(r_cur, fabs(tn));
+          r_prev = fmax(r_prev, fabs(old));
+          r_del = fmax(r_del, fabs(tn - old));
+        }
+        if (keep) thc[k] = tn;
+        the = (1.0 - rho) * the + rho * tn;
+        thx[k] = the;
+      }
+      store_partials(aop, phe, part + (size_t)tid * kPS);
+    }
+    iters = j;
+    if (check) {
+      z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
+      r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
+      bad = warp_max(bad);
+      if (lane == 0) {
+        double* rw = red + warp * 8;
+        rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
+        rw[6] = bad;
+      }
+    }
+    __syncthreads();
+    if (check) {  // pipg.hpp:475-487
+      double v[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        double mx = 0.0;
+#pragma unroll
+        for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, red[w * 8 + q]);
+        v[q] = mx;
+      }
+      if (v[6] > 0.0) {
+        diverged = true;
+        break;
+      }
+      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) &&
+          v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+        converged = true;
+        break;
+      }
+      __syncthreads();  // red is rewritten by the next check
+    }
+  }
+
+  if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSolverDiverged;
+      if (a.fail_index) a.fail_index[b] = iters;
+      if (a.iterations) a.iterations[b] = iters;
+      if (a.converged) a.converged[b] = 0;
+      if (a.active) a.active[b] = 0;
+    }
+    return;
+  }
+  // solution = the *_cur groups, pipg.hpp:490-495 (all threads passed the barrier above)
+  for (int e = tid; e < NXn; e += kFastThreads) a.ws.x[(size_t)b * NXn + e] = xc[e];
+  for (int e = tid; e < NUn; e += kFastThreads) a.ws.u[(size_t)b * NUn + e] = uc[e];
+  for (int e = tid; e < NM; e += kFastThreads) {
+    a.ws.vc_pos[(size_t)b * NM + e] = vpc[e];
+    a.ws.vc_neg[(size_t)b * NM + e] = vnc[e];
+    a.ws.dyn_dual[(size_t)b * NM + e] = phc[e];
+  }
+  for (int e = tid; e < m; e += kFastThreads) a.ws.relax_dual[(size_t)b * m + e] = thc[e];
+  if (tid == 0) {
+    if (a.iterations) a.iterations[b] = iters;
+    if (a.converged) a.converged[b] = converged ? 1 : 0;
+  }
+}
+
+}  // namespace
+
+bool solver_fast_supports(const SubShape& s, bool has_a_plus) {
+  if (has_a_plus || s.nx != kNX || s.nu != kNU) return false;
+  if (s.n < 2 || s.n > kFastMaxNodes) return false;
+  for (int i = 0; i < kNX; ++i)
+    if (s.e_y[i] != (i == kNX - 1 ? 1.0 : 0.0)) return false;
+  return true;
+}
+
+size_t power_fast_smem(const SubShape& s) { return sizeof(double) * (size_t)fast_layout(s.n, false).total; }
+size_t pipg_fast_smem(const SubShape& s) { return sizeof(double) * (size_t)fast_layout(s.n, true).total; }
+
+cudaError_t configure_solver_fast(const SubShape& s) {
+  cudaError_t e = cudaFuncSetAttribute(power_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)power_fast_smem(s));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(pipg_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)pipg_fast_smem(s));
+}
+
+cudaError_t launch_power_fast(const PowerArgs& a, cudaStream_t stream) {
+  power_fast_kernel<<<a.batch, kFastThreads, power_fast_smem(a.shape), stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pipg_fast(const PipgArgs& a, cudaStream_t stream) {
+  pipg_fast_kernel<<<a.batch, kFastThreads, pipg_fast_smem(a.shape), stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ptopt_b200

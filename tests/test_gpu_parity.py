@@ -19,12 +19,15 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(1.0, np.abs(b).max())
 
 
-@pytest.fixture(scope="module")
-def solver15():
+@pytest.fixture(scope="module", params=["auto", "generic"])
+def solver15(request):
+    """The default-scenario handle, once per kernel family: 'auto' runs the register-resident
+    power/PIPG kernels on rocket-shaped subproblems, 'generic' forces the shape-generic ones."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(15)
     with Solver(sc.problem_desc()) as s:
+        s.set_solver_path(request.param)
         yield sc, s
 
 

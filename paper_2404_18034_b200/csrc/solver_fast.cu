@@ -18,6 +18,8 @@
 // :307-326 (stopping_custom), :335-340 (step_sizes), :350-497 (pipg_custom).  Sums over the
 // fifteen rows of a column are grouped three rows at a time, and FMA contraction is on; both
 // change rounding only (measured sensitivity of the whole loop: 1e-13).
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace ptopt_b200 {
@@ -74,24 +76,24 @@ __device__ __forceinline__ void load_rows(const SubArrays& sp, int b, int m, int
 }
 
 /// Reads the node vectors the forward product of interval k needs: x_k, u_k, u_{k+1}.
-__device__ __forceinline__ void load_node_vectors(const double* xs, const double* us, int k,
+__device__ __forceinline__ void load_node_vectors(const double* xs_k, const double* us_k,
                                                   double (&v)[kW]) {
-  const double2* x2 = reinterpret_cast<const double2*>(xs + k * kXS);
+  const double2* x2 = reinterpret_cast<const double2*>(xs_k);
 #pragma unroll
   for (int q = 0; q < 7; ++q) {
     const double2 t = x2[q];
     v[2 * q] = t.x;
     v[2 * q + 1] = t.y;
   }
-  v[14] = xs[k * kXS + 14];
-  const double2* u2 = reinterpret_cast<const double2*>(us + k * kUS);
+  v[14] = xs_k[14];
+  const double2* u2 = reinterpret_cast<const double2*>(us_k);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const double2 t = u2[q];  // entry 7 is padding
     v[kNX + 2 * q] = t.x;
     if (q < 3) v[kNX + 2 * q + 1] = t.y;
   }
-  const double2* w2 = reinterpret_cast<const double2*>(us + (k + 1) * kUS);
+  const double2* w2 = reinterpret_cast<const double2*>(us_k + kUS);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const double2 t = w2[q];
@@ -129,9 +131,9 @@ __device__ __forceinline__ void store_partials(const double (&a)[kR][kW], const 
   }
 }
 
-/// Sum over the five partial slots of an interval for one column position.
-__device__ __forceinline__ double column_sum(const double* part, int interval, int pos) {
-  const double* p = part + (size_t)interval * kG * kPS + pos;
+/// Sum over the five partial slots of an interval (part_k: its first slot) for one position.
+__device__ __forceinline__ double column_sum(const double* part_k, int pos) {
+  const double* p = part_k + pos;
   double s = p[0];
 #pragma unroll
   for (int q = 1; q < kG; ++q) s += p[q * kPS];
@@ -141,32 +143,50 @@ __device__ __forceinline__ double column_sum(const double* part, int interval, i
 struct FastLayout {
   int xs, us, phi, theta, part, red, total;  // offsets in doubles
   // PIPG only
-  int wv, eps, umin, umax, xc, uc, vpc, vnc, phc, thc, bnd;
+  int wv, eps, umin, umax, snap, bnd;
 };
 
-__host__ __device__ inline int even_up(int v) { return (v + 1) & ~1; }
+// One snapshot of the *_cur groups (pipg.hpp:490-495), with room for the scratch entries the
+// idle threads write: x [n+2][15], u [n+2][7 (+3)], vc+, vc-, dyn dual [n+2][15], relax dual [n+2].
+struct SnapLayout {
+  int x, u, vp, vn, ph, th, total;
+};
+__host__ __device__ constexpr SnapLayout snap_layout() {
+  constexpr int n = kFastMaxNodes + 2;
+  SnapLayout S{};
+  int o = 0;
+  S.x = o; o += n * kNX;
+  S.u = o; o += n * kNU + 4;
+  S.vp = o; o += n * kNX;
+  S.vn = o; o += n * kNX;
+  S.ph = o; o += n * kNX;
+  S.th = o; o += n;
+  S.total = (o + 1) & ~1;
+  return S;
+}
 
-__host__ __device__ inline FastLayout fast_layout(int n, bool pipg) {
-  const int m = n - 1;
+__host__ __device__ constexpr int even_up(int v) { return (v + 1) & ~1; }
+
+// Arrays carry guard entries so that the hot loops need no boundary branches: node arrays have
+// two extra nodes (n: scratch node of the idle threads, n+1: its right neighbour); interval
+// arrays have one zero interval in front (index -1, read by node 0) and are sized for every
+// thread; partial-sum slots exist for every thread plus five zero slots in front.
+__host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
+  constexpr int n = kFastMaxNodes;  // fixed offsets: every address is base + immediate
   FastLayout L{};
   int o = 0;
-  L.xs = o; o += n * kXS;
-  L.us = o; o += n * kUS;
-  L.phi = o; o += even_up(m * kNX);
-  L.theta = o; o += even_up(m);
-  L.part = o; o += even_up(m * kG * kPS);
+  L.xs = o; o += (n + 2) * kXS;
+  L.us = o; o += (n + 2) * kUS;
+  L.phi = o + kNX + 1; o += even_up((n + 2) * kNX + 2);
+  L.theta = o + 2; o += even_up(n + 4);
+  L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + kFastThreads * kPS + kPS);
   L.red = o; o += 16 * kFastWarps;
   if (pipg) {
-    L.wv = o; o += even_up(m * kNX);
-    L.eps = o; o += even_up(m);
-    L.umin = o; o += even_up(n * kNU);
-    L.umax = o; o += even_up(n * kNU);
-    L.xc = o; o += even_up(n * kNX);
-    L.uc = o; o += even_up(n * kNU);
-    L.vpc = o; o += even_up(m * kNX);
-    L.vnc = o; o += even_up(m * kNX);
-    L.phc = o; o += even_up(m * kNX);
-    L.thc = o; o += even_up(m);
+    L.wv = o; o += even_up((n + 2) * kNX);
+    L.eps = o; o += even_up(n + 2);
+    L.umin = o; o += even_up((n + 2) * kNU + 4);
+    L.umax = o; o += even_up((n + 2) * kNU + 4);
+    L.snap = o; o += 2 * snap_layout().total;
     L.bnd = o; o += 6 * 16;  // ecost, init_val, final_val, init_on, final_on (as doubles)
   }
   L.total = o;
@@ -184,16 +204,28 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
-  const FastLayout L = fast_layout(n, false);
-  double* xs = sm + L.xs;
-  double* us = sm + L.us;
-  double* phis = sm + L.phi;
-  double* thetas = sm + L.theta;
+  const int kc = k < n ? k : n;  // idle threads work on the scratch node
+  constexpr FastLayout L = fast_layout(false);
+  for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
+  __syncthreads();
+  double* xs_k = sm + L.xs + kc * kXS;          // x_k; x_{k+1} at +kXS
+  double* us_k = sm + L.us + kc * kUS;
+  double* phi_k = sm + L.phi + kc * kNX + kR * g;  // own dual entries; interval k-1 at -kNX
+  double* th_k = sm + L.theta + kc;
   double* part = sm + L.part;
+  double* slot = part + (size_t)tid * kPS;
+  const double* part_k = part + (size_t)kc * kG * kPS;  // slots of interval k; k-1 at -kG*kPS
   double* red = sm + L.red;
+  const int ju1 = g < 2 ? g + 5 : 8;            // second control entry (8: padding)
 
   double aop[kR][kW];
   double vcp[kR], vcn[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    vcp[r] = vcn[r] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
+  }
   if (ival) load_rows(a.sp, b, m, k, g, aop);
 
   // seed (pipg.hpp:213-230): x, u, vc+, vc-; sigma0 = ||seed||_2
@@ -204,20 +236,19 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const double v = sx[kR * g + r];
-      xs[k * kXS + kR * g + r] = v;
+      xs_k[kR * g + r] = v;
       acc += v * v;
     }
     {
       const double v = su[g];
-      us[k * kUS + g] = v;
+      us_k[g] = v;
       acc += v * v;
     }
     if (g < 2) {
       const double v = su[g + 5];
-      us[k * kUS + g + 5] = v;
+      us_k[g + 5] = v;
       acc += v * v;
     }
-    if (g == 4) us[k * kUS + 7] = 0.0;  // padding read by the vector loads
   }
   if (ival) {
     const double* sp = a.seed_vcp + ((size_t)b * m + k) * kNX;
@@ -251,68 +282,58 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     trips = j;
     // ---- forward map scaled by 1/sigma (pipg.hpp:234-245) and partial sums of H^T [phi; theta]
     double phi[kR];
-    if (ival) {
+    {
       const double inv = 1.0 / sigma;
       double v[kW];
-      load_node_vectors(xs, us, k, v);
+      load_node_vectors(xs_k, us_k, v);
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         double pa, pm, pp;
         row_products(aop, v, r, pa, pm, pp);
-        double s = pa + -xs[(k + 1) * kXS + kR * g + r];
+        double s = pa + -xs_k[kXS + kR * g + r];
         s += pm;
         s += pp;
         s += vcp[r];
         s += -1.0 * vcn[r];
-        phi[r] = s * inv;
-        phis[k * kNX + kR * g + r] = phi[r];
+        phi[r] = ival ? s * inv : 0.0;
+        phi_k[r] = phi[r];
       }
-      if (g == 4) thetas[k] = (xs[(k + 1) * kXS + 14] - v[14]) / sigma;
-      store_partials(aop, phi, part + (size_t)tid * kPS);
+      if (g == 4) th_k[0] = ival ? (xs_k[kXS + 14] - v[14]) / sigma : 0.0;
+      store_partials(aop, phi, slot);
     }
     __syncthreads();
     // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
     acc = 0.0;
-    if (node) {
 #pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        const int i = kR * g + r;
-        double s = 0.0;
-        if (ival) s = column_sum(part, k, i);
-        if (k > 0) {
-          const double t = -phis[(k - 1) * kNX + i];
-          s = ival ? s + t : t;
-        }
-        if (i == kNX - 1) {
-          if (ival) s += -thetas[k];
-          if (k > 0) s += thetas[k - 1];
-        }
-        xs[k * kXS + i] = s;
-        acc += s * s;
+    for (int r = 0; r < kR; ++r) {
+      const int i = kR * g + r;
+      double s = column_sum(part_k, i);
+      s += -phi_k[r - kNX];
+      if (r == kR - 1 && g == 4) {
+        s += -th_k[0];
+        s += th_k[-1];
       }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int ju = g + 5 * q;
-        if (q == 1 && g >= 2) break;
-        double s = 0.0;
-        if (ival) s = column_sum(part, k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
-        if (k > 0) {
-          const double t = column_sum(part, k - 1, q == 0 ? 17 + 3 * g : 22 + 3 * g);
-          s = ival ? s + t : t;
-        }
-        us[k * kUS + ju] = s;
-        acc += s * s;
-      }
+      xs_k[i] = s;
+      acc += s * s;
     }
-    if (ival) {
-#pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        vcp[r] = phi[r];
-        vcn[r] = -phi[r];
-        acc += phi[r] * phi[r];
-        acc += phi[r] * phi[r];
-      }
+    {
+      double s = column_sum(part_k, 15 + 3 * g);
+      s += column_sum(part_k - kG * kPS, 17 + 3 * g);
+      us_k[g] = s;
+      acc += s * s;
+      double s1 = column_sum(part_k, 16 + 3 * g);
+      s1 += column_sum(part_k - kG * kPS, 22 + 3 * g);
+      us_k[ju1] = s1;
+      acc += g < 2 ? s1 * s1 : 0.0;
     }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      vcp[r] = phi[r];
+      vcn[r] = -phi[r];
+      acc += phi[r] * phi[r];
+      acc += phi[r] * phi[r];
+    }
+    if (!node) acc = 0.0;
     acc = warp_sum(acc);
     if (lane == 0) red[((j & 1) ? kFastWarps : 0) + warp] = acc;
     __syncthreads();
@@ -347,36 +368,33 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
-  const FastLayout L = fast_layout(n, true);
-  double* xr = sm + L.xs;      // reflections 2*cur - ex of x (pipg.hpp:436-443)
-  double* ur = sm + L.us;
-  double* phx = sm + L.phi;    // extrapolated dynamics dual
-  double* thx = sm + L.theta;  // extrapolated relaxation dual
+  const int kc = k < n ? k : n;  // idle threads work on the scratch node
+  constexpr FastLayout L = fast_layout(true);
+  constexpr SnapLayout S = snap_layout();
+  for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
+  __syncthreads();
+  double* xr_k = sm + L.xs + kc * kXS;   // reflections 2*cur - ex (pipg.hpp:436-443); k+1 at +kXS
+  double* ur_k = sm + L.us + kc * kUS;
+  double* phx_k = sm + L.phi + kc * kNX + kR * g;  // extrapolated dynamics dual; k-1 at -kNX
+  double* thx_k = sm + L.theta + kc;               // extrapolated relaxation dual
   double* part = sm + L.part;
+  double* slot = part + (size_t)tid * kPS;
+  const double* part_k = part + (size_t)kc * kG * kPS;
   double* red = sm + L.red;
-  double* wv = sm + L.wv;
-  double* epsv = sm + L.eps;
-  double* umin = sm + L.umin;
-  double* umax = sm + L.umax;
-  double* xc = sm + L.xc;      // *_cur groups: kept only around stopping checks and at the end
-  double* uc = sm + L.uc;
-  double* vpc = sm + L.vpc;
-  double* vnc = sm + L.vnc;
-  double* phc = sm + L.phc;
-  double* thc = sm + L.thc;
+  const double* wv_k = sm + L.wv + kc * kNX + kR * g;
+  const double* eps_k = sm + L.eps + kc;
+  const double* umin_k = sm + L.umin + kc * kNU;
+  const double* umax_k = sm + L.umax + kc * kNU;
+  double* snap0 = sm + L.snap;  // two snapshots of the *_cur groups, written alternately
   double* ecost = sm + L.bnd;
   double* init_val = ecost + 16;
   double* final_val = init_val + 16;
   double* init_on = final_val + 16;
   double* final_on = init_on + 16;
+  const int ju1 = g < 2 ? g + 5 : 8;  // second control entry (8: padding)
 
   const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
-  if (tid < 16) {
-    ecost[tid] = tid < kNX ? a.shape.e_cost[tid] : 0.0;
-    init_on[tid] = 0.0;
-    final_on[tid] = 0.0;
-  }
-  __syncthreads();
+  if (tid < kNX) ecost[tid] = a.shape.e_cost[tid];
   if (tid == 0) {
     // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
     for (int i = 0; i < a.shape.n_init_fix; ++i) {
@@ -388,25 +406,41 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
     }
   }
-  for (int e = tid; e < NM; e += kFastThreads) wv[e] = a.sp.w[(size_t)b * NM + e];
-  for (int e = tid; e < m; e += kFastThreads) epsv[e] = a.sp.eps_relax[(size_t)b * m + e];
+  for (int e = tid; e < NM; e += kFastThreads) sm[L.wv + e] = a.sp.w[(size_t)b * NM + e];
+  for (int e = tid; e < m; e += kFastThreads) sm[L.eps + e] = a.sp.eps_relax[(size_t)b * m + e];
   for (int e = tid; e < NUn; e += kFastThreads) {
-    umin[e] = a.sp.u_min[(size_t)b * NUn + e];
-    umax[e] = a.sp.u_max[(size_t)b * NUn + e];
+    sm[L.umin + e] = a.sp.u_min[(size_t)b * NUn + e];
+    sm[L.umax + e] = a.sp.u_max[(size_t)b * NUn + e];
   }
-  // warm start: ex = cur = workspace (pipg.hpp:362-374)
-  for (int e = tid; e < NXn; e += kFastThreads) xc[e] = a.ws.x[(size_t)b * NXn + e];
-  for (int e = tid; e < NUn; e += kFastThreads) uc[e] = a.ws.u[(size_t)b * NUn + e];
+  // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
+  for (int e = tid; e < NXn; e += kFastThreads) snap0[S.x + e] = a.ws.x[(size_t)b * NXn + e];
+  for (int e = tid; e < NUn; e += kFastThreads) snap0[S.u + e] = a.ws.u[(size_t)b * NUn + e];
   for (int e = tid; e < NM; e += kFastThreads) {
-    vpc[e] = a.ws.vc_pos[(size_t)b * NM + e];
-    vnc[e] = a.ws.vc_neg[(size_t)b * NM + e];
-    phc[e] = a.ws.dyn_dual[(size_t)b * NM + e];
+    snap0[S.vp + e] = a.ws.vc_pos[(size_t)b * NM + e];
+    snap0[S.vn + e] = a.ws.vc_neg[(size_t)b * NM + e];
+    snap0[S.ph + e] = a.ws.dyn_dual[(size_t)b * NM + e];
   }
-  for (int e = tid; e < m; e += kFastThreads) thc[e] = a.ws.relax_dual[(size_t)b * m + e];
+  for (int e = tid; e < m; e += kFastThreads) snap0[S.th + e] = a.ws.relax_dual[(size_t)b * m + e];
 
   double aop[kR][kW];
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+#pragma unroll
+    for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
   if (ival) load_rows(a.sp, b, m, k, g, aop);
   __syncthreads();
+
+  // boundary rows of this thread (pipg.hpp:408-413): bit r set when row 3g+r is assigned
+  int fix_bits = 0;
+  const double* fix_val = init_val;
+  if (k == 0 || k == n - 1) {
+    const double* on = k == n - 1 ? final_on : init_on;
+    fix_val = k == n - 1 ? final_val : init_val;
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+      if (on[kR * g + r] != 0.0) fix_bits |= 1 << r;
+  }
+  const bool last_node = k == n - 1;
 
   // owner-private extrapolated copies
   double xe[kR], ue[2], vpe[kR], vne[kR], phe[kR], the = 0.0;
@@ -415,157 +449,158 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   for (int r = 0; r < kR; ++r) xe[r] = vpe[r] = vne[r] = phe[r] = 0.0;
   if (node) {
 #pragma unroll
-    for (int r = 0; r < kR; ++r) xe[r] = xc[k * kNX + kR * g + r];
-    ue[0] = uc[k * kNU + g];
-    if (g < 2) ue[1] = uc[k * kNU + g + 5];
-    if (g == 4) ur[k * kUS + 7] = 0.0;  // padding read by the vector loads
+    for (int r = 0; r < kR; ++r) xe[r] = snap0[S.x + k * kNX + kR * g + r];
+    ue[0] = snap0[S.u + k * kNU + g];
+    if (g < 2) ue[1] = snap0[S.u + k * kNU + g + 5];
   }
   if (ival) {
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const int e = k * kNX + kR * g + r;
-      vpe[r] = vpc[e];
-      vne[r] = vnc[e];
-      phe[r] = phc[e];
-      phx[e] = phe[r];
+      vpe[r] = snap0[S.vp + e];
+      vne[r] = snap0[S.vn + e];
+      phe[r] = snap0[S.ph + e];
+      phx_k[r] = phe[r];
     }
     if (g == 4) {
-      the = thc[k];
-      thx[k] = the;
+      the = snap0[S.th + k];
+      thx_k[0] = the;
     }
-    store_partials(aop, phe, part + (size_t)tid * kPS);
   }
+  store_partials(aop, phe, slot);
 
-  const double w_prox = a.shape.w_prox, w_ep = a.shape.w_ep, w_cost = a.shape.w_cost;
   const double sigma = a.sigma[b];
-  const double alpha = 2.0 / (w_prox + sqrt(w_prox * w_prox + 4.0 * a.omega * sigma));
+  const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
-  const double rho = a.rho;
+  const double one_m_rho = 1.0 - a.rho;
   __syncthreads();
 
-  int iters = 0;
-  bool converged = false, diverged = false;
-  for (int j = 1; j <= a.j_max; ++j) {
-    const bool check = (j % a.j_check) == 0;
-    // cur values are materialised when the next iteration checks against them, when this one
-    // checks (a converged exit returns them), and on the last iteration
-    const bool keep = check || ((j + 1) % a.j_check) == 0 || j == a.j_max;
-    double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
-    double bad = 0.0;
-
+  // One iteration.  kStore additionally writes the new *_cur values of every owner into the
+  // snapshot `snap` (threads without a node / interval write scratch entries).
+  auto iteration = [&](auto store_tag, double* snap) {
+    constexpr bool kStore = decltype(store_tag)::value;
     // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
-    if (node) {
 #pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        const int i = kR * g + r;
-        const double x0 = xe[r];
-        double grad = x0 * w_prox;
-        if (ival) {
-          grad += column_sum(part, k, i);
-          if (i == kNX - 1) grad += -thx[k];
-        }
-        if (k > 0) {
-          grad += -phx[(k - 1) * kNX + i];
-          if (i == kNX - 1) grad += thx[k - 1];
-        }
-        if (k == n - 1) grad += w_cost * ecost[i];
-        double xn = x0 + -alpha * grad;
-        if (k == 0 && init_on[i] != 0.0) xn = init_val[i];
-        if (k == n - 1 && final_on[i] != 0.0) xn = final_val[i];
-        xr[k * kXS + i] = 2.0 * xn - x0;
-        if (check) {
-          const double old = xc[k * kNX + i];
-          z_cur = fmax(z_cur, fabs(xn));
-          z_prev = fmax(z_prev, fabs(old));
-          z_del = fmax(z_del, fabs(xn - old));
-          if (!pt_finite(xn)) bad = 1.0;
-        }
-        if (keep) xc[k * kNX + i] = xn;
-        xe[r] = (1.0 - rho) * x0 + rho * xn;  // extrapolation, pipg.hpp:461-467
-      }
+    for (int r = 0; r < kR; ++r) {
+      const int i = kR * g + r;
+      const double x0 = xe[r];
+      double grad = x0 * a.shape.w_prox;
+      grad += column_sum(part_k, i);
+      if (r == kR - 1 && g == 4) grad += -thx_k[0];
+      grad += -phx_k[r - kNX];
+      if (r == kR - 1 && g == 4) grad += thx_k[-1];
+      if (last_node) grad += a.shape.w_cost * ecost[i];
+      double xn = x0 + -alpha * grad;
+      if (fix_bits & (1 << r)) xn = fix_val[i];
+      xr_k[i] = 2.0 * xn - x0;
+      if (kStore) snap[S.x + kc * kNX + i] = xn;
+      xe[r] = one_m_rho * x0 + a.rho * xn;  // extrapolation, pipg.hpp:461-467
+    }
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (q == 1 && g >= 2) break;
-        const int ju = g + 5 * q;
-        const double u0 = ue[q];
-        double grad = u0 * w_prox;
-        if (ival) grad += column_sum(part, k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
-        if (k > 0) grad += column_sum(part, k - 1, q == 0 ? 17 + 3 * g : 22 + 3 * g);
-        double un = u0 + -alpha * grad;
-        // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
-        const double lo = umin[k * kNU + ju], hi = umax[k * kNU + ju];
-        const double cl = (hi < un) ? hi : un;
-        un = (lo < cl) ? cl : lo;
-        ur[k * kUS + ju] = 2.0 * un - u0;
-        if (check) {
-          const double old = uc[k * kNU + ju];
-          z_cur = fmax(z_cur, fabs(un));
-          z_prev = fmax(z_prev, fabs(old));
-          z_del = fmax(z_del, fabs(un - old));
-          if (!pt_finite(un)) bad = 1.0;
-        }
-        if (keep) uc[k * kNU + ju] = un;
-        ue[q] = (1.0 - rho) * u0 + rho * un;
+    for (int q = 0; q < 2; ++q) {
+      const int ju = q == 0 ? g : ju1;
+      const double u0 = ue[q];
+      double grad = u0 * a.shape.w_prox;
+      grad += column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
+      grad += column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+      double un = u0 + -alpha * grad;
+      // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
+      const double lo = umin_k[ju], hi = umax_k[ju];
+      const double cl = (hi < un) ? hi : un;
+      un = (lo < cl) ? cl : lo;
+      ur_k[ju] = 2.0 * un - u0;
+      if (kStore) {
+        if (q == 0 || g < 2) snap[S.u + kc * kNU + ju] = un;
       }
+      ue[q] = one_m_rho * u0 + a.rho * un;
     }
     __syncthreads();
 
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
     //      extrapolation of the dual groups (:468-472) and the partial sums of H^T phi_ex for
     //      the next primal step
-    if (ival) {
+    {
       double v[kW];
-      load_node_vectors(xr, ur, k, v);
+      load_node_vectors(xr_k, ur_k, v);
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
-        const int e = k * kNX + kR * g + r;
         double pa, pm, pp;
         row_products(aop, v, r, pa, pm, pp);
-        double resid = pa + -xr[(k + 1) * kXS + kR * g + r];
+        double resid = pa + -xr_k[kXS + kR * g + r];
         resid += pm;
         resid += pp;
         const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
-        const double vp = fmax(0.0, vp0 - alpha * (w_ep + p0));
-        const double vn = fmax(0.0, vn0 - alpha * (w_ep - p0));
-        resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv[e];
+        const double vp = fmax(0.0, vp0 - alpha * (a.shape.w_ep + p0));
+        const double vn = fmax(0.0, vn0 - alpha * (a.shape.w_ep - p0));
+        resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv_k[r];
         const double pn = p0 + beta * resid;
-        if (check) {
-          const double op = vpc[e], on = vnc[e], od = phc[e];
-          z_cur = fmax(z_cur, fmax(fabs(vp), fabs(vn)));
-          z_prev = fmax(z_prev, fmax(fabs(op), fabs(on)));
-          z_del = fmax(z_del, fmax(fabs(vp - op), fabs(vn - on)));
-          r_cur = fmax(r_cur, fabs(pn));
-          r_prev = fmax(r_prev, fabs(od));
-          r_del = fmax(r_del, fabs(pn - od));
-          if (!pt_finite(pn)) bad = 1.0;
+        if (kStore) {
+          const int e = kc * kNX + kR * g + r;
+          snap[S.vp + e] = vp;
+          snap[S.vn + e] = vn;
+          snap[S.ph + e] = pn;
         }
-        if (keep) {
-          vpc[e] = vp;
-          vnc[e] = vn;
-          phc[e] = pn;
-        }
-        phe[r] = (1.0 - rho) * p0 + rho * pn;
-        vpe[r] = (1.0 - rho) * vp0 + rho * vp;
-        vne[r] = (1.0 - rho) * vn0 + rho * vn;
-        phx[e] = phe[r];
+        const double pe = one_m_rho * p0 + a.rho * pn;
+        phe[r] = ival ? pe : 0.0;
+        vpe[r] = one_m_rho * vp0 + a.rho * vp;
+        vne[r] = one_m_rho * vn0 + a.rho * vn;
+        phx_k[r] = phe[r];
       }
       if (g == 4) {
-        const double drift = xr[(k + 1) * kXS + 14] - v[14] - epsv[k];
+        const double drift = xr_k[kXS + 14] - v[14] - eps_k[0];
         const double tn = fmax(0.0, the + beta * drift);
-        if (check) {
-          const double old = thc[k];
-          r_cur = fmax(r_cur, fabs(tn));
-          r_prev = fmax(r_prev, fabs(old));
-          r_del = fmax(r_del, fabs(tn - old));
-        }
-        if (keep) thc[k] = tn;
-        the = (1.0 - rho) * the + rho * tn;
-        thx[k] = the;
+        if (kStore) snap[S.th + kc] = tn;
+        the = ival ? one_m_rho * the + a.rho * tn : 0.0;
+        thx_k[0] = the;
       }
-      store_partials(aop, phe, part + (size_t)tid * kPS);
+      store_partials(aop, phe, slot);
+    }
+  };
+
+  int iters = 0, cur_set = 0;  // snapshot holding the latest materialised *_cur groups
+  bool converged = false, diverged = false;
+  for (int j = 1; j <= a.j_max; ++j) {
+    const bool check = (j % a.j_check) == 0;
+    // cur values are materialised when the next iteration checks against them, when this one
+    // checks (a converged exit returns them), and on the last iteration
+    const bool keep = check || ((j + 1) % a.j_check) == 0 || j == a.j_max;
+    if (keep) {
+      cur_set ^= 1;
+      iteration(std::true_type{}, snap0 + cur_set * S.total);
+    } else {
+      iteration(std::false_type{}, nullptr);
     }
     iters = j;
-    if (check) {
+    __syncthreads();
+    if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
+      const double* cur = snap0 + cur_set * S.total;
+      const double* prev = snap0 + (cur_set ^ 1) * S.total;
+      double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
+      double bad = 0.0;
+      auto primal = [&](int off, int count, bool finite_checked) {
+        for (int e = tid; e < count; e += kFastThreads) {
+          const double c = cur[off + e], o = prev[off + e];
+          z_cur = fmax(z_cur, fabs(c));
+          z_prev = fmax(z_prev, fabs(o));
+          z_del = fmax(z_del, fabs(c - o));
+          if (finite_checked && !pt_finite(c)) bad = 1.0;
+        }
+      };
+      auto dual = [&](int off, int count, bool finite_checked) {
+        for (int e = tid; e < count; e += kFastThreads) {
+          const double c = cur[off + e], o = prev[off + e];
+          r_cur = fmax(r_cur, fabs(c));
+          r_prev = fmax(r_prev, fabs(o));
+          r_del = fmax(r_del, fabs(c - o));
+          if (finite_checked && !pt_finite(c)) bad = 1.0;
+        }
+      };
+      primal(S.x, NXn, true);
+      primal(S.u, NUn, true);
+      primal(S.vp, NM, false);
+      primal(S.vn, NM, false);
+      dual(S.ph, NM, true);
+      dual(S.th, m, false);
       z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
       r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
       bad = warp_max(bad);
@@ -574,9 +609,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
         rw[6] = bad;
       }
-    }
-    __syncthreads();
-    if (check) {  // pipg.hpp:475-487
+      __syncthreads();
       double v[7];
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
@@ -585,6 +618,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, red[w * 8 + q]);
         v[q] = mx;
       }
+      __syncthreads();  // red and the snapshots are rewritten later
       if (v[6] > 0.0) {
         diverged = true;
         break;
@@ -594,7 +628,6 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         converged = true;
         break;
       }
-      __syncthreads();  // red is rewritten by the next check
     }
   }
 
@@ -608,15 +641,17 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
     }
     return;
   }
-  // solution = the *_cur groups, pipg.hpp:490-495 (all threads passed the barrier above)
-  for (int e = tid; e < NXn; e += kFastThreads) a.ws.x[(size_t)b * NXn + e] = xc[e];
-  for (int e = tid; e < NUn; e += kFastThreads) a.ws.u[(size_t)b * NUn + e] = uc[e];
+  // solution = the *_cur groups, pipg.hpp:490-495 (all threads passed a barrier after the last
+  // snapshot write)
+  const double* cur = snap0 + cur_set * S.total;
+  for (int e = tid; e < NXn; e += kFastThreads) a.ws.x[(size_t)b * NXn + e] = cur[S.x + e];
+  for (int e = tid; e < NUn; e += kFastThreads) a.ws.u[(size_t)b * NUn + e] = cur[S.u + e];
   for (int e = tid; e < NM; e += kFastThreads) {
-    a.ws.vc_pos[(size_t)b * NM + e] = vpc[e];
-    a.ws.vc_neg[(size_t)b * NM + e] = vnc[e];
-    a.ws.dyn_dual[(size_t)b * NM + e] = phc[e];
+    a.ws.vc_pos[(size_t)b * NM + e] = cur[S.vp + e];
+    a.ws.vc_neg[(size_t)b * NM + e] = cur[S.vn + e];
+    a.ws.dyn_dual[(size_t)b * NM + e] = cur[S.ph + e];
   }
-  for (int e = tid; e < m; e += kFastThreads) a.ws.relax_dual[(size_t)b * m + e] = thc[e];
+  for (int e = tid; e < m; e += kFastThreads) a.ws.relax_dual[(size_t)b * m + e] = cur[S.th + e];
   if (tid == 0) {
     if (a.iterations) a.iterations[b] = iters;
     if (a.converged) a.converged[b] = converged ? 1 : 0;
@@ -633,8 +668,8 @@ bool solver_fast_supports(const SubShape& s, bool has_a_plus) {
   return true;
 }
 
-size_t power_fast_smem(const SubShape& s) { return sizeof(double) * (size_t)fast_layout(s.n, false).total; }
-size_t pipg_fast_smem(const SubShape& s) { return sizeof(double) * (size_t)fast_layout(s.n, true).total; }
+size_t power_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_layout(false).total; }
+size_t pipg_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_layout(true).total; }
 
 cudaError_t configure_solver_fast(const SubShape& s) {
   cudaError_t e = cudaFuncSetAttribute(power_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -134,10 +134,8 @@ __device__ __forceinline__ void store_partials(const double (&a)[kR][kW], const 
 /// Sum over the five partial slots of an interval (part_k: its first slot) for one position.
 __device__ __forceinline__ double column_sum(const double* part_k, int pos) {
   const double* p = part_k + pos;
-  double s = p[0];
-#pragma unroll
-  for (int q = 1; q < kG; ++q) s += p[q * kPS];
-  return s;
+  const double p0 = p[0], p1 = p[kPS], p2 = p[2 * kPS], p3 = p[3 * kPS], p4 = p[4 * kPS];
+  return ((p0 + p1) + (p2 + p3)) + p4;  // short dependency chain; rounding-only change
 }
 
 struct FastLayout {
@@ -277,79 +275,98 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   }
   sigma = sqrt(sigma);
 
+  // The norm of trip j-1 is reduced while trip j's forward products are already running: the
+  // products do not need sigma until they are scaled, so the block reduction, the square root
+  // and the reciprocal overlap with them instead of forming a serial stage of their own.
   int trips = 0;
+  bool done = false;
   for (int j = 1; j <= a.j_max; ++j) {
-    trips = j;
-    // ---- forward map scaled by 1/sigma (pipg.hpp:234-245) and partial sums of H^T [phi; theta]
-    double phi[kR];
-    {
-      const double inv = 1.0 / sigma;
-      double v[kW];
-      load_node_vectors(xs_k, us_k, v);
-#pragma unroll
-      for (int r = 0; r < kR; ++r) {
-        double pa, pm, pp;
-        row_products(aop, v, r, pa, pm, pp);
-        double s = pa + -xs_k[kXS + kR * g + r];
-        s += pm;
-        s += pp;
-        s += vcp[r];
-        s += -1.0 * vcn[r];
-        phi[r] = ival ? s * inv : 0.0;
-        phi_k[r] = phi[r];
-      }
-      if (g == 4) th_k[0] = ival ? (xs_k[kXS + 14] - v[14]) / sigma : 0.0;
-      store_partials(aop, phi, slot);
-    }
-    __syncthreads();
-    // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
-    acc = 0.0;
+    // ---- forward map (pipg.hpp:234-245): products first, then the scale 1/sigma
+    double v[kW];
+    load_node_vectors(xs_k, us_k, v);
+    double s[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-      const int i = kR * g + r;
-      double s = column_sum(part_k, i);
-      s += -phi_k[r - kNX];
-      if (r == kR - 1 && g == 4) {
-        s += -th_k[0];
-        s += th_k[-1];
+      double pa, pm, pp;
+      row_products(aop, v, r, pa, pm, pp);
+      double t = pa + -xs_k[kXS + kR * g + r];
+      t += pm;
+      t += pp;
+      t += vcp[r];
+      t += -1.0 * vcn[r];
+      s[r] = t;
+    }
+    const double dy = xs_k[kXS + 14] - v[14];
+    if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+      const double* rd = red + (((j - 1) & 1) ? kFastWarps : 0);
+      double sq = 0.0;
+#pragma unroll
+      for (int w = 0; w < kFastWarps; ++w) sq += rd[w];
+      const double sigma_star = sqrt(sq);
+      if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
+        sigma = 0.0;
+        done = true;
+        break;
       }
-      xs_k[i] = s;
-      acc += s * s;
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
+      sigma = sigma_star;
+      if (hit) {
+        done = true;
+        break;
+      }
     }
-    {
-      double s = column_sum(part_k, 15 + 3 * g);
-      s += column_sum(part_k - kG * kPS, 17 + 3 * g);
-      us_k[g] = s;
-      acc += s * s;
-      double s1 = column_sum(part_k, 16 + 3 * g);
-      s1 += column_sum(part_k - kG * kPS, 22 + 3 * g);
-      us_k[ju1] = s1;
-      acc += g < 2 ? s1 * s1 : 0.0;
+    trips = j;
+    const double inv = 1.0 / sigma;
+    double phi[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      phi[r] = ival ? s[r] * inv : 0.0;
+      phi_k[r] = phi[r];
     }
+    if (g == 4) th_k[0] = ival ? dy / sigma : 0.0;
+    store_partials(aop, phi, slot);
+    // vc+ = phi, vc- = -phi and their share of the norm (pipg.hpp:268-279)
+    double acc_d = 0.0;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       vcp[r] = phi[r];
       vcn[r] = -phi[r];
-      acc += phi[r] * phi[r];
-      acc += phi[r] * phi[r];
+      acc_d += phi[r] * phi[r];
+      acc_d += phi[r] * phi[r];
     }
-    if (!node) acc = 0.0;
+    __syncthreads();
+    // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
+    double sx[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
+    const double su0 = column_sum(part_k, 15 + 3 * g) + column_sum(part_k - kG * kPS, 17 + 3 * g);
+    const double su1 = column_sum(part_k, 16 + 3 * g) + column_sum(part_k - kG * kPS, 22 + 3 * g);
+    double acc_x = 0.0;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      double t = sx[r] + -phi_k[r - kNX];
+      if (r == kR - 1 && g == 4) {
+        t += -th_k[0];
+        t += th_k[-1];
+      }
+      xs_k[kR * g + r] = t;
+      acc_x += t * t;
+    }
+    us_k[g] = su0;
+    us_k[ju1] = su1;
+    double acc_u = su0 * su0;
+    acc_u += g < 2 ? su1 * su1 : 0.0;
+    acc = node ? (acc_x + acc_u) + acc_d : 0.0;
     acc = warp_sum(acc);
     if (lane == 0) red[((j & 1) ? kFastWarps : 0) + warp] = acc;
     __syncthreads();
-    double sigma_star = 0.0;
+  }
+  if (!done) {  // j_max trips without meeting the tolerance: sigma is the last norm
+    const double* rd = red + ((a.j_max & 1) ? kFastWarps : 0);
+    double sq = 0.0;
 #pragma unroll
-    for (int w = 0; w < kFastWarps; ++w) sigma_star += red[((j & 1) ? kFastWarps : 0) + w];
-    sigma_star = sqrt(sigma_star);
-    if (sigma_star == 0.0) {  // seed in the null space, pipg.hpp:280-284
-      sigma = 0.0;
-      break;
-    }
-    if (fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma)) {
-      sigma = sigma_star;
-      break;
-    }
-    sigma = sigma_star;
+    for (int w = 0; w < kFastWarps; ++w) sq += rd[w];
+    sigma = sqrt(sq);
   }
   if (tid == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sigma;
@@ -479,20 +496,39 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   // snapshot `snap` (threads without a node / interval write scratch entries).
   auto iteration = [&](auto store_tag, double* snap) {
     constexpr bool kStore = decltype(store_tag)::value;
-    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
+    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry.  The
+    //      terms that do not need the partial sums are gathered first so that the dependent
+    //      chain behind the shared-memory loads stays short.
+    double base[kR], fv[kR], sx[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int i = kR * g + r;
+      fv[r] = fix_val[i];
+      double t = xe[r] * a.shape.w_prox;
+      if (last_node) t += a.shape.w_cost * ecost[i];
+      t += -phx_k[r - kNX];
+      if (r == kR - 1 && g == 4) t += thx_k[-1] - thx_k[0];
+      base[r] = t;
+    }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
+    double su[2], lo[2], hi[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ju = q == 0 ? g : ju1;
+      lo[q] = umin_k[ju];
+      hi[q] = umax_k[ju];
+      su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g) +
+              column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+    }
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const int i = kR * g + r;
       const double x0 = xe[r];
-      double grad = x0 * a.shape.w_prox;
-      grad += column_sum(part_k, i);
-      if (r == kR - 1 && g == 4) grad += -thx_k[0];
-      grad += -phx_k[r - kNX];
-      if (r == kR - 1 && g == 4) grad += thx_k[-1];
-      if (last_node) grad += a.shape.w_cost * ecost[i];
+      const double grad = base[r] + sx[r];
       double xn = x0 + -alpha * grad;
-      if (fix_bits & (1 << r)) xn = fix_val[i];
-      xr_k[i] = 2.0 * xn - x0;
+      xn = (fix_bits & (1 << r)) ? fv[r] : xn;
+      xr_k[i] = fma(2.0, xn, -x0);
       if (kStore) snap[S.x + kc * kNX + i] = xn;
       xe[r] = one_m_rho * x0 + a.rho * xn;  // extrapolation, pipg.hpp:461-467
     }
@@ -500,15 +536,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
     for (int q = 0; q < 2; ++q) {
       const int ju = q == 0 ? g : ju1;
       const double u0 = ue[q];
-      double grad = u0 * a.shape.w_prox;
-      grad += column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
-      grad += column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+      const double grad = u0 * a.shape.w_prox + su[q];
       double un = u0 + -alpha * grad;
       // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
-      const double lo = umin_k[ju], hi = umax_k[ju];
-      const double cl = (hi < un) ? hi : un;
-      un = (lo < cl) ? cl : lo;
-      ur_k[ju] = 2.0 * un - u0;
+      const double cl = (hi[q] < un) ? hi[q] : un;
+      un = (lo[q] < cl) ? cl : lo[q];
+      ur_k[ju] = fma(2.0, un, -u0);
       if (kStore) {
         if (q == 0 || g < 2) snap[S.u + kc * kNU + ju] = un;
       }
@@ -559,11 +592,14 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
 
   int iters = 0, cur_set = 0;  // snapshot holding the latest materialised *_cur groups
   bool converged = false, diverged = false;
+  int to_check = a.j_check;  // iterations left until the next stopping test (counts down to 0)
   for (int j = 1; j <= a.j_max; ++j) {
-    const bool check = (j % a.j_check) == 0;
+    --to_check;
+    const bool check = to_check == 0;
     // cur values are materialised when the next iteration checks against them, when this one
     // checks (a converged exit returns them), and on the last iteration
-    const bool keep = check || ((j + 1) % a.j_check) == 0 || j == a.j_max;
+    const bool keep = to_check <= 1 || j == a.j_max;
+    if (check) to_check = a.j_check;
     if (keep) {
       cur_set ^= 1;
       iteration(std::true_type{}, snap0 + cur_set * S.total);

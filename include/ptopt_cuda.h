@@ -311,6 +311,76 @@ int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double
                                    double* final_defect_inf, double* history, int32_t* power_trips,
                                    int32_t* status, int32_t* fail_index);
 
+/* ---- Monte Carlo harness around the solve --------------------------------- */
+
+/* mc::DispersionSpec (proj/include/ptopt/montecarlo.hpp:20-31). */
+typedef struct ptopt_dispersion_spec {
+  double r_low[3];
+  double r_high[3];
+  uint64_t seed;
+} ptopt_dispersion_spec;
+
+/* mc::RunRecord (proj/include/ptopt/montecarlo.hpp:67-78).  `failure` becomes
+ * status/fail_index (ptopt_instance_status); a failed record keeps the
+ * reference's defaults (converged 0, zeros).  wall_time has no per-instance
+ * meaning on the device and is not reported. */
+typedef struct ptopt_run_record {
+  int32_t run_id;
+  int32_t converged;
+  int32_t scp_iterations;
+  int32_t status;
+  int32_t fail_index;
+  int32_t reserved_;
+  double initial_position[3];
+  double propellant_used;
+  double final_defect_inf;
+  double max_pointwise_g;
+  double max_node_y_increase;
+} ptopt_run_record;
+
+/* Instance generation exactly as mc::solve_instance does it for run ids
+ * first_run_id .. first_run_id+batch-1: mc::disperse (montecarlo.hpp:55-65),
+ * mc::run_seed (:51-53) and initial_guess (proj/include/ptopt/rocket_problem.hpp:127-163)
+ * about the handle's problem.  nominal_init_state [14] is RocketBoundary::initial; the
+ * terminal targets are the handle's final_fix values (unpinned slots default as
+ * RocketBoundary does).  Outputs: init_state [B][14], x_guess [B][nodes][15],
+ * u_guess [B][nodes][7], rng_seed [B].  Integer draws and every floating-point
+ * operation are bit-exact with the reference. */
+int ptopt_cuda_generate_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                              const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                              double* init_state, double* x_guess, double* u_guess,
+                              uint64_t* rng_seed);
+int ptopt_cuda_generate_batch_dev(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                                  const double* nominal_init_state,
+                                  const ptopt_dispersion_spec* spec, double* init_state,
+                                  double* x_guess, double* u_guess, uint64_t* rng_seed);
+
+/* Batched dense_violation_audit (proj/include/ptopt/discretizer.hpp:249-285) with
+ * propagate_state (:153-187): x [B][nodes][15], u [B][nodes][7] ->
+ * max_pointwise_g [B], interval_y_increase [B][M] (total_y_increase is their
+ * in-order sum).  status/fail_index report a domain error inside the propagation
+ * (first failing interval). */
+int ptopt_cuda_dense_audit_batch(ptopt_cuda_handle* h, int batch, int substeps, const double* x,
+                                 const double* u, double* max_pointwise_g,
+                                 double* interval_y_increase, int32_t* status,
+                                 int32_t* fail_index);
+int ptopt_cuda_dense_audit_batch_dev(ptopt_cuda_handle* h, int batch, int substeps,
+                                     const double* x, const double* u, double* max_pointwise_g,
+                                     double* interval_y_increase, int32_t* status,
+                                     int32_t* fail_index);
+
+/* mc::run_batch (proj/include/ptopt/montecarlo.hpp:140-175) for run ids
+ * first_run_id .. first_run_id+batch-1, everything on the device: generation ->
+ * scp_solve -> audit -> records.  Only the records (and, when x_out/u_out are
+ * non-NULL, the final trajectories [B][nodes][15] / [B][nodes][7]) cross to the
+ * host.  The reference's `workers` argument has no counterpart: every instance
+ * is its own CTA.  Sharding a batch over GPUs = one handle per device with
+ * disjoint run-id ranges (records are pure functions of the run id). */
+int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                         const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                         int audit_substeps, ptopt_run_record* records, double* x_out,
+                         double* u_out);
+
 /* ---- measurement --------------------------------------------------------- */
 
 #define PTOPT_STAGE_COUNT 6

@@ -152,6 +152,30 @@ class WorkspaceArrays(C.Structure):
     ]
 
 
+class DispersionSpec(C.Structure):
+    """mc::DispersionSpec (proj/include/ptopt/montecarlo.hpp:20-31)."""
+
+    _fields_ = [("r_low", C.c_double * 3), ("r_high", C.c_double * 3), ("seed", C.c_uint64)]
+
+
+class RunRecord(C.Structure):
+    """mc::RunRecord (proj/include/ptopt/montecarlo.hpp:67-78) as ptopt_run_record."""
+
+    _fields_ = [
+        ("run_id", C.c_int32),
+        ("converged", C.c_int32),
+        ("scp_iterations", C.c_int32),
+        ("status", C.c_int32),
+        ("fail_index", C.c_int32),
+        ("reserved_", C.c_int32),
+        ("initial_position", C.c_double * 3),
+        ("propellant_used", C.c_double),
+        ("final_defect_inf", C.c_double),
+        ("max_pointwise_g", C.c_double),
+        ("max_node_y_increase", C.c_double),
+    ]
+
+
 STATUS_NAMES = {
     ST_OK: "ok",
     ST_PROPAGATION_DIVERGED: "propagation diverged",

@@ -29,8 +29,18 @@ EXPORTS = [
     "ptopt_cuda_power_iteration_batch", "ptopt_cuda_power_iteration_batch_dev",
     "ptopt_cuda_pipg_batch", "ptopt_cuda_pipg_batch_dev",
     "ptopt_cuda_scp_solve_batch", "ptopt_cuda_scp_solve_batch_dev",
+    "ptopt_cuda_generate_batch", "ptopt_cuda_generate_batch_dev",
+    "ptopt_cuda_dense_audit_batch", "ptopt_cuda_dense_audit_batch_dev",
+    "ptopt_cuda_run_batch",
     "ptopt_cuda_scp_stage_times", "ptopt_cuda_measure_fp64_peak",
 ]
+
+RECORD_DTYPE = np.dtype([
+    ("run_id", np.int32), ("converged", np.int32), ("scp_iterations", np.int32),
+    ("status", np.int32), ("fail_index", np.int32), ("reserved_", np.int32),
+    ("initial_position", np.float64, (3,)), ("propellant_used", np.float64),
+    ("final_defect_inf", np.float64), ("max_pointwise_g", np.float64),
+    ("max_node_y_increase", np.float64)])
 
 STAGE_NAMES = ("linearize", "prepare", "power_iteration", "pipg", "update", "graph_total")
 
@@ -234,6 +244,54 @@ class Solver:
             self._h, C.c_int(B), C.byref(shape), C.byref(s), C.byref(cfg), _hp(sigma), C.byref(w),
             _hp(iters), _hp(conv), _hp(status), _hp(fail)))
         return iters, conv.astype(bool), status, fail
+
+    # ------------------------------------------------------------- Monte Carlo harness
+    @staticmethod
+    def _spec(r_low, r_high, seed):
+        sp = abi.DispersionSpec()
+        sp.r_low[:] = list(r_low)
+        sp.r_high[:] = list(r_high)
+        sp.seed = int(seed)
+        return sp
+
+    def generate_batch(self, batch, first_run_id, nominal_init_state, r_low, r_high, seed):
+        """disperse + run_seed + initial_guess on the device (montecarlo.hpp:43-65,
+        rocket_problem.hpp:127-163) for run ids first_run_id .. first_run_id+batch-1."""
+        n = self.nodes
+        out = dict(init_state=np.empty((batch, abi.NXI)), x_guess=np.empty((batch, n, abi.NX)),
+                   u_guess=np.empty((batch, n, abi.NU)), rng_seed=np.empty(batch, np.uint64))
+        sp = self._spec(r_low, r_high, seed)
+        _check(self.lib.ptopt_cuda_generate_batch(
+            self._h, C.c_int(batch), C.c_int64(first_run_id), _hp(_np(nominal_init_state)),
+            C.byref(sp), _hp(out["init_state"]), _hp(out["x_guess"]), _hp(out["u_guess"]),
+            _hp(out["rng_seed"])))
+        return out
+
+    def dense_violation_audit(self, x, u, substeps):
+        """Batched dense_violation_audit (discretizer.hpp:249-285)."""
+        x, u = _np(x), _np(u)
+        B, m = x.shape[0], self.nodes - 1
+        out = dict(max_pointwise_g=np.empty(B), interval_y_increase=np.empty((B, m)),
+                   status=np.empty(B, np.int32), fail_index=np.empty(B, np.int32))
+        _check(self.lib.ptopt_cuda_dense_audit_batch(
+            self._h, C.c_int(B), C.c_int(substeps), _hp(x), _hp(u), _hp(out["max_pointwise_g"]),
+            _hp(out["interval_y_increase"]), _hp(out["status"]), _hp(out["fail_index"])))
+        return out
+
+    def run_batch(self, batch, first_run_id, nominal_init_state, r_low, r_high, seed,
+                  audit_substeps=64, keep_trajectories=False, records=None, x_out=None,
+                  u_out=None):
+        """mc::run_batch (montecarlo.hpp:140-175) on the device; returns a structured array of
+        ptopt_run_record (and the trajectories when asked)."""
+        n = self.nodes
+        rec = np.empty(batch, RECORD_DTYPE) if records is None else records
+        if keep_trajectories and x_out is None:
+            x_out, u_out = np.empty((batch, n, abi.NX)), np.empty((batch, n, abi.NU))
+        sp = self._spec(r_low, r_high, seed)
+        _check(self.lib.ptopt_cuda_run_batch(
+            self._h, C.c_int(batch), C.c_int64(first_run_id), _hp(_np(nominal_init_state)),
+            C.byref(sp), C.c_int(audit_substeps), _hp(rec), _hp(x_out), _hp(u_out)))
+        return (rec, x_out, u_out) if keep_trajectories else rec
 
     # ---------------------------------------------------------------------- SCP loop
     def scp_solve(self, init_state, x_guess, u_guess, rng_seed):

@@ -62,6 +62,9 @@ enum BufId {
   S_UMIN, S_UMAX, S_INITVAL, S_FINALVAL, S_SEEDX, S_SEEDU, S_WSX, S_WSU, S_WSP, S_WSN, S_WSD,
   S_WSR, S_SIGMA, S_PITERS, S_FAILKEY, S_ACTIVE, S_CONV, S_SOLVES, S_LASTSTEP, S_FDEF, S_HIST,
   S_TRIPS, S_STATUS, S_FAILIDX,
+  // Monte Carlo harness
+  R_QTAB, R_INIT, R_XG, R_UG, R_SEED, R_XOUT, R_UOUT, R_ITERS, R_CONV, R_FDEF, R_STATUS, R_FAILIDX,
+  R_GMAX, R_DY, R_AKEY, R_PG, R_RECORDS,
   kNumBufs
 };
 
@@ -965,6 +968,258 @@ int ptopt_cuda_scp_solve_batch_dev(ptopt_cuda_handle* h, int batch, const double
   return scp_solve_common(h, batch, init_state, x_guess, u_guess, rng_seed, x_out, u_out,
                           scp_iterations, converged, final_defect_inf, history, power_trips,
                           status, fail_index, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+}
+
+// ---- Monte Carlo harness ---------------------------------------------------------------
+
+namespace {
+
+/// slerp of rocket_problem.hpp:98-120, evaluated on the host with the C library.
+void slerp_host(const double* qa, const double* qb_in, double t, double* q) {
+  double qb[4] = {qb_in[0], qb_in[1], qb_in[2], qb_in[3]};
+  double d = qa[0] * qb[0] + qa[1] * qb[1] + qa[2] * qb[2] + qa[3] * qb[3];
+  if (d < 0.0) {
+    for (double& c : qb) c = -c;
+    d = -d;
+  }
+  if (d > 1.0 - 1e-10) {
+    for (int i = 0; i < 4; ++i) q[i] = (1.0 - t) * qa[i] + t * qb[i];
+  } else {
+    const double ang = std::acos(d < 1.0 ? d : 1.0);
+    const double sa = std::sin(ang);
+    const double ca = std::sin((1.0 - t) * ang) / sa;
+    const double cb = std::sin(t * ang) / sa;
+    for (int i = 0; i < 4; ++i) q[i] = ca * qa[i] + cb * qb[i];
+  }
+  double nq = 0.0;
+  for (int i = 0; i < 4; ++i) nq += q[i] * q[i];
+  nq = std::sqrt(nq);
+  for (int i = 0; i < 4; ++i) q[i] /= nq;
+}
+
+int generate_dev(ptopt_cuda_handle* h, int batch, int64_t first_run_id, const double* nominal,
+                 const ptopt_dispersion_spec* spec, double* init_state, double* x_guess,
+                 double* u_guess, uint64_t* rng_seed) {
+  if (!nominal || !spec || !init_state || !x_guess || !u_guess || !rng_seed)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "generate: null argument");
+  for (int i = 0; i < 3; ++i)  // DispersionSpec::validate, montecarlo.hpp:25-30
+    if (!(spec->r_low[i] <= spec->r_high[i]))
+      return fail(PTOPT_ERR_INVALID_ARGUMENT,
+                  "montecarlo.dispersion: low > high on axis " + std::to_string(i + 1));
+  const ptopt_problem_desc& d = h->desc;
+  GenerateArgs a;
+  a.batch = batch;
+  a.nodes = d.nodes;
+  a.first_run_id = first_run_id;
+  for (int i = 0; i < kNXI; ++i) {
+    a.nominal[i] = nominal[i];
+    a.fin[i] = 0.0;
+  }
+  a.fin[10] = 1.0;  // RocketBoundary defaults: identity attitude, everything else zero
+  for (int i = 0; i < d.n_final_fix; ++i)
+    if (d.final_fix_idx[i] >= 0 && d.final_fix_idx[i] < kNXI) a.fin[d.final_fix_idx[i]] = d.final_fix_val[i];
+  for (int i = 0; i < 3; ++i) {
+    a.r_low[i] = spec->r_low[i];
+    a.r_high[i] = spec->r_high[i];
+    a.g[i] = d.vehicle.g_inertial[i];
+  }
+  a.seed = spec->seed;
+  a.t_f_guess = d.t_f_guess;
+  const double* g = d.vehicle.g_inertial;
+  const double g_norm = std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  const double burn = nominal[0] * std::exp(-d.vehicle.alpha_mdot * g_norm * d.t_f_guess);
+  a.m_end = d.vehicle.m_dry < burn ? burn : d.vehicle.m_dry;  // std::max(m_dry, burn)
+  std::vector<double> qtab((size_t)d.nodes * 4);
+  for (int k = 0; k < d.nodes; ++k) slerp_host(nominal + 7, a.fin + 7, h->tau[k], &qtab[(size_t)k * 4]);
+  PT_CUDA(h->buf[R_QTAB].ensure(qtab.size() * 8));
+  // the table is consumed by the kernel enqueued right after this copy; wait for earlier
+  // consumers of the staging buffer first
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  PT_CUDA(cudaMemcpyAsync(h->buf[R_QTAB].p, qtab.data(), qtab.size() * 8, cudaMemcpyHostToDevice,
+                          h->stream));
+  PT_CUDA(cudaStreamSynchronize(h->stream));  // qtab is a stack-lifetime host buffer
+  a.tau = h->d_tau;
+  a.qtab = h->buf[R_QTAB].as<double>();
+  a.init_state = init_state;
+  a.x_guess = x_guess;
+  a.u_guess = u_guess;
+  a.rng_seed = reinterpret_cast<unsigned long long*>(rng_seed);
+  launch_generate(a, h->stream);
+  h->launches += 1;
+  PT_CUDA(cudaGetLastError());
+  return PTOPT_OK;
+}
+
+int audit_dev(ptopt_cuda_handle* h, int batch, int substeps, const double* x, const double* u,
+              const int* skip, double* max_pointwise_g, double* interval_y_increase,
+              int32_t* status, int32_t* fail_index) {
+  if (substeps < 1)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "dense_violation_audit: substeps must be >= 1");
+  const size_t B = (size_t)batch, m = (size_t)h->desc.nodes - 1;
+  AuditArgs a;
+  a.model = h->model;
+  a.batch = batch;
+  a.nodes = h->desc.nodes;
+  a.substeps = substeps;
+  a.tau = h->d_tau;
+  a.x = x;
+  a.u = u;
+  a.skip = skip;
+  PT_TRY(device_out(h, R_GMAX, B * m, &a.interval_g_max));
+  if (interval_y_increase) {
+    a.interval_y_increase = interval_y_increase;
+  } else {
+    PT_TRY(device_out(h, R_DY, B * m, &a.interval_y_increase));
+  }
+  PT_TRY(device_out(h, R_AKEY, B, &a.fail_key));
+  launch_init_fail_key(a.fail_key, batch, h->stream);
+  launch_audit(a, max_pointwise_g, status, fail_index, h->stream);
+  h->launches += 3;
+  PT_CUDA(cudaGetLastError());
+  return PTOPT_OK;
+}
+
+}  // namespace
+
+int ptopt_cuda_generate_batch_dev(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                                  const double* nominal_init_state,
+                                  const ptopt_dispersion_spec* spec, double* init_state,
+                                  double* x_guess, double* u_guess, uint64_t* rng_seed) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "montecarlo.batch_size must be >= 1");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  return generate_dev(h, batch, first_run_id, nominal_init_state, spec, init_state, x_guess,
+                      u_guess, rng_seed);
+}
+
+int ptopt_cuda_generate_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                              const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                              double* init_state, double* x_guess, double* u_guess,
+                              uint64_t* rng_seed) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "montecarlo.batch_size must be >= 1");
+  if (!init_state || !x_guess || !u_guess || !rng_seed)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "generate: null output");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes;
+  double *di, *dx, *du;
+  uint64_t* ds;
+  PT_TRY(device_out(h, R_INIT, B * kNXI, &di));
+  PT_TRY(device_out(h, R_XG, B * n * kNX, &dx));
+  PT_TRY(device_out(h, R_UG, B * n * kNU, &du));
+  PT_TRY(device_out(h, R_SEED, B, &ds));
+  PT_TRY(generate_dev(h, batch, first_run_id, nominal_init_state, spec, di, dx, du, ds));
+  PT_TRY(download(h, init_state, di, B * kNXI));
+  PT_TRY(download(h, x_guess, dx, B * n * kNX));
+  PT_TRY(download(h, u_guess, du, B * n * kNU));
+  PT_TRY(download(h, rng_seed, ds, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_dense_audit_batch_dev(ptopt_cuda_handle* h, int batch, int substeps,
+                                     const double* x, const double* u, double* max_pointwise_g,
+                                     double* interval_y_increase, int32_t* status,
+                                     int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!x || !u) return fail(PTOPT_ERR_INVALID_ARGUMENT, "audit: null trajectory");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  if (status) PT_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * (size_t)batch, h->stream));
+  if (fail_index)
+    PT_CUDA(cudaMemsetAsync(fail_index, 0xff, sizeof(int32_t) * (size_t)batch, h->stream));
+  return audit_dev(h, batch, substeps, x, u, nullptr, max_pointwise_g, interval_y_increase, status,
+                   fail_index);
+}
+
+int ptopt_cuda_dense_audit_batch(ptopt_cuda_handle* h, int batch, int substeps, const double* x,
+                                 const double* u, double* max_pointwise_g,
+                                 double* interval_y_increase, int32_t* status,
+                                 int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!x || !u) return fail(PTOPT_ERR_INVALID_ARGUMENT, "audit: null trajectory");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
+  const double *dx, *du;
+  double *dg, *dy;
+  int *dst, *dfi;
+  PT_TRY(upload(h, B_X, x, B * n * kNX, &dx));
+  PT_TRY(upload(h, B_U, u, B * n * kNU, &du));
+  PT_TRY(device_out(h, R_PG, B, &dg));
+  PT_TRY(device_out(h, R_DY, B * m, &dy));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
+  PT_TRY(ptopt_cuda_dense_audit_batch_dev(h, batch, substeps, dx, du, dg, dy, dst, dfi));
+  PT_TRY(download(h, max_pointwise_g, dg, B));
+  PT_TRY(download(h, interval_y_increase, dy, B * m));
+  PT_TRY(download(h, status, dst, B));
+  PT_TRY(download(h, fail_index, dfi, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
+                         const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                         int audit_substeps, ptopt_run_record* records, double* x_out,
+                         double* u_out) {
+  static_assert(sizeof(ptopt_run_record) == sizeof(RunRecordDev), "record layouts must agree");
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "montecarlo.batch_size must be >= 1");
+  if (!records) return fail(PTOPT_ERR_INVALID_ARGUMENT, "run_batch: null records");
+  if (audit_substeps < 1)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "dense_violation_audit: substeps must be >= 1");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes;
+  double *di, *dxg, *dug, *dxo, *duo, *dfd, *dpg;
+  uint64_t* ds;
+  int *dit, *dst, *dfi;
+  unsigned char* dcv;
+  RunRecordDev* drec;
+  PT_TRY(device_out(h, R_INIT, B * kNXI, &di));
+  PT_TRY(device_out(h, R_XG, B * n * kNX, &dxg));
+  PT_TRY(device_out(h, R_UG, B * n * kNU, &dug));
+  PT_TRY(device_out(h, R_SEED, B, &ds));
+  PT_TRY(device_out(h, R_XOUT, B * n * kNX, &dxo));
+  PT_TRY(device_out(h, R_UOUT, B * n * kNU, &duo));
+  PT_TRY(device_out(h, R_ITERS, B, &dit));
+  PT_TRY(device_out(h, R_CONV, B, &dcv));
+  PT_TRY(device_out(h, R_FDEF, B, &dfd));
+  PT_TRY(device_out(h, R_STATUS, B, &dst));
+  PT_TRY(device_out(h, R_FAILIDX, B, &dfi));
+  PT_TRY(device_out(h, R_PG, B, &dpg));
+  PT_TRY(device_out(h, R_RECORDS, B, &drec));
+  PT_TRY(generate_dev(h, batch, first_run_id, nominal_init_state, spec, di, dxg, dug, ds));
+  PT_TRY(scp_solve_common(h, batch, di, dxg, dug, ds, dxo, duo, dit, dcv, dfd, nullptr, nullptr,
+                          dst, dfi, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice));
+  PT_TRY(audit_dev(h, batch, audit_substeps, dxo, duo, dst, dpg, nullptr, dst, dfi));
+  RecordArgs ra;
+  ra.batch = batch;
+  ra.nodes = h->desc.nodes;
+  ra.first_run_id = first_run_id;
+  ra.init_state = di;
+  ra.x = dxo;
+  ra.scp_iterations = dit;
+  ra.converged = dcv;
+  ra.final_defect = dfd;
+  ra.max_pointwise_g = dpg;
+  ra.status = dst;
+  ra.fail_index = dfi;
+  ra.records = drec;
+  launch_records(ra, h->stream);
+  h->launches += 1;
+  PT_CUDA(cudaGetLastError());
+  PT_CUDA(cudaMemcpyAsync(records, drec, B * sizeof(ptopt_run_record), cudaMemcpyDeviceToHost,
+                          h->stream));
+  PT_TRY(download(h, x_out, dxo, B * n * kNX));
+  PT_TRY(download(h, u_out, duo, B * n * kNU));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
 }
 
 // ---- measurement ----------------------------------------------------------------------

@@ -408,3 +408,96 @@ def test_scp_solve_n50_two_instances(ptor):
     # sigma history spot values of SURVEY.md 6.3-4 are for the nominal instance; here we only
     # require the first power iteration to need thousands of trips as the survey observed
     assert out["power_trips"][0, 0] > 1000
+
+
+# ---------------------------------------------------------------- Monte Carlo harness
+def test_generate_batch_is_bit_exact(ptor):
+    """disperse + run_seed + initial_guess on the device equal the oracle bit for bit (integer
+    draws and separately rounded floating-point operations), incl. a slerp that takes the
+    trigonometric branch."""
+    from paper_2404_18034_b200.binding import Solver
+
+    for q_init in ((0.0, 0.0, 0.0, 1.0), (0.1, -0.2, 0.05, 0.97)):
+        sc = scenario.default_scenario(23)
+        q = np.array(q_init) / np.linalg.norm(q_init)
+        nominal = np.array(sc.initial_state)
+        nominal[7:11] = q
+        d = sc.problem_desc()
+        spec = sc.dispersion
+        first, B = 1000, 37
+        with Solver(d) as s:
+            out = s.generate_batch(B, first, nominal, spec.r_low, spec.r_high, spec.seed)
+        for b in range(B):
+            rid = first + b
+            init = nominal.copy()
+            init[1:4] = ptor.disperse(spec.r_low, spec.r_high, spec.seed, rid)
+            rc, xg, ug = ptor.initial_guess(d, init)
+            assert rc == 0
+            np.testing.assert_array_equal(out["init_state"][b], init)
+            np.testing.assert_array_equal(out["x_guess"][b], xg)
+            np.testing.assert_array_equal(out["u_guess"][b], ug)
+            assert int(out["rng_seed"][b]) == ptor.run_seed(spec.seed, rid)
+
+
+def test_dense_audit_matches_oracle(solver15, ptor):
+    sc, s = solver15
+    d = sc.problem_desc()
+    rng = np.random.default_rng(99)
+    xs, us = [], []
+    for rid in range(6):
+        init = scenario.disperse(sc, rid)
+        x, u = scenario.initial_guess(sc, init)
+        if rid >= 3:  # active constraints: the violation integrator grows
+            _, x, u = stressed_iterate(sc, rid, rng)
+        xs.append(x)
+        us.append(u)
+    xs, us = np.stack(xs), np.stack(us)
+    bad = xs.copy()
+    bad_u = us.copy()
+    bad_u[2, 7, 6] = -0.5  # nonpositive dilation at node 7: first failing interval is 6
+    out = s.dense_violation_audit(bad, bad_u, 16)
+    for b in range(6):
+        rc, g, ytot, dy = ptor.dense_audit(d, bad[b], bad_u[b], 16)
+        if b == 2:
+            assert rc == abi.ST_DILATION_NONPOSITIVE and out["status"][b] == rc
+            assert out["fail_index"][b] == 6
+            continue
+        assert rc == 0 and out["status"][b] == 0
+        assert abs(out["max_pointwise_g"][b] - g) <= TOL_DISC * max(1.0, abs(g))
+        assert np.abs(out["interval_y_increase"][b] - dy).max() <= TOL_DISC * max(1.0, np.abs(dy).max())
+        assert abs(out["interval_y_increase"][b].sum() - ytot) <= 1e-9 * max(1.0, abs(ytot))
+
+
+def test_run_batch_records_match_oracle(ptor):
+    """mc::run_batch on the device (generation -> scp_solve -> audit -> records) against the
+    CPU oracle's run_batch, reduced budget; run ids are offset to exercise first_run_id."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(12)
+    sc.max_iters = 3
+    sc.pipg_j_max = 250
+    sc.power_j_max = 300
+    d = sc.problem_desc()
+    spec = sc.dispersion
+    B = 9
+    with Solver(d) as s:
+        rec, xo, uo = s.run_batch(B, 0, sc.initial_state, spec.r_low, spec.r_high, spec.seed,
+                                  audit_substeps=16, keep_trajectories=True)
+        tail = s.run_batch(4, 5, sc.initial_state, spec.r_low, spec.r_high, spec.seed,
+                           audit_substeps=16)
+    wall, ref, xr, ur = ptor.run_batch(d, sc.initial_state, spec.r_low, spec.r_high, spec.seed, B,
+                                       2, 16, keep=True)
+    for b in range(B):
+        assert rec["run_id"][b] == b and rec["status"][b] == 0 and ref[b, 7] == 0
+        assert rec["converged"][b] == ref[b, 1] and rec["scp_iterations"][b] == ref[b, 2]
+        assert abs(rec["propellant_used"][b] - ref[b, 3]) <= TOL_ITER
+        assert abs(rec["final_defect_inf"][b] - ref[b, 4]) <= TOL_ITER
+        assert abs(rec["max_pointwise_g"][b] - ref[b, 5]) <= TOL_ITER
+        assert abs(rec["max_node_y_increase"][b] - ref[b, 6]) <= TOL_ITER
+        np.testing.assert_array_equal(rec["initial_position"][b],
+                                      ptor.disperse(spec.r_low, spec.r_high, spec.seed, b))
+        assert np.abs(xo[b] - xr[b]).max() <= TOL_ITER and np.abs(uo[b] - ur[b]).max() <= TOL_ITER
+    # records are pure functions of the run id: a shard starting at run 5 reproduces them
+    for f in ("run_id", "converged", "scp_iterations", "propellant_used", "final_defect_inf",
+              "max_pointwise_g", "max_node_y_increase"):
+        np.testing.assert_array_equal(tail[f], rec[f][5:9])

@@ -231,6 +231,16 @@ int ptopt_cuda_linearize_batch_dev(ptopt_cuda_handle* h, int batch, const double
                                    const double* u, double* A, double* Bm, double* Bp, double* w,
                                    double* x_end, int32_t* status, int32_t* fail_index);
 
+/* Batched propagate_interval (proj/include/ptopt/discretizer.hpp:82-149): independent
+ * intervals, each with its own end points.  x_k [B][15], u_k/u_k1 [B][7],
+ * tau_k/tau_k1 [B] -> A [B][15][15], Bm/Bp [B][15][7], w/x_end [B][15].
+ * status[b] != 0 is what the reference throws for interval b (the caller knows
+ * the interval index it passed as `interval_index`). */
+int ptopt_cuda_propagate_interval_batch(ptopt_cuda_handle* h, int batch, const double* x_k,
+                                        const double* u_k, const double* u_k1, const double* tau_k,
+                                        const double* tau_k1, int steps, double* A, double* Bm,
+                                        double* Bp, double* w, double* x_end, int32_t* status);
+
 /* ---- scaled subproblem assembly ---------------------------------------- */
 
 /* Batched assemble_subproblem (proj/include/ptopt/scp.hpp:139-217) for the

@@ -25,6 +25,7 @@ EXPORTS = [
     "ptopt_cuda_create", "ptopt_cuda_destroy", "ptopt_cuda_synchronize",
     "ptopt_cuda_set_solver_path",
     "ptopt_cuda_linearize_batch", "ptopt_cuda_linearize_batch_dev",
+    "ptopt_cuda_propagate_interval_batch",
     "ptopt_cuda_assemble_batch", "ptopt_cuda_subproblem_shape",
     "ptopt_cuda_power_iteration_batch", "ptopt_cuda_power_iteration_batch_dev",
     "ptopt_cuda_pipg_batch", "ptopt_cuda_pipg_batch_dev",
@@ -167,6 +168,20 @@ class Solver:
         _check(self.lib.ptopt_cuda_linearize_batch(
             self._h, C.c_int(B), _hp(x), _hp(u), _hp(out["A"]), _hp(out["Bm"]), _hp(out["Bp"]),
             _hp(out["w"]), _hp(out["x_end"]), _hp(out["status"]), _hp(out["fail_index"])))
+        return out
+
+    def propagate_interval(self, x_k, u_k, u_k1, tau_k, tau_k1, steps):
+        """Batched propagate_interval (discretizer.hpp:82-149): one row per interval."""
+        x_k, u_k, u_k1 = _np(x_k), _np(u_k), _np(u_k1)
+        tau_k, tau_k1 = _np(tau_k), _np(tau_k1)
+        B = x_k.shape[0]
+        out = dict(A=np.empty((B, abi.NX, abi.NX)), Bm=np.empty((B, abi.NX, abi.NU)),
+                   Bp=np.empty((B, abi.NX, abi.NU)), w=np.empty((B, abi.NX)),
+                   x_end=np.empty((B, abi.NX)), status=np.empty(B, np.int32))
+        _check(self.lib.ptopt_cuda_propagate_interval_batch(
+            self._h, C.c_int(B), _hp(x_k), _hp(u_k), _hp(u_k1), _hp(tau_k), _hp(tau_k1),
+            C.c_int(steps), _hp(out["A"]), _hp(out["Bm"]), _hp(out["Bp"]), _hp(out["w"]),
+            _hp(out["x_end"]), _hp(out["status"])))
         return out
 
     def linearize_all_dev(self, x, u, A, Bm, Bp, w, x_end, status=None, fail_index=None):

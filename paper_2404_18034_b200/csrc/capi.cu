@@ -56,7 +56,7 @@ enum BufId {
   B_X, B_U, B_A, B_BM, B_BP, B_W, B_XEND, B_STATUS, B_FAILIDX, B_FAILKEY, B_INIT,
   B_AM, B_AP, B_BMH, B_BPH, B_WH, B_EPS, B_UMIN, B_UMAX, B_INITVAL, B_FINALVAL,
   B_SEEDX, B_SEEDU, B_SEEDP, B_SEEDN, B_SIGMA, B_TRIPS, B_ITERS, B_CONV,
-  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR,
+  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR, B_TAU,
   // SCP loop state (separate so a stand-alone call never disturbs a captured graph)
   S_ZX, S_ZU, S_INIT, S_SEED, S_A, S_BM, S_BP, S_W, S_XEND, S_AM, S_BMH, S_BPH, S_WH, S_EPS,
   S_UMIN, S_UMAX, S_INITVAL, S_FINALVAL, S_SEEDX, S_SEEDU, S_WSX, S_WSU, S_WSP, S_WSN, S_WSD,
@@ -269,6 +269,7 @@ LinearizeArgs linearize_args(ptopt_cuda_handle* h, int batch, const double* x, c
   a.nodes = h->desc.nodes;
   a.steps = h->desc.integrator_steps;
   a.tau = h->d_tau;
+  a.tau_stride = 0;
   a.x = x;
   a.u = u;
   a.A = A;
@@ -678,6 +679,64 @@ int ptopt_cuda_linearize_batch(ptopt_cuda_handle* h, int batch, const double* x,
   PT_TRY(download(h, x_end, dxe, B * m * kNX));
   PT_TRY(download(h, status, dst, B));
   PT_TRY(download(h, fail_index, dfi, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_propagate_interval_batch(ptopt_cuda_handle* h, int batch, const double* x_k,
+                                        const double* u_k, const double* u_k1, const double* tau_k,
+                                        const double* tau_k1, int steps, double* A, double* Bm,
+                                        double* Bp, double* w, double* x_end, int32_t* status) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (steps < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "propagate_interval: steps must be >= 1");
+  if (!x_k || !u_k || !u_k1 || !tau_k || !tau_k1 || !A || !Bm || !Bp || !w || !x_end)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "propagate_interval: null array");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch;
+  // every interval becomes a two-node instance with its own grid {tau_k, tau_k1}
+  std::vector<double> hx(B * 2 * kNX, 0.0), hu(B * 2 * kNU), ht(B * 2);
+  for (size_t b = 0; b < B; ++b) {
+    for (int i = 0; i < kNX; ++i) hx[b * 2 * kNX + i] = x_k[b * kNX + i];
+    for (int i = 0; i < kNU; ++i) {
+      hu[b * 2 * kNU + i] = u_k[b * kNU + i];
+      hu[b * 2 * kNU + kNU + i] = u_k1[b * kNU + i];
+    }
+    ht[b * 2] = tau_k[b];
+    ht[b * 2 + 1] = tau_k1[b];
+  }
+  const double *dx, *du, *dt;
+  double *dA, *dBm, *dBp, *dw, *dxe;
+  int *dst, *dfi, *dkey;
+  PT_TRY(upload(h, B_X, hx.data(), hx.size(), &dx));
+  PT_TRY(upload(h, B_U, hu.data(), hu.size(), &du));
+  PT_TRY(upload(h, B_TAU, ht.data(), ht.size(), &dt));
+  PT_CUDA(cudaStreamSynchronize(h->stream));  // the staging vectors die with this call
+  PT_TRY(device_out(h, B_A, B * kNX * kNX, &dA));
+  PT_TRY(device_out(h, B_BM, B * kNX * kNU, &dBm));
+  PT_TRY(device_out(h, B_BP, B * kNX * kNU, &dBp));
+  PT_TRY(device_out(h, B_W, B * kNX, &dw));
+  PT_TRY(device_out(h, B_XEND, B * kNX, &dxe));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
+  PT_TRY(device_out(h, B_FAILKEY, B, &dkey));
+  LinearizeArgs a = linearize_args(h, batch, dx, du, dA, dBm, dBp, dw, dxe, dkey, nullptr);
+  a.nodes = 2;
+  a.steps = steps;
+  a.tau = dt;
+  a.tau_stride = 2;
+  launch_init_fail_key(dkey, batch, h->stream);
+  launch_linearize(a, h->stream);
+  launch_decode_fail_key(dkey, batch, dst, dfi, h->stream);
+  h->launches += 3;
+  PT_CUDA(cudaGetLastError());
+  PT_TRY(download(h, A, dA, B * kNX * kNX));
+  PT_TRY(download(h, Bm, dBm, B * kNX * kNU));
+  PT_TRY(download(h, Bp, dBp, B * kNX * kNU));
+  PT_TRY(download(h, w, dw, B * kNX));
+  PT_TRY(download(h, x_end, dxe, B * kNX));
+  PT_TRY(download(h, status, dst, B));
   PT_CUDA(cudaStreamSynchronize(h->stream));
   return PTOPT_OK;
 }

@@ -52,7 +52,8 @@ linearize_kernel(LinearizeArgs a) {
   }
 
   double col[kNX], x_end[kNX];
-  const int rc = propagate_lane(a.model, lane, lane == 0, ws.sc, xk, uk, uk1, a.tau[k], a.tau[k + 1],
+  const double* tau = a.tau + (size_t)b * a.tau_stride;
+  const int rc = propagate_lane(a.model, lane, lane == 0, ws.sc, xk, uk, uk1, tau[k], tau[k + 1],
                                 a.steps, col, x_end, WarpSync());
   if (rc != kStOk) {
     // first failing interval wins, as the serial reference loop would report it

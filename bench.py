@@ -162,8 +162,8 @@ def run_own_arm(args):
     import numpy as np
     import torch
 
-    from paper_2404_18034_b200 import scenario
-    from paper_2404_18034_b200.binding import Solver
+    from paper_2404_18034_b200 import scenario, sharding
+    from paper_2404_18034_b200.binding import RECORD_DTYPE, Solver
 
     rank, local_rank, world = dist_env()
     if not torch.cuda.is_available():
@@ -184,8 +184,9 @@ def run_own_arm(args):
     sc = scenario.default_scenario(n)
     desc = sc.problem_desc()
     mi = int(desc.max_iters)
-    ids = range(rank * B, (rank + 1) * B)  # weak scaling: B run ids per rank
-    batch = scenario.make_batch(sc, ids)
+    first_id, count = sharding.shard_range(world * B, world, rank)  # weak scaling: B ids per rank
+    assert count == B
+    batch = scenario.make_batch(sc, range(first_id, first_id + B))
 
     stream = torch.cuda.Stream(device=dev)
     solver = Solver(desc, device=local_rank, stream=stream)
@@ -265,11 +266,24 @@ def run_own_arm(args):
     e2e_s = time.perf_counter() - t0
     assert np.array_equal(h_out["x"], d_x.cpu().numpy()), "e2e and device-resident results differ"
 
+    # ---- the reference-facing batch call, mc::run_batch: generation, solve, audit and records on
+    #      the device; only the dispersion spec goes in and the RunRecords come back
+    spec = sc.dispersion
+    records = torch.empty(B * RECORD_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy().view(RECORD_DTYPE)
+    barrier()
+    t0 = time.perf_counter()
+    solver.run_batch(B, first_id, sc.initial_state, spec.r_low, spec.r_high, spec.seed,
+                     audit_substeps=sc.audit_substeps, records=records)
+    torch.cuda.synchronize()
+    rb_s = time.perf_counter() - t0
+    assert (records["run_id"] == np.arange(first_id, first_id + B)).all()
+    assert np.array_equal(records["scp_iterations"], h_out["scp_iterations"])
+
     # ---- max over ranks
     if use_dist:
-        t = torch.tensor([ms_total, e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, e2e_s = float(t[0]), float(t[1])
+        ms_total = sharding.max_over_ranks(ms_total)
+        e2e_s = sharding.max_over_ranks(e2e_s)
+        rb_s = sharding.max_over_ranks(rb_s)
         bad = torch.tensor([int((status != 0).sum())], device=dev)
         dist.all_reduce(bad)
         n_bad = int(bad[0])
@@ -296,6 +310,13 @@ def run_own_arm(args):
             "clocks": clocks.summary(),
             "e2e": {"value": world * B * e2e_steps / e2e_s, "unit": "solves/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+            "e2e_run_batch": {"value": world * B / rb_s, "unit": "solves/s",
+                              "call": "ptopt_cuda_run_batch (mc::run_batch: generation + solve + audit "
+                                      "+ records on the device)",
+                              "h2d_bytes_per_step": 8 * (14 + 7 + 4 * n),
+                              "d2h_bytes_per_step": int(records.nbytes),
+                              "converged_fraction": float(records["converged"].mean()),
+                              "propellant_mean": float(records["propellant_used"].mean())},
             "gpu_launches": int(launches),
             "stages_ms": stages,
             "work": {"power_trips_mean": sum_trips / B, "pipg_iterations_mean": pipg_iters / B,

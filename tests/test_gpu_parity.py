@@ -501,3 +501,69 @@ def test_run_batch_records_match_oracle(ptor):
     for f in ("run_id", "converged", "scp_iterations", "propellant_used", "final_defect_inf",
               "max_pointwise_g", "max_node_y_increase"):
         np.testing.assert_array_equal(tail[f], rec[f][5:9])
+
+
+def test_cuda_path_against_golden_vectors():
+    """The CUDA path against the vectors the unmodified reference produced
+    (tests/golden/make_golden.py) — no oracle in the loop."""
+    from pathlib import Path
+
+    from paper_2404_18034_b200.binding import Solver
+
+    gold = dict(np.load(Path(__file__).resolve().parent / "golden" / "reference_vectors.npz"))
+    sc15 = scenario.default_scenario(15)
+    with Solver(sc15.problem_desc()) as s:
+        B = gold["pi_x"].shape[0]
+        out = s.propagate_interval(gold["pi_x"], gold["pi_u"], gold["pi_u1"],
+                                   np.full(B, gold["pi_tau"][0]), np.full(B, gold["pi_tau"][1]), 16)
+        assert (out["status"] == 0).all()
+        for k, g in (("A", "pi_A"), ("Bm", "pi_Bm"), ("Bp", "pi_Bp"), ("w", "pi_w"), ("x_end", "pi_x_end")):
+            for b in range(B):
+                assert rel_err(out[k][b], gold[g][b]) <= TOL_DISC, (k, b)
+    sc = scenario.default_scenario(10)
+    spec = sc.dispersion
+    init = np.array(sc.initial_state)
+    init[1:4] = gold["gen_r"][0]
+    with Solver(sc.problem_desc()) as s:
+        gen = s.generate_batch(1, 4095, sc.initial_state, spec.r_low, spec.r_high, spec.seed)
+        np.testing.assert_array_equal(gen["x_guess"][0], gold["gen_x"][3])
+        np.testing.assert_array_equal(gen["u_guess"][0], gold["gen_u"][3])
+        assert gen["rng_seed"][0] == gold["gen_seed"][3]
+        lin = s.linearize_all(gold["gen_x"][:1], gold["gen_u"][:1])
+        for k, g in (("A", "lin_A"), ("Bm", "lin_Bm"), ("Bp", "lin_Bp"), ("w", "lin_w"), ("x_end", "lin_x_end")):
+            assert rel_err(lin[k][0], gold[g]) <= TOL_DISC, k
+        gb = {k: gold[g][None] for k, g in (("A", "lin_A"), ("Bm", "lin_Bm"), ("Bp", "lin_Bp"),
+                                            ("x_end", "lin_x_end"))}
+        asm = s.assemble_subproblem(init[None], gold["gen_x"][:1], gold["gen_u"][:1], gb)
+        for f, g in (("A_minus", "asm_A_minus"), ("B_minus", "asm_B_minus"), ("B_plus", "asm_B_plus"),
+                     ("w", "asm_w"), ("eps_relax", "asm_eps"), ("u_min", "asm_u_min"),
+                     ("u_max", "asm_u_max"), ("init_fix_val", "asm_init"), ("final_fix_val", "asm_final")):
+            np.testing.assert_array_equal(asm[f][0], gold[g])  # power-of-two scaling: exact
+        shape = s.subproblem_shape()
+        sub = {f: asm[f] for f in ("A_minus", "B_minus", "B_plus", "w", "eps_relax", "u_min", "u_max",
+                                    "init_fix_val", "final_fix_val")}
+        z = np.zeros((1, 9, 15))
+        sigma, _, st = s.power_iteration_custom(shape, sub, gold["pw_seed_x"][None], gold["pw_seed_u"][None],
+                                                z, z, 1e-12, 1e-12, 0.05, 10000)
+        assert st[0] == 0 and abs(sigma[0] / float(gold["pw_sigma"]) - 1.0) <= TOL_SIGMA
+        cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=300, j_check=301, eps_abs=1e-11, eps_rel=1e-11,
+                             eps_buff=0.05)
+        ws = ws_dict(Workspace(NX, NU, 10))
+        it, _, st, _ = s.pipg_custom(shape, sub, cfg, [float(gold["pw_sigma"])], ws)
+        assert st[0] == 0 and it[0] == 300
+        for f in Workspace.FIELDS:
+            assert np.abs(ws[f][0] - gold[f"pipg_{f}"]).max() <= TOL_ITER, f
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 4, 300, 400
+    with Solver(sc.problem_desc()) as s:
+        res = s.scp_solve(init[None], gold["gen_x"][:1], gold["gen_u"][:1], gold["gen_seed"][:1])
+        assert res["status"][0] == 0 and res["scp_iterations"][0] == gold["scp_meta"][0]
+        assert np.abs(res["x"][0] - gold["scp_x"]).max() <= TOL_ITER
+        assert np.abs(res["u"][0] - gold["scp_u"]).max() <= TOL_ITER
+        np.testing.assert_array_equal(res["history"][0][:, 3], gold["scp_history"][:, 3])
+        rec = s.run_batch(3, 0, sc.initial_state, spec.r_low, spec.r_high, spec.seed, audit_substeps=16)
+        ref = gold["rb_records"]
+        assert (rec["status"] == 0).all() and (ref[:, 7] == 0).all()
+        np.testing.assert_array_equal(rec["scp_iterations"], ref[:, 2].astype(np.int32))
+        for f, c in (("propellant_used", 3), ("final_defect_inf", 4), ("max_pointwise_g", 5),
+                     ("max_node_y_increase", 6)):
+            assert np.abs(rec[f] - ref[:, c]).max() <= TOL_ITER, f

@@ -279,6 +279,20 @@ def run_own_arm(args):
     assert (records["run_id"] == np.arange(first_id, first_id + B)).all()
     assert np.array_equal(records["scp_iterations"], h_out["scp_iterations"])
 
+    # ---- p50 latency of a single full solve (batch of one) through the host-pointer call
+    lat_ms = []
+    if rank == 0 and args.latency_runs > 0:
+        one = {k: np.ascontiguousarray(h_in[k][:1]) for k in h_in}
+        one_out = {k: np.ascontiguousarray(v[:1]) for k, v in h_out.items()}
+        with Solver(desc, device=local_rank) as single:
+            single.scp_solve_into(one["init_state"], one["x_guess"], one["u_guess"], one["rng_seed"], one_out)
+            for _ in range(args.latency_runs):
+                t0 = time.perf_counter()
+                single.scp_solve_into(one["init_state"], one["x_guess"], one["u_guess"], one["rng_seed"],
+                                      one_out)
+                lat_ms.append(1e3 * (time.perf_counter() - t0))
+        assert np.array_equal(one_out["x"][0], h_out["x"][0]), "batch-of-one result differs"
+
     # ---- max over ranks
     if use_dist:
         ms_total = sharding.max_over_ranks(ms_total)
@@ -317,6 +331,10 @@ def run_own_arm(args):
                               "d2h_bytes_per_step": int(records.nbytes),
                               "converged_fraction": float(records["converged"].mean()),
                               "propellant_mean": float(records["propellant_used"].mean())},
+            "single_solve_latency_ms": {"p50": statistics.median(lat_ms) if lat_ms else None,
+                                        "min": min(lat_ms) if lat_ms else None, "runs": len(lat_ms),
+                                        "what": "one N=50 instance, full 25-iteration budget, "
+                                                "ptopt_cuda_scp_solve_batch with host buffers"},
             "gpu_launches": int(launches),
             "stages_ms": stages,
             "work": {"power_trips_mean": sum_trips / B, "pipg_iterations_mean": pipg_iters / B,
@@ -361,6 +379,8 @@ def main():
     ap.add_argument("--cpu-instances", type=int, default=0,
                     help="instances in the CPU sample (default: one per host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-runs", type=int, default=5,
+                    help="batch-of-one solves timed for the p50 single-solve latency (0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -15,6 +15,7 @@ namespace ptopt_b200 {
 namespace {
 
 constexpr int kMaxWarps = 32;
+constexpr int kMaxGenericThreads = 768;  // 72 registers per thread must fit one SM's register file
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -45,7 +46,7 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ M, int rows
   return acc;
 }
 
-__global__ void power_generic_kernel(PowerArgs a) {
+__global__ void __launch_bounds__(kMaxGenericThreads, 1) power_generic_kernel(PowerArgs a) {
   extern __shared__ double sm[];
   const int b = blockIdx.x;
   if (a.active && !a.active[b]) return;
@@ -179,7 +180,7 @@ __global__ void power_generic_kernel(PowerArgs a) {
   }
 }
 
-__global__ void pipg_generic_kernel(PipgArgs a) {
+__global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(PipgArgs a) {
   extern __shared__ double sm[];
   const int b = blockIdx.x;
   if (a.active && !a.active[b]) return;
@@ -439,7 +440,7 @@ __global__ void pipg_generic_kernel(PipgArgs a) {
 int solver_generic_threads(const SubShape& s) {
   int t = ((s.n * s.nx + 31) / 32) * 32;
   if (t < 64) t = 64;
-  if (t > 1024) t = 1024;
+  if (t > kMaxGenericThreads) t = kMaxGenericThreads;
   return t;
 }
 

@@ -567,3 +567,102 @@ def test_cuda_path_against_golden_vectors():
         for f, c in (("propellant_used", 3), ("final_defect_inf", 4), ("max_pointwise_g", 5),
                      ("max_node_y_increase", 6)):
             assert np.abs(rec[f] - ref[:, c]).max() <= TOL_ITER, f
+
+
+# ---------------------------------------------------------------- BASELINE configs at full size
+def test_config3_pipg_2000_iterations_batch1024_n50(ptor):
+    """BASELINE config 3: fixed 2000 PIPG iterations, batch 1024, N=50.  Subproblems of the first
+    8 dispersed instances (CPU-assembled, sigma injected from the CPU power iteration) tiled to
+    1024; a subset is compared with the oracle, the rest through invariants: identical inputs
+    give identical outputs wherever they sit in the batch, slacks / relaxation dual are
+    nonnegative, boundary rows equal their targets, controls stay in the box."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(50)
+    d = sc.problem_desc()
+    n, m, base, B = 50, 49, 8, 1024
+    subs, sigmas = [], []
+    shape = rocket_shape(d)
+    for rid in range(base):
+        init = scenario.disperse(sc, rid)
+        x, u = scenario.initial_guess(sc, init)
+        rc, blocks = ptor.linearize_all(d, x, u)
+        assert rc == 0
+        rc, sub, _ = ptor.assemble(d, init, x, u, blocks)
+        assert rc == 0
+        sx, su = ptor.scp_seed(scenario.run_seed(sc.dispersion.seed, rid), n)
+        z = np.zeros((m, NX))
+        rc, sigma, _ = ptor.power_iteration(shape, sub, sx, su, z, z, 1e-12, 1e-12, 0.05, 10000)
+        assert rc == 0
+        subs.append(sub)
+        sigmas.append(sigma)
+    tile = np.arange(B) % base
+    fields = ("A_minus", "B_minus", "B_plus", "w", "eps_relax", "u_min", "u_max", "init_fix_val",
+              "final_fix_val")
+    batch = {f: np.stack([getattr(subs[i], f) for i in range(base)])[tile] for f in fields}
+    sig = np.array(sigmas)[tile]
+    cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=2000, j_check=2001, eps_abs=1e-11, eps_rel=1e-11,
+                         eps_buff=0.05)
+    ws = {f: np.zeros((B,) + getattr(Workspace(NX, NU, n), f).shape) for f in Workspace.FIELDS}
+    with Solver(d) as s:
+        it, conv, status, _ = s.pipg_custom(s.subproblem_shape(), batch, cfg, sig, ws)
+    assert (status == 0).all() and (it == 2000).all() and not conv.any()
+    for i in (0, 5):  # oracle parity on two of the base instances (the CPU needs ~0.3 s each)
+        ref = Workspace(NX, NU, n)
+        rc, it_ref, _, _ = ptor.pipg(shape, subs[i], cfg, sigmas[i], ref)
+        assert rc == 0 and it_ref == 2000
+        for f in Workspace.FIELDS:
+            assert np.abs(ws[f][i] - getattr(ref, f)).max() <= TOL_ITER, f
+    for f in Workspace.FIELDS:  # position independence / determinism across the batch
+        np.testing.assert_array_equal(ws[f], ws[f][:base][tile])
+    assert (ws["vc_pos"] >= 0).all() and (ws["vc_neg"] >= 0).all() and (ws["relax_dual"] >= 0).all()
+    np.testing.assert_array_equal(ws["x"][:, 0, :], batch["init_fix_val"])
+    fin_idx = [int(i) for i in d.final_fix_idx[: d.n_final_fix]]
+    np.testing.assert_array_equal(ws["x"][:, -1, fin_idx], batch["final_fix_val"])
+    assert (ws["u"] >= batch["u_min"]).all() and (ws["u"] <= batch["u_max"]).all()
+
+
+def test_config4_scp_batch4096_n50_properties():
+    """BASELINE config 4 shape (batch 4096, N=50) with a reduced iteration budget: the graph
+    relaunch is deterministic, every instance's result is independent of where it sits in the
+    batch (a permuted batch gives permuted results), all instances finish with status ok and
+    unit quaternions, and the history rows past the last iteration are zero."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(50)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 60, 80
+    d = sc.problem_desc()
+    B, base = 4096, 64
+    small = scenario.make_batch(sc, range(base))
+    rng = np.random.default_rng(7)
+    tile = rng.integers(0, base, B)
+    tile[:base] = np.arange(base)
+    big = {k: small[k][tile] for k in ("init_state", "x_guess", "u_guess", "rng_seed")}
+    with Solver(d) as s:
+        out = s.scp_solve(big["init_state"], big["x_guess"], big["u_guess"], big["rng_seed"])
+        again = s.scp_solve(big["init_state"], big["x_guess"], big["u_guess"], big["rng_seed"])
+    assert (out["status"] == 0).all() and (out["scp_iterations"] == 2).all()
+    for k in ("x", "u", "history", "power_trips", "final_defect_inf"):
+        np.testing.assert_array_equal(out[k], again[k])
+        np.testing.assert_array_equal(out[k], out[k][:base][tile])
+    q = out["x"][:, :, 7:11]
+    assert np.abs(np.linalg.norm(q, axis=2) - 1.0).max() <= 1e-14
+    assert (out["history"][:, :, 3] == 60).all() and (out["power_trips"] > 0).all()
+
+
+def test_config5_n100_runs_on_the_generic_kernels(ptor):
+    """BASELINE config 5 shape (N=100): above the register-resident kernels' node limit, served by
+    the shape-generic kernels; reduced budget, parity with the oracle on two instances."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(100)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 150, 200
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [3, 65535])
+    with Solver(d) as s:
+        out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+    for b in range(2):
+        rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                                 int(batch["rng_seed"][b]), with_trips=True)
+        assert rc == 0
+        check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])

@@ -34,6 +34,8 @@ constexpr int kUS = 10;      // node stride of u vectors
 constexpr int kPS = 35;      // stride of one thread's partial-sum slot (== 3 mod 16: conflict-free)
 constexpr int kFastThreads = 256;
 constexpr int kFastWarps = kFastThreads / 32;
+static_assert((kFastThreads - 1) / kG <= kFastMaxNodes, "every thread needs a (scratch) node inside the layout");
+static_assert(kG * kFastMaxNodes <= kFastThreads, "five threads per node");
 
 // position of a column's partial sum inside a slot: x columns first, then the B- / B+ columns
 // interleaved so that the five owners of a node read with a 3-double spacing (no bank conflicts)
@@ -177,7 +179,7 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
   L.us = o; o += (n + 2) * kUS;
   L.phi = o + kNX + 1; o += even_up((n + 2) * kNX + 2);
   L.theta = o + 2; o += even_up(n + 4);
-  L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + kFastThreads * kPS + kPS);
+  L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + (n + 2) * kG * kPS);
   L.red = o; o += 16 * kFastWarps;
   if (pipg) {
     L.wv = o; o += even_up((n + 2) * kNX);
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
-  const int kc = k < n ? k : n;  // idle threads work on the scratch node
+  const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
   constexpr FastLayout L = fast_layout(false);
   for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
   __syncthreads();
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   double* slot = part + (size_t)tid * kPS;
   const double* part_k = part + (size_t)kc * kG * kPS;  // slots of interval k; k-1 at -kG*kPS
   double* red = sm + L.red;
-  const int ju1 = g < 2 ? g + 5 : 8;            // second control entry (8: padding)
+  const int ju1 = g + 5;                        // second control entry (g >= 2: a padding slot of its own)
 
   double aop[kR][kW];
   double vcp[kR], vcn[kR];
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
-  const int kc = k < n ? k : n;  // idle threads work on the scratch node
+  const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
   constexpr FastLayout L = fast_layout(true);
   constexpr SnapLayout S = snap_layout();
   for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   double* final_val = init_val + 16;
   double* init_on = final_val + 16;
   double* final_on = init_on + 16;
-  const int ju1 = g < 2 ? g + 5 : 8;  // second control entry (8: padding)
+  const int ju1 = g + 5;  // second control entry (g >= 2: a padding slot of its own)
 
   const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
   if (tid < kNX) ecost[tid] = a.shape.e_cost[tid];

@@ -202,11 +202,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   if (a.active && !a.active[b]) return;
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x, nwarps = T >> 5;  // launched with just enough warps for 5 threads per node
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
   const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
   constexpr FastLayout L = fast_layout(false);
-  for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
+  for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
   __syncthreads();
   double* xs_k = sm + L.xs + kc * kXS;          // x_k; x_{k+1} at +kXS
   double* us_k = sm + L.us + kc * kUS;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   __syncthreads();
   double sigma = 0.0;
 #pragma unroll
-  for (int w = 0; w < kFastWarps; ++w) sigma += red[w];
+  for (int w = 0; w < kFastWarps; ++w) sigma += w < nwarps ? red[w] : 0.0;
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (tid == 0) {
       if (a.status) a.status[b] = kStSeedZero;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
       const double* rd = red + (((j - 1) & 1) ? kFastWarps : 0);
       double sq = 0.0;
 #pragma unroll
-      for (int w = 0; w < kFastWarps; ++w) sq += rd[w];
+      for (int w = 0; w < kFastWarps; ++w) sq += w < nwarps ? rd[w] : 0.0;
       const double sigma_star = sqrt(sq);
       if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         sigma = 0.0;
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     const double* rd = red + ((a.j_max & 1) ? kFastWarps : 0);
     double sq = 0.0;
 #pragma unroll
-    for (int w = 0; w < kFastWarps; ++w) sq += rd[w];
+    for (int w = 0; w < kFastWarps; ++w) sq += w < nwarps ? rd[w] : 0.0;
     sigma = sqrt(sq);
   }
   if (tid == 0) {
@@ -385,12 +386,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   if (a.active && !a.active[b]) return;
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x, nwarps = T >> 5;  // launched with just enough warps for 5 threads per node
   const int k = tid / kG, g = tid - k * kG;
   const bool node = k < n, ival = k < m;
   const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
   constexpr FastLayout L = fast_layout(true);
   constexpr SnapLayout S = snap_layout();
-  for (int e = tid; e < L.total; e += kFastThreads) sm[e] = 0.0;
+  for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
   __syncthreads();
   double* xr_k = sm + L.xs + kc * kXS;   // reflections 2*cur - ex (pipg.hpp:436-443); k+1 at +kXS
   double* ur_k = sm + L.us + kc * kUS;
@@ -425,21 +427,21 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
     }
   }
-  for (int e = tid; e < NM; e += kFastThreads) sm[L.wv + e] = a.sp.w[(size_t)b * NM + e];
-  for (int e = tid; e < m; e += kFastThreads) sm[L.eps + e] = a.sp.eps_relax[(size_t)b * m + e];
-  for (int e = tid; e < NUn; e += kFastThreads) {
+  for (int e = tid; e < NM; e += T) sm[L.wv + e] = a.sp.w[(size_t)b * NM + e];
+  for (int e = tid; e < m; e += T) sm[L.eps + e] = a.sp.eps_relax[(size_t)b * m + e];
+  for (int e = tid; e < NUn; e += T) {
     sm[L.umin + e] = a.sp.u_min[(size_t)b * NUn + e];
     sm[L.umax + e] = a.sp.u_max[(size_t)b * NUn + e];
   }
   // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
-  for (int e = tid; e < NXn; e += kFastThreads) snap0[S.x + e] = a.ws.x[(size_t)b * NXn + e];
-  for (int e = tid; e < NUn; e += kFastThreads) snap0[S.u + e] = a.ws.u[(size_t)b * NUn + e];
-  for (int e = tid; e < NM; e += kFastThreads) {
+  for (int e = tid; e < NXn; e += T) snap0[S.x + e] = a.ws.x[(size_t)b * NXn + e];
+  for (int e = tid; e < NUn; e += T) snap0[S.u + e] = a.ws.u[(size_t)b * NUn + e];
+  for (int e = tid; e < NM; e += T) {
     snap0[S.vp + e] = a.ws.vc_pos[(size_t)b * NM + e];
     snap0[S.vn + e] = a.ws.vc_neg[(size_t)b * NM + e];
     snap0[S.ph + e] = a.ws.dyn_dual[(size_t)b * NM + e];
   }
-  for (int e = tid; e < m; e += kFastThreads) snap0[S.th + e] = a.ws.relax_dual[(size_t)b * m + e];
+  for (int e = tid; e < m; e += T) snap0[S.th + e] = a.ws.relax_dual[(size_t)b * m + e];
 
   double aop[kR][kW];
 #pragma unroll
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
       double bad = 0.0;
       auto primal = [&](int off, int count, bool finite_checked) {
-        for (int e = tid; e < count; e += kFastThreads) {
+        for (int e = tid; e < count; e += T) {
           const double c = cur[off + e], o = prev[off + e];
           z_cur = fmax(z_cur, fabs(c));
           z_prev = fmax(z_prev, fabs(o));
@@ -625,7 +627,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         }
       };
       auto dual = [&](int off, int count, bool finite_checked) {
-        for (int e = tid; e < count; e += kFastThreads) {
+        for (int e = tid; e < count; e += T) {
           const double c = cur[off + e], o = prev[off + e];
           r_cur = fmax(r_cur, fabs(c));
           r_prev = fmax(r_prev, fabs(o));
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       for (int q = 0; q < 7; ++q) {
         double mx = 0.0;
 #pragma unroll
-        for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, red[w * 8 + q]);
+        for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, w < nwarps ? red[w * 8 + q] : 0.0);
         v[q] = mx;
       }
       __syncthreads();  // red and the snapshots are rewritten later
@@ -682,14 +684,14 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   // solution = the *_cur groups, pipg.hpp:490-495 (all threads passed a barrier after the last
   // snapshot write)
   const double* cur = snap0 + cur_set * S.total;
-  for (int e = tid; e < NXn; e += kFastThreads) a.ws.x[(size_t)b * NXn + e] = cur[S.x + e];
-  for (int e = tid; e < NUn; e += kFastThreads) a.ws.u[(size_t)b * NUn + e] = cur[S.u + e];
-  for (int e = tid; e < NM; e += kFastThreads) {
+  for (int e = tid; e < NXn; e += T) a.ws.x[(size_t)b * NXn + e] = cur[S.x + e];
+  for (int e = tid; e < NUn; e += T) a.ws.u[(size_t)b * NUn + e] = cur[S.u + e];
+  for (int e = tid; e < NM; e += T) {
     a.ws.vc_pos[(size_t)b * NM + e] = cur[S.vp + e];
     a.ws.vc_neg[(size_t)b * NM + e] = cur[S.vn + e];
     a.ws.dyn_dual[(size_t)b * NM + e] = cur[S.ph + e];
   }
-  for (int e = tid; e < m; e += kFastThreads) a.ws.relax_dual[(size_t)b * m + e] = cur[S.th + e];
+  for (int e = tid; e < m; e += T) a.ws.relax_dual[(size_t)b * m + e] = cur[S.th + e];
   if (tid == 0) {
     if (a.iterations) a.iterations[b] = iters;
     if (a.converged) a.converged[b] = converged ? 1 : 0;
@@ -717,13 +719,16 @@ cudaError_t configure_solver_fast(const SubShape& s) {
                               (int)pipg_fast_smem(s));
 }
 
+/// Just enough warps for five threads per node (the kernels size their loops by blockDim).
+static int fast_threads(const SubShape& s) { return ((kG * s.n + 31) / 32) * 32; }
+
 cudaError_t launch_power_fast(const PowerArgs& a, cudaStream_t stream) {
-  power_fast_kernel<<<a.batch, kFastThreads, power_fast_smem(a.shape), stream>>>(a);
+  power_fast_kernel<<<a.batch, fast_threads(a.shape), power_fast_smem(a.shape), stream>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pipg_fast(const PipgArgs& a, cudaStream_t stream) {
-  pipg_fast_kernel<<<a.batch, kFastThreads, pipg_fast_smem(a.shape), stream>>>(a);
+  pipg_fast_kernel<<<a.batch, fast_threads(a.shape), pipg_fast_smem(a.shape), stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -666,3 +666,23 @@ def test_config5_n100_runs_on_the_generic_kernels(ptor):
                                  int(batch["rng_seed"][b]), with_trips=True)
         assert rc == 0
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+
+
+@pytest.mark.parametrize("nodes", [2, 3, 32, 51, 52])
+def test_scp_solve_node_count_edges(ptor, nodes):
+    """Node counts at the edges of the register-resident kernels: the minimum grid, a count whose
+    thread groups fill the warps exactly (32), the largest supported (51) and the first one that
+    falls back to the shape-generic kernels (52)."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(nodes)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 120, 150
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [0, 11])
+    with Solver(d) as s:
+        out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+    for b in range(2):
+        rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                                 int(batch["rng_seed"][b]), with_trips=True)
+        assert rc == 0
+        check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])

@@ -314,6 +314,21 @@ def run_own_arm(args):
         dom = max(("linearize", "power_iteration", "pipg"), key=lambda k: stages[k])
         achieved = flop[dom] / (stages[dom] * 1e-3) * 1e-12
         total_flop = sum(flop.values())
+        # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+        # (profiles/ncu_traffic.json: bytes for a 148-instance launch), scaled to this batch
+        traffic = None
+        kernel_of = {"linearize": "linearize_kernel", "power_iteration": "power_fast_kernel",
+                     "pipg": "pipg_fast_kernel"}
+        tpath = ROOT / "profiles" / "ncu_traffic.json"
+        if tpath.exists() and n == 50:
+            tk = json.loads(tpath.read_text())["kernels"].get(kernel_of[dom])
+            if tk:
+                per_instance = (tk["dram_read_bytes"] + tk["dram_write_bytes"]) / 148.0
+                traffic = per_instance * B
+        m_int = n - 1
+        compulsory = {"linearize": B * (n * 22 + m_int * 465) * 8,
+                      "power_iteration": B * (m_int * 435 + n * 22 + 2 * m_int * 15) * 8,
+                      "pipg": B * (m_int * 435 + 2 * (n * 22 + m_int * 46) + m_int * 16 + 2 * n * 7) * 8}
         value = world * B * args.steps / (ms_total * 1e-3)
         line = {
             "metric": "SCP solves/sec (batched, N=50)", "value": value, "unit": "solves/s",
@@ -346,7 +361,9 @@ def run_own_arm(args):
                 "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
                                "no fp64 entry)",
-                "traffic": None,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, scaled from a "
+                                                    "148-instance capture)",
+                "compulsory_hbm_bytes_per_launch": compulsory[dom],
                 "per_stage": {k: {"tflops": flop[k] / (stages[k] * 1e-3) * 1e-12,
                                   "frac": flop[k] / (stages[k] * 1e-3) * 1e-12 / fp64_peak,
                                   "share_of_step": stages[k] / stages["graph_total"]}

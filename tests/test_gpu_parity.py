@@ -686,3 +686,31 @@ def test_scp_solve_node_count_edges(ptor, nodes):
                                  int(batch["rng_seed"][b]), with_trips=True)
         assert rc == 0
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+
+
+def test_solver_divergence_inside_the_scp_loop(ptor):
+    """A spectral estimate cut off after one power-iteration trip is far too small, the step
+    sizes are too large and PIPG blows up: the reference throws SolverDiverged at the stopping
+    check that first sees a non-finite iterate.  Inside the batched loop every instance stops
+    with the same status and iteration index (they differ between instances)."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(12)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 3, 2500, 1
+    sc.pipg_eps_buff = 0.0
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [0, 1])
+    refs = []
+    for b in range(2):
+        rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                                 int(batch["rng_seed"][b]))
+        assert rc == abi.ST_SOLVER_DIVERGED, rc
+        refs.append(ref["fail_index"])
+    assert refs[0] != refs[1]
+    for path in ("auto", "generic"):
+        with Solver(d) as s:
+            s.set_solver_path(path)
+            out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+        assert (out["status"] == abi.ST_SOLVER_DIVERGED).all()
+        assert list(out["fail_index"]) == refs, (out["fail_index"], refs)
+        assert (out["scp_iterations"] == 0).all() and not out["converged"].any()

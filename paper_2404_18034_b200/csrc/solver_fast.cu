@@ -184,8 +184,8 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
   if (pipg) {
     L.wv = o; o += even_up((n + 2) * kNX);
     L.eps = o; o += even_up(n + 2);
-    L.umin = o; o += even_up((n + 2) * kNU + 4);
-    L.umax = o; o += even_up((n + 2) * kNU + 4);
+    L.umin = o; o += 2 * kFastThreads;  // {lo, hi} of each thread's first control entry
+    L.umax = o; o += 2 * kFastThreads;  // {lo, hi} of its second one (+-inf where it has none)
     L.snap = o; o += 2 * snap_layout().total;
     L.bnd = o; o += 6 * 16;  // ecost, init_val, final_val, init_on, final_on (as doubles)
   }
@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   double* red = sm + L.red;
   const double* wv_k = sm + L.wv + kc * kNX + kR * g;
   const double* eps_k = sm + L.eps + kc;
-  const double* umin_k = sm + L.umin + kc * kNU;
-  const double* umax_k = sm + L.umax + kc * kNU;
+  double2* bnd0 = reinterpret_cast<double2*>(sm + L.umin) + tid;  // conflict-free 16-byte slots
+  double2* bnd1 = reinterpret_cast<double2*>(sm + L.umax) + tid;
   double* snap0 = sm + L.snap;  // two snapshots of the *_cur groups, written alternately
   double* ecost = sm + L.bnd;
   double* init_val = ecost + 16;
@@ -429,9 +429,11 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   }
   for (int e = tid; e < NM; e += T) sm[L.wv + e] = a.sp.w[(size_t)b * NM + e];
   for (int e = tid; e < m; e += T) sm[L.eps + e] = a.sp.eps_relax[(size_t)b * m + e];
-  for (int e = tid; e < NUn; e += T) {
-    sm[L.umin + e] = a.sp.u_min[(size_t)b * NUn + e];
-    sm[L.umax + e] = a.sp.u_max[(size_t)b * NUn + e];
+  {  // box of this thread's control entries (pipg.hpp:418-419); scratch entries are unbounded
+    const double* lo = a.sp.u_min + (size_t)b * NUn + k * kNU;
+    const double* hi = a.sp.u_max + (size_t)b * NUn + k * kNU;
+    *bnd0 = node ? make_double2(lo[g], hi[g]) : make_double2(-INFINITY, INFINITY);
+    *bnd1 = (node && g < 2) ? make_double2(lo[g + 5], hi[g + 5]) : make_double2(-INFINITY, INFINITY);
   }
   // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
   for (int e = tid; e < NXn; e += T) snap0[S.x + e] = a.ws.x[(size_t)b * NXn + e];
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       if (on[kR * g + r] != 0.0) fix_bits |= 1 << r;
   }
   const bool last_node = k == n - 1;
+  const bool warp_fix = __any_sync(0xffffffffu, fix_bits != 0);  // warp-uniform
 
   // owner-private extrapolated copies
   double xe[kR], ue[2], vpe[kR], vne[kR], phe[kR], the = 0.0;
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const int i = kR * g + r;
-      fv[r] = fix_val[i];
+      fv[r] = warp_fix ? fix_val[i] : 0.0;
       double t = xe[r] * a.shape.w_prox;
       if (last_node) t += a.shape.w_cost * ecost[i];
       t += -phx_k[r - kNX];
@@ -520,8 +523,9 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int ju = q == 0 ? g : ju1;
-      lo[q] = umin_k[ju];
-      hi[q] = umax_k[ju];
+      const double2 bq = q == 0 ? *bnd0 : *bnd1;
+      lo[q] = bq.x;
+      hi[q] = bq.y;
       su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g) +
               column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
     }

@@ -18,11 +18,15 @@
 // :307-326 (stopping_custom), :335-340 (step_sizes), :350-497 (pipg_custom).  Sums over the
 // fifteen rows of a column are grouped three rows at a time, and FMA contraction is on; both
 // change rounding only (measured sensitivity of the whole loop: 1e-13).
+#include <cooperative_groups.h>
+
 #include <type_traits>
 
 #include "kernels.cuh"
 
 namespace ptopt_b200 {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -180,7 +184,7 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
   L.phi = o + kNX + 1; o += even_up((n + 2) * kNX + 2);
   L.theta = o + 2; o += even_up(n + 4);
   L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + (n + 2) * kG * kPS);
-  L.red = o; o += 16 * kFastWarps;
+  L.red = o; o += 16 * kFastWarps;  // power: [2][warps] own + [2][warps] partner; pipg: [warps][8]
   if (pipg) {
     L.wv = o; o += even_up((n + 2) * kNX);
     L.eps = o; o += even_up(n + 2);
@@ -194,17 +198,84 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Horizon split.  Up to kFastMaxNodes nodes one CTA holds the whole instance.  Above that (up to
+// 2 * kFastMaxNodes) a thread-block cluster of two CTAs shares it: rank 0 takes the first
+// ceil(n/2) nodes, rank 1 the rest; each keeps its operator rows in its own SM's registers.  The
+// only coupling across the cut is the one between neighbouring nodes, so after every phase each
+// CTA copies the few boundary values it needs from its partner's shared memory (DSMEM) into the
+// guard entries the single-CTA code already reads: rank 0 the partner's first node vectors into
+// its "next node" slot, rank 1 the partner's last interval (partial sums, duals) into its
+// "previous interval" slots.  Phase barriers become cluster barriers.
+// ---------------------------------------------------------------------------------------------
+struct Split {
+  int rank;   // CTA rank inside the cluster (0 without clusters)
+  int node0;  // first global node of this CTA
+  int nloc;   // nodes of this CTA
+  int half;   // nodes of rank 0
+};
+
+template <bool kCluster>
+__device__ __forceinline__ Split make_split(int n) {
+  Split sp;
+  if constexpr (kCluster) {
+    sp.rank = (int)cg::this_cluster().block_rank();
+    sp.half = (n + 1) / 2;
+    sp.node0 = sp.rank * sp.half;
+    sp.nloc = sp.rank == 0 ? sp.half : n - sp.half;
+  } else {
+    sp.rank = 0;
+    sp.half = n;
+    sp.node0 = 0;
+    sp.nloc = n;
+  }
+  return sp;
+}
+
+/// Partial-sum positions of the B+ columns (read by the next node's control owners).
+__device__ __forceinline__ int bp_position(int c) { return c < 5 ? 17 + 3 * c : 22 + 3 * (c - 5); }
+
+/// rank 1: the partner's last interval -> this CTA's "previous interval" guard entries
+/// (B+ partial sums of its five slots, extrapolated / scaled duals).  Called by every thread of
+/// rank 1 after a cluster barrier; followed by a block barrier.
+__device__ __forceinline__ void pull_prev_interval(double* sm, const double* remote, int off_part,
+                                                   int off_phi, int off_theta, int last, int tid) {
+  if (tid < kG * kNU) {
+    const int q = tid / kNU, pos = bp_position(tid - q * kNU);
+    sm[off_part - kG * kPS + q * kPS + pos] = remote[off_part + (last * kG + q) * kPS + pos];
+  } else if (tid < kG * kNU + kNX) {
+    const int i = tid - kG * kNU;
+    sm[off_phi - kNX + i] = remote[off_phi + last * kNX + i];
+  } else if (tid == kG * kNU + kNX) {
+    sm[off_theta - 1] = remote[off_theta + last];
+  }
+}
+
+/// rank 0: the partner's first node vectors -> this CTA's "next node" entries.
+__device__ __forceinline__ void pull_next_node(double* sm, const double* remote, int off_x, int off_u,
+                                               int next, int tid) {
+  if (tid < kNX) {
+    sm[off_x + next * kXS + tid] = remote[off_x + tid];
+  } else if (tid < kNX + kNU) {
+    const int i = tid - kNX;
+    sm[off_u + next * kUS + i] = remote[off_u + i];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
+template <bool kCluster>
 __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int b = blockIdx.x;
-  if (a.active && !a.active[b]) return;
+  const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
+  if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   const int n = a.shape.n, m = n - 1;
+  const Split cut = make_split<kCluster>(n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockDim.x, nwarps = T >> 5;  // launched with just enough warps for 5 threads per node
-  const int k = tid / kG, g = tid - k * kG;
-  const bool node = k < n, ival = k < m;
+  const int k = tid / kG, g = tid - k * kG;   // local node, row group
+  const int kg = cut.node0 + k;               // global node
+  const bool node = k < cut.nloc, ival = node && kg < m;
   const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
   constexpr FastLayout L = fast_layout(false);
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
@@ -216,8 +287,39 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   double* part = sm + L.part;
   double* slot = part + (size_t)tid * kPS;
   const double* part_k = part + (size_t)kc * kG * kPS;  // slots of interval k; k-1 at -kG*kPS
-  double* red = sm + L.red;
+  double* red = sm + L.red;       // [2][kFastWarps] own partial sums of the norm, by trip parity
+  double* redp = red + 2 * kFastWarps;  // the partner's (clusters only)
   const int ju1 = g + 5;                        // second control entry (g >= 2: a padding slot of its own)
+  const double* remote = nullptr;
+  if constexpr (kCluster) remote = cg::this_cluster().map_shared_rank(sm, cut.rank ^ 1);
+
+  // phase barriers (+ the boundary exchange of a cluster)
+  auto after_forward = [&]() {  // partial sums and duals are written
+    if constexpr (kCluster) {
+      cg::this_cluster().sync();
+      if (cut.rank == 1) pull_prev_interval(sm, remote, L.part, L.phi, L.theta, cut.half - 1, tid);
+    }
+    __syncthreads();
+  };
+  auto after_adjoint = [&](int parity) {  // node vectors and the norm's partial sums are written
+    if constexpr (kCluster) {
+      cg::this_cluster().sync();
+      if (cut.rank == 0) pull_next_node(sm, remote, L.xs, L.us, cut.nloc, tid);
+      if (tid >= 32 && tid < 32 + nwarps)
+        redp[parity * kFastWarps + tid - 32] = remote[L.red + parity * kFastWarps + tid - 32];
+    }
+    __syncthreads();
+  };
+  auto norm_sq = [&](int parity) {  // sum of both CTAs' partial sums, rank 0's first
+    double own = 0.0, other = 0.0;
+#pragma unroll
+    for (int w = 0; w < kFastWarps; ++w) {
+      own += w < nwarps ? red[parity * kFastWarps + w] : 0.0;
+      if constexpr (kCluster) other += w < nwarps ? redp[parity * kFastWarps + w] : 0.0;
+    }
+    if constexpr (kCluster) return cut.rank == 0 ? own + other : other + own;
+    return own;
+  };
 
   double aop[kR][kW];
   double vcp[kR], vcn[kR];
@@ -227,13 +329,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
 #pragma unroll
     for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
   }
-  if (ival) load_rows(a.sp, b, m, k, g, aop);
+  if (ival) load_rows(a.sp, b, m, kg, g, aop);
 
   // seed (pipg.hpp:213-230): x, u, vc+, vc-; sigma0 = ||seed||_2
   double acc = 0.0;
   if (node) {
-    const double* sx = a.seed_x + ((size_t)b * n + k) * kNX;
-    const double* su = a.seed_u + ((size_t)b * n + k) * kNU;
+    const double* sx = a.seed_x + ((size_t)b * n + kg) * kNX;
+    const double* su = a.seed_u + ((size_t)b * n + kg) * kNU;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const double v = sx[kR * g + r];
@@ -252,8 +354,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     }
   }
   if (ival) {
-    const double* sp = a.seed_vcp + ((size_t)b * m + k) * kNX;
-    const double* sn = a.seed_vcn + ((size_t)b * m + k) * kNX;
+    const double* sp = a.seed_vcp + ((size_t)b * m + kg) * kNX;
+    const double* sn = a.seed_vcn + ((size_t)b * m + kg) * kNX;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       vcp[r] = sp[kR * g + r];
@@ -264,16 +366,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   }
   acc = warp_sum(acc);
   if (lane == 0) red[warp] = acc;
-  __syncthreads();
-  double sigma = 0.0;
-#pragma unroll
-  for (int w = 0; w < kFastWarps; ++w) sigma += w < nwarps ? red[w] : 0.0;
+  after_adjoint(0);  // also brings rank 0 the partner's first node of the seed
+  double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
-    if (tid == 0) {
+    if (tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSeedZero;
       a.sigma[b] = 0.0;
       if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
     }
+    if constexpr (kCluster) cg::this_cluster().sync();  // the partner may still be reading
     return;
   }
   sigma = sqrt(sigma);
@@ -301,11 +402,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     }
     const double dy = xs_k[kXS + 14] - v[14];
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
-      const double* rd = red + (((j - 1) & 1) ? kFastWarps : 0);
-      double sq = 0.0;
-#pragma unroll
-      for (int w = 0; w < kFastWarps; ++w) sq += w < nwarps ? rd[w] : 0.0;
-      const double sigma_star = sqrt(sq);
+      const double sigma_star = sqrt(norm_sq((j - 1) & 1));
       if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         sigma = 0.0;
         done = true;
@@ -337,7 +434,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
       acc_d += phi[r] * phi[r];
       acc_d += phi[r] * phi[r];
     }
-    __syncthreads();
+    after_forward();
     // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
     double sx[kR];
 #pragma unroll
@@ -361,35 +458,34 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     acc_u += g < 2 ? su1 * su1 : 0.0;
     acc = node ? (acc_x + acc_u) + acc_d : 0.0;
     acc = warp_sum(acc);
-    if (lane == 0) red[((j & 1) ? kFastWarps : 0) + warp] = acc;
-    __syncthreads();
+    if (lane == 0) red[(j & 1) * kFastWarps + warp] = acc;
+    after_adjoint(j & 1);
   }
-  if (!done) {  // j_max trips without meeting the tolerance: sigma is the last norm
-    const double* rd = red + ((a.j_max & 1) ? kFastWarps : 0);
-    double sq = 0.0;
-#pragma unroll
-    for (int w = 0; w < kFastWarps; ++w) sq += w < nwarps ? rd[w] : 0.0;
-    sigma = sqrt(sq);
-  }
-  if (tid == 0) {
+  if (!done) sigma = sqrt(norm_sq(a.j_max & 1));  // j_max trips without meeting the tolerance
+  if (tid == 0 && cut.rank == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sigma;
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
   }
+  if constexpr (kCluster) cg::this_cluster().sync();  // the partner may still be reading
 }
 
 // ---------------------------------------------------------------------------------------------
 // customized PIPG (pipg.hpp:350-497)
 // ---------------------------------------------------------------------------------------------
+template <bool kCluster>
 __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int b = blockIdx.x;
-  if (a.active && !a.active[b]) return;
+  const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
+  if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   const int n = a.shape.n, m = n - 1;
+  const Split cut = make_split<kCluster>(n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int T = blockDim.x, nwarps = T >> 5;  // launched with just enough warps for 5 threads per node
-  const int k = tid / kG, g = tid - k * kG;
-  const bool node = k < n, ival = k < m;
+  const int k = tid / kG, g = tid - k * kG;   // local node, row group
+  const int kg = cut.node0 + k;               // global node
+  const bool node = k < cut.nloc, ival = node && kg < m;
   const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
+  const int mloc = cut.nloc - (cut.node0 + cut.nloc == n ? 1 : 0);  // intervals owned by this CTA
   constexpr FastLayout L = fast_layout(true);
   constexpr SnapLayout S = snap_layout();
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
@@ -413,8 +509,29 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   double* init_on = final_val + 16;
   double* final_on = init_on + 16;
   const int ju1 = g + 5;  // second control entry (g >= 2: a padding slot of its own)
+  const double* remote = nullptr;
+  if constexpr (kCluster) remote = cg::this_cluster().map_shared_rank(sm, cut.rank ^ 1);
 
-  const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
+  // phase barriers (+ the boundary exchange of a cluster)
+  auto after_dual = [&]() {  // partial sums and extrapolated duals are written
+    if constexpr (kCluster) {
+      cg::this_cluster().sync();
+      if (cut.rank == 1) pull_prev_interval(sm, remote, L.part, L.phi, L.theta, cut.half - 1, tid);
+    }
+    __syncthreads();
+  };
+  auto after_primal = [&]() {  // reflections are written
+    if constexpr (kCluster) {
+      cg::this_cluster().sync();
+      if (cut.rank == 0) pull_next_node(sm, remote, L.xs, L.us, cut.nloc, tid);
+    }
+    __syncthreads();
+  };
+
+  // this CTA's share of the instance-major global arrays
+  const size_t gx = ((size_t)b * n + cut.node0) * kNX, gu = ((size_t)b * n + cut.node0) * kNU;
+  const size_t gm = ((size_t)b * m + cut.node0) * kNX, gt = (size_t)b * m + cut.node0;
+  const int NXn = cut.nloc * kNX, NUn = cut.nloc * kNU, NM = mloc * kNX;
   if (tid < kNX) ecost[tid] = a.shape.e_cost[tid];
   if (tid == 0) {
     // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
@@ -427,43 +544,43 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
     }
   }
-  for (int e = tid; e < NM; e += T) sm[L.wv + e] = a.sp.w[(size_t)b * NM + e];
-  for (int e = tid; e < m; e += T) sm[L.eps + e] = a.sp.eps_relax[(size_t)b * m + e];
+  for (int e = tid; e < NM; e += T) sm[L.wv + e] = a.sp.w[gm + e];
+  for (int e = tid; e < mloc; e += T) sm[L.eps + e] = a.sp.eps_relax[gt + e];
   {  // box of this thread's control entries (pipg.hpp:418-419); scratch entries are unbounded
-    const double* lo = a.sp.u_min + (size_t)b * NUn + k * kNU;
-    const double* hi = a.sp.u_max + (size_t)b * NUn + k * kNU;
+    const double* lo = a.sp.u_min + gu + k * kNU;
+    const double* hi = a.sp.u_max + gu + k * kNU;
     *bnd0 = node ? make_double2(lo[g], hi[g]) : make_double2(-INFINITY, INFINITY);
     *bnd1 = (node && g < 2) ? make_double2(lo[g + 5], hi[g + 5]) : make_double2(-INFINITY, INFINITY);
   }
   // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
-  for (int e = tid; e < NXn; e += T) snap0[S.x + e] = a.ws.x[(size_t)b * NXn + e];
-  for (int e = tid; e < NUn; e += T) snap0[S.u + e] = a.ws.u[(size_t)b * NUn + e];
+  for (int e = tid; e < NXn; e += T) snap0[S.x + e] = a.ws.x[gx + e];
+  for (int e = tid; e < NUn; e += T) snap0[S.u + e] = a.ws.u[gu + e];
   for (int e = tid; e < NM; e += T) {
-    snap0[S.vp + e] = a.ws.vc_pos[(size_t)b * NM + e];
-    snap0[S.vn + e] = a.ws.vc_neg[(size_t)b * NM + e];
-    snap0[S.ph + e] = a.ws.dyn_dual[(size_t)b * NM + e];
+    snap0[S.vp + e] = a.ws.vc_pos[gm + e];
+    snap0[S.vn + e] = a.ws.vc_neg[gm + e];
+    snap0[S.ph + e] = a.ws.dyn_dual[gm + e];
   }
-  for (int e = tid; e < m; e += T) snap0[S.th + e] = a.ws.relax_dual[(size_t)b * m + e];
+  for (int e = tid; e < mloc; e += T) snap0[S.th + e] = a.ws.relax_dual[gt + e];
 
   double aop[kR][kW];
 #pragma unroll
   for (int r = 0; r < kR; ++r)
 #pragma unroll
     for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
-  if (ival) load_rows(a.sp, b, m, k, g, aop);
+  if (ival) load_rows(a.sp, b, m, kg, g, aop);
   __syncthreads();
 
   // boundary rows of this thread (pipg.hpp:408-413): bit r set when row 3g+r is assigned
   int fix_bits = 0;
   const double* fix_val = init_val;
-  if (k == 0 || k == n - 1) {
-    const double* on = k == n - 1 ? final_on : init_on;
-    fix_val = k == n - 1 ? final_val : init_val;
+  const bool last_node = node && kg == n - 1;
+  if (node && (kg == 0 || kg == n - 1)) {
+    const double* on = last_node ? final_on : init_on;
+    fix_val = last_node ? final_val : init_val;
 #pragma unroll
     for (int r = 0; r < kR; ++r)
       if (on[kR * g + r] != 0.0) fix_bits |= 1 << r;
   }
-  const bool last_node = k == n - 1;
   const bool warp_fix = __any_sync(0xffffffffu, fix_bits != 0);  // warp-uniform
 
   // owner-private extrapolated copies
@@ -497,7 +614,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
   const double one_m_rho = 1.0 - a.rho;
-  __syncthreads();
+  after_dual();
 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into the
   // snapshot `snap` (threads without a node / interval write scratch entries).
@@ -522,7 +639,6 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
     double su[2], lo[2], hi[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int ju = q == 0 ? g : ju1;
       const double2 bq = q == 0 ? *bnd0 : *bnd1;
       lo[q] = bq.x;
       hi[q] = bq.y;
@@ -555,7 +671,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       }
       ue[q] = one_m_rho * u0 + a.rho * un;
     }
-    __syncthreads();
+    after_primal();
 
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
     //      extrapolation of the dual groups (:468-472) and the partial sums of H^T phi_ex for
@@ -615,7 +731,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       iteration(std::false_type{}, nullptr);
     }
     iters = j;
-    __syncthreads();
+    after_dual();
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
       const double* cur = snap0 + cur_set * S.total;
       const double* prev = snap0 + (cur_set ^ 1) * S.total;
@@ -644,7 +760,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       primal(S.vp, NM, false);
       primal(S.vn, NM, false);
       dual(S.ph, NM, true);
-      dual(S.th, m, false);
+      dual(S.th, mloc, false);
       z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
       r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
       bad = warp_max(bad);
@@ -662,7 +778,18 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, w < nwarps ? red[w * 8 + q] : 0.0);
         v[q] = mx;
       }
-      __syncthreads();  // red and the snapshots are rewritten later
+      if constexpr (kCluster) {  // combine with the partner's maxima (seven DSMEM loads per thread)
+        if (tid == 0) {
+#pragma unroll
+          for (int q = 0; q < 7; ++q) red[kFastWarps * 8 + q] = v[q];
+        }
+        cg::this_cluster().sync();
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v[q] = fmax(v[q], remote[L.red + kFastWarps * 8 + q]);
+        cg::this_cluster().sync();  // red and the snapshots are rewritten later
+      } else {
+        __syncthreads();  // red and the snapshots are rewritten later
+      }
       if (v[6] > 0.0) {
         diverged = true;
         break;
@@ -676,37 +803,39 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   }
 
   if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
-    if (tid == 0) {
+    if (tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSolverDiverged;
       if (a.fail_index) a.fail_index[b] = iters;
       if (a.iterations) a.iterations[b] = iters;
       if (a.converged) a.converged[b] = 0;
       if (a.active) a.active[b] = 0;
     }
+    if constexpr (kCluster) cg::this_cluster().sync();  // nobody leaves while the partner reads
     return;
   }
   // solution = the *_cur groups, pipg.hpp:490-495 (all threads passed a barrier after the last
   // snapshot write)
   const double* cur = snap0 + cur_set * S.total;
-  for (int e = tid; e < NXn; e += T) a.ws.x[(size_t)b * NXn + e] = cur[S.x + e];
-  for (int e = tid; e < NUn; e += T) a.ws.u[(size_t)b * NUn + e] = cur[S.u + e];
+  for (int e = tid; e < NXn; e += T) a.ws.x[gx + e] = cur[S.x + e];
+  for (int e = tid; e < NUn; e += T) a.ws.u[gu + e] = cur[S.u + e];
   for (int e = tid; e < NM; e += T) {
-    a.ws.vc_pos[(size_t)b * NM + e] = cur[S.vp + e];
-    a.ws.vc_neg[(size_t)b * NM + e] = cur[S.vn + e];
-    a.ws.dyn_dual[(size_t)b * NM + e] = cur[S.ph + e];
+    a.ws.vc_pos[gm + e] = cur[S.vp + e];
+    a.ws.vc_neg[gm + e] = cur[S.vn + e];
+    a.ws.dyn_dual[gm + e] = cur[S.ph + e];
   }
-  for (int e = tid; e < m; e += T) a.ws.relax_dual[(size_t)b * m + e] = cur[S.th + e];
-  if (tid == 0) {
+  for (int e = tid; e < mloc; e += T) a.ws.relax_dual[gt + e] = cur[S.th + e];
+  if (tid == 0 && cut.rank == 0) {
     if (a.iterations) a.iterations[b] = iters;
     if (a.converged) a.converged[b] = converged ? 1 : 0;
   }
+  if constexpr (kCluster) cg::this_cluster().sync();  // nobody leaves while the partner reads
 }
 
 }  // namespace
 
 bool solver_fast_supports(const SubShape& s, bool has_a_plus) {
   if (has_a_plus || s.nx != kNX || s.nu != kNU) return false;
-  if (s.n < 2 || s.n > kFastMaxNodes) return false;
+  if (s.n < 2 || s.n > 2 * kFastMaxNodes) return false;
   for (int i = 0; i < kNX; ++i)
     if (s.e_y[i] != (i == kNX - 1 ? 1.0 : 0.0)) return false;
   return true;
@@ -716,24 +845,57 @@ size_t power_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_l
 size_t pipg_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_layout(true).total; }
 
 cudaError_t configure_solver_fast(const SubShape& s) {
-  cudaError_t e = cudaFuncSetAttribute(power_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)power_fast_smem(s));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(pipg_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)pipg_fast_smem(s));
+  const int ps = (int)power_fast_smem(s), gs = (int)pipg_fast_smem(s);
+  cudaError_t e = cudaFuncSetAttribute(power_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(power_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(pipg_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gs);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(pipg_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gs);
+  return e;
 }
 
-/// Just enough warps for five threads per node (the kernels size their loops by blockDim).
-static int fast_threads(const SubShape& s) { return ((kG * s.n + 31) / 32) * 32; }
+namespace {
+
+/// One CTA per instance up to kFastMaxNodes nodes, a cluster of two above.
+bool needs_cluster(const SubShape& s) { return s.n > kFastMaxNodes; }
+
+/// Just enough warps for five threads per (local) node; the kernels size their loops by blockDim.
+int fast_threads(const SubShape& s) {
+  const int nodes = needs_cluster(s) ? (s.n + 1) / 2 : s.n;
+  return ((kG * nodes + 31) / 32) * 32;
+}
+
+template <class Args>
+cudaError_t launch_fast(void (*single)(Args), void (*paired)(Args), const Args& a, size_t smem,
+                        cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3((unsigned)fast_threads(a.shape));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr{};
+  if (needs_cluster(a.shape)) {
+    cfg.gridDim = dim3(2u * (unsigned)a.batch);
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, paired, a);
+  }
+  cfg.gridDim = dim3((unsigned)a.batch);
+  return cudaLaunchKernelEx(&cfg, single, a);
+}
+
+}  // namespace
 
 cudaError_t launch_power_fast(const PowerArgs& a, cudaStream_t stream) {
-  power_fast_kernel<<<a.batch, fast_threads(a.shape), power_fast_smem(a.shape), stream>>>(a);
-  return cudaGetLastError();
+  return launch_fast<PowerArgs>(power_fast_kernel<false>, power_fast_kernel<true>, a, power_fast_smem(a.shape),
+                                stream);
 }
 
 cudaError_t launch_pipg_fast(const PipgArgs& a, cudaStream_t stream) {
-  pipg_fast_kernel<<<a.batch, fast_threads(a.shape), pipg_fast_smem(a.shape), stream>>>(a);
-  return cudaGetLastError();
+  return launch_fast<PipgArgs>(pipg_fast_kernel<false>, pipg_fast_kernel<true>, a, pipg_fast_smem(a.shape),
+                               stream);
 }
 
 }  // namespace ptopt_b200

@@ -650,29 +650,34 @@ def test_config4_scp_batch4096_n50_properties():
     assert (out["history"][:, :, 3] == 60).all() and (out["power_trips"] > 0).all()
 
 
-def test_config5_n100_runs_on_the_generic_kernels(ptor):
-    """BASELINE config 5 shape (N=100): above the register-resident kernels' node limit, served by
-    the shape-generic kernels; reduced budget, parity with the oracle on two instances."""
+@pytest.mark.parametrize("path", ["auto", "generic"])
+def test_config5_n100_cluster_and_generic_kernels(ptor, path):
+    """BASELINE config 5 shape (N=100): above the single-CTA node limit, so each instance is split
+    over a two-CTA cluster ('auto'); the shape-generic kernels serve it too ('generic').  Reduced
+    budget with stopping checks, parity with the oracle on three instances."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(100)
     sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 150, 200
     d = sc.problem_desc()
-    batch = scenario.make_batch(sc, [3, 65535])
+    batch = scenario.make_batch(sc, [3, 65535, 12])
     with Solver(d) as s:
+        s.set_solver_path(path)
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
-    for b in range(2):
+    for b in range(3):
         rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
                                  int(batch["rng_seed"][b]), with_trips=True)
         assert rc == 0
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-@pytest.mark.parametrize("nodes", [2, 3, 32, 51, 52])
+@pytest.mark.parametrize("nodes", [2, 3, 32, 51, 52, 64, 77, 102, 103])
 def test_scp_solve_node_count_edges(ptor, nodes):
     """Node counts at the edges of the register-resident kernels: the minimum grid, a count whose
-    thread groups fill the warps exactly (32), the largest supported (51) and the first one that
-    falls back to the shape-generic kernels (52)."""
+    thread groups fill the warps exactly (32), the largest single-CTA count (51), the first one
+    that is split over a two-CTA cluster (52), cluster splits with an even / odd node count and no
+    idle threads (64, 77), the largest cluster count (102) and the first one that falls back to
+    the shape-generic kernels (103)."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(nodes)

@@ -156,7 +156,7 @@ struct SnapLayout {
   int x, u, vp, vn, ph, th, total;
 };
 __host__ __device__ constexpr SnapLayout snap_layout() {
-  constexpr int n = kFastMaxNodes + 2;
+  constexpr int n = kFastMaxNodes + 3;
   SnapLayout S{};
   int o = 0;
   S.x = o; o += n * kNX;
@@ -179,15 +179,15 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
   constexpr int n = kFastMaxNodes;  // fixed offsets: every address is base + immediate
   FastLayout L{};
   int o = 0;
-  L.xs = o; o += (n + 2) * kXS;
-  L.us = o; o += (n + 2) * kUS;
-  L.phi = o + kNX + 1; o += even_up((n + 2) * kNX + 2);
-  L.theta = o + 2; o += even_up(n + 4);
-  L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + (n + 2) * kG * kPS);
+  L.xs = o; o += (n + 4) * kXS;
+  L.us = o; o += (n + 4) * kUS;
+  L.phi = o + kNX + 1; o += even_up((n + 3) * kNX + 2);
+  L.theta = o + 2; o += even_up(n + 6);
+  L.part = o + kG * kPS + 1; o += even_up(kG * kPS + 1 + (n + 3) * kG * kPS);
   L.red = o; o += 16 * kFastWarps;  // power: [2][warps] own + [2][warps] partner; pipg: [warps][8]
   if (pipg) {
-    L.wv = o; o += even_up((n + 2) * kNX);
-    L.eps = o; o += even_up(n + 2);
+    L.wv = o; o += even_up((n + 3) * kNX);
+    L.eps = o; o += even_up(n + 4);
     L.umin = o; o += 2 * kFastThreads;  // {lo, hi} of each thread's first control entry
     L.umax = o; o += 2 * kFastThreads;  // {lo, hi} of its second one (+-inf where it has none)
     L.snap = o; o += 2 * snap_layout().total;
@@ -201,11 +201,12 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
 // Horizon split.  Up to kFastMaxNodes nodes one CTA holds the whole instance.  Above that (up to
 // 2 * kFastMaxNodes) a thread-block cluster of two CTAs shares it: rank 0 takes the first
 // ceil(n/2) nodes, rank 1 the rest; each keeps its operator rows in its own SM's registers.  The
-// only coupling across the cut is the one between neighbouring nodes, so after every phase each
-// CTA copies the few boundary values it needs from its partner's shared memory (DSMEM) into the
-// guard entries the single-CTA code already reads: rank 0 the partner's first node vectors into
-// its "next node" slot, rank 1 the partner's last interval (partial sums, duals) into its
-// "previous interval" slots.  Phase barriers become cluster barriers.
+// only coupling across the cut is the one between neighbouring nodes, so the owners of the boundary
+// values store them twice: locally, and through distributed shared memory into the guard entries
+// the partner's single-CTA code already reads — rank 1's first node vectors into rank 0's "next
+// node" slot, rank 0's last interval (B+ partial sums, duals) into rank 1's "previous interval"
+// slots, every warp's share of a reduction into the partner's copy.  Phase barriers become
+// cluster barriers (release / acquire), nothing is ever read remotely.
 // ---------------------------------------------------------------------------------------------
 struct Split {
   int rank;   // CTA rank inside the cluster (0 without clusters)
@@ -231,34 +232,17 @@ __device__ __forceinline__ Split make_split(int n) {
   return sp;
 }
 
-/// Partial-sum positions of the B+ columns (read by the next node's control owners).
-__device__ __forceinline__ int bp_position(int c) { return c < 5 ? 17 + 3 * c : 22 + 3 * (c - 5); }
-
-/// rank 1: the partner's last interval -> this CTA's "previous interval" guard entries
-/// (B+ partial sums of its five slots, extrapolated / scaled duals).  Called by every thread of
-/// rank 1 after a cluster barrier; followed by a block barrier.
-__device__ __forceinline__ void pull_prev_interval(double* sm, const double* remote, int off_part,
-                                                   int off_phi, int off_theta, int last, int tid) {
-  if (tid < kG * kNU) {
-    const int q = tid / kNU, pos = bp_position(tid - q * kNU);
-    sm[off_part - kG * kPS + q * kPS + pos] = remote[off_part + (last * kG + q) * kPS + pos];
-  } else if (tid < kG * kNU + kNX) {
-    const int i = tid - kG * kNU;
-    sm[off_phi - kNX + i] = remote[off_phi + last * kNX + i];
-  } else if (tid == kG * kNU + kNX) {
-    sm[off_theta - 1] = remote[off_theta + last];
-  }
+/// Address of `local` (a pointer into this CTA's shared memory) inside CTA `rank` of the cluster.
+template <class T>
+__device__ __forceinline__ T* in_cta(T* local, int rank) {
+  return cg::this_cluster().map_shared_rank(local, rank);
 }
 
-/// rank 0: the partner's first node vectors -> this CTA's "next node" entries.
-__device__ __forceinline__ void pull_next_node(double* sm, const double* remote, int off_x, int off_u,
-                                               int next, int tid) {
-  if (tid < kNX) {
-    sm[off_x + next * kXS + tid] = remote[off_x + tid];
-  } else if (tid < kNX + kNU) {
-    const int i = tid - kNX;
-    sm[off_u + next * kUS + i] = remote[off_u + i];
-  }
+/// Copies the B+ partial sums a thread has just published in `slot` into `remote_slot` (the
+/// matching "previous interval" guard slot of the partner CTA).
+__device__ __forceinline__ void push_bp_partials(const double* slot, double* remote_slot) {
+#pragma unroll
+  for (int c = 0; c < kNU; ++c) remote_slot[pos_bp(c)] = slot[pos_bp(c)];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -276,10 +260,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   const int k = tid / kG, g = tid - k * kG;   // local node, row group
   const int kg = cut.node0 + k;               // global node
   const bool node = k < cut.nloc, ival = node && kg < m;
-  const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
+  // threads past the last node work on scratch nodes of their own; in a cluster node `nloc` of
+  // rank 0 is not scratch (the partner pushes its first node there), so they start one further
+  const int kc = (kCluster && k >= cut.nloc) ? k + 1 : k;
   constexpr FastLayout L = fast_layout(false);
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
-  __syncthreads();
+  // in a cluster: both CTAs are running and have cleared their memory before any remote store
+  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
   double* xs_k = sm + L.xs + kc * kXS;          // x_k; x_{k+1} at +kXS
   double* us_k = sm + L.us + kc * kUS;
   double* phi_k = sm + L.phi + kc * kNX + kR * g;  // own dual entries; interval k-1 at -kNX
@@ -290,25 +277,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   double* red = sm + L.red;       // [2][kFastWarps] own partial sums of the norm, by trip parity
   double* redp = red + 2 * kFastWarps;  // the partner's (clusters only)
   const int ju1 = g + 5;                        // second control entry (g >= 2: a padding slot of its own)
-  const double* remote = nullptr;
-  if constexpr (kCluster) remote = cg::this_cluster().map_shared_rank(sm, cut.rank ^ 1);
-
-  // phase barriers (+ the boundary exchange of a cluster)
-  auto after_forward = [&]() {  // partial sums and duals are written
-    if constexpr (kCluster) {
-      cg::this_cluster().sync();
-      if (cut.rank == 1) pull_prev_interval(sm, remote, L.part, L.phi, L.theta, cut.half - 1, tid);
-    }
-    __syncthreads();
-  };
-  auto after_adjoint = [&](int parity) {  // node vectors and the norm's partial sums are written
-    if constexpr (kCluster) {
-      cg::this_cluster().sync();
-      if (cut.rank == 0) pull_next_node(sm, remote, L.xs, L.us, cut.nloc, tid);
-      if (tid >= 32 && tid < 32 + nwarps)
-        redp[parity * kFastWarps + tid - 32] = remote[L.red + parity * kFastWarps + tid - 32];
-    }
-    __syncthreads();
+  // boundary owners of a cluster: the last node of rank 0 feeds rank 1's "previous interval"
+  // guard entries, the first node of rank 1 feeds rank 0's "next node" entries
+  const bool push_prev = kCluster && cut.rank == 0 && k == cut.half - 1;
+  const bool push_next = kCluster && cut.rank == 1 && k == 0 && node;
+  auto phase_barrier = [&]() {
+    if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
   };
   auto norm_sq = [&](int parity) {  // sum of both CTAs' partial sums, rank 0's first
     double own = 0.0, other = 0.0;
@@ -364,9 +338,19 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
       acc += vcn[r] * vcn[r];
     }
   }
+  if constexpr (kCluster) {  // rank 0's "next node" is the partner's first node
+    if (cut.rank == 0 && tid < kNX + kNU) {
+      const size_t gn = (size_t)b * n + cut.half;
+      if (tid < kNX) sm[L.xs + cut.nloc * kXS + tid] = a.seed_x[gn * kNX + tid];
+      else sm[L.us + cut.nloc * kUS + tid - kNX] = a.seed_u[gn * kNU + tid - kNX];
+    }
+  }
   acc = warp_sum(acc);
-  if (lane == 0) red[warp] = acc;
-  after_adjoint(0);  // also brings rank 0 the partner's first node of the seed
+  if (lane == 0) {
+    red[warp] = acc;
+    if constexpr (kCluster) *in_cta(redp + warp, cut.rank ^ 1) = acc;
+  }
+  phase_barrier();
   double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (tid == 0 && cut.rank == 0) {
@@ -423,8 +407,16 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
       phi[r] = ival ? s[r] * inv : 0.0;
       phi_k[r] = phi[r];
     }
-    if (g == 4) th_k[0] = ival ? dy / sigma : 0.0;
+    const double th = ival ? dy / sigma : 0.0;
+    if (g == 4) th_k[0] = th;
+    if (push_prev) {  // the same values into rank 1's guard entries for interval -1
+      double* rphi = in_cta(sm + L.phi - kNX + kR * g, 1);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) rphi[r] = phi[r];
+      if (g == 4) *in_cta(sm + L.theta - 1, 1) = th;
+    }
     store_partials(aop, phi, slot);
+    if (push_prev) push_bp_partials(slot, in_cta(part - kG * kPS + g * kPS, 1));
     // vc+ = phi, vc- = -phi and their share of the norm (pipg.hpp:268-279)
     double acc_d = 0.0;
 #pragma unroll
@@ -434,7 +426,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
       acc_d += phi[r] * phi[r];
       acc_d += phi[r] * phi[r];
     }
-    after_forward();
+    phase_barrier();
     // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
     double sx[kR];
 #pragma unroll
@@ -450,16 +442,25 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
         t += th_k[-1];
       }
       xs_k[kR * g + r] = t;
+      if (push_next) *in_cta(sm + L.xs + cut.half * kXS + kR * g + r, 0) = t;
       acc_x += t * t;
     }
     us_k[g] = su0;
     us_k[ju1] = su1;
+    if (push_next) {
+      double* ru = in_cta(sm + L.us + cut.half * kUS, 0);
+      ru[g] = su0;
+      if (g < 2) ru[g + 5] = su1;
+    }
     double acc_u = su0 * su0;
     acc_u += g < 2 ? su1 * su1 : 0.0;
     acc = node ? (acc_x + acc_u) + acc_d : 0.0;
     acc = warp_sum(acc);
-    if (lane == 0) red[(j & 1) * kFastWarps + warp] = acc;
-    after_adjoint(j & 1);
+    if (lane == 0) {
+      red[(j & 1) * kFastWarps + warp] = acc;
+      if constexpr (kCluster) *in_cta(redp + (j & 1) * kFastWarps + warp, cut.rank ^ 1) = acc;
+    }
+    phase_barrier();
   }
   if (!done) sigma = sqrt(norm_sq(a.j_max & 1));  // j_max trips without meeting the tolerance
   if (tid == 0 && cut.rank == 0) {
@@ -484,12 +485,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   const int k = tid / kG, g = tid - k * kG;   // local node, row group
   const int kg = cut.node0 + k;               // global node
   const bool node = k < cut.nloc, ival = node && kg < m;
-  const int kc = k;  // threads past the last node work on scratch nodes of their own (layout has kFastMaxNodes + 2)
+  // threads past the last node work on scratch nodes of their own; in a cluster node `nloc` of
+  // rank 0 is not scratch (the partner pushes its first node there), so they start one further
+  const int kc = (kCluster && k >= cut.nloc) ? k + 1 : k;
   const int mloc = cut.nloc - (cut.node0 + cut.nloc == n ? 1 : 0);  // intervals owned by this CTA
   constexpr FastLayout L = fast_layout(true);
   constexpr SnapLayout S = snap_layout();
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
-  __syncthreads();
+  // in a cluster: both CTAs are running and have cleared their memory before any remote store
+  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
   double* xr_k = sm + L.xs + kc * kXS;   // reflections 2*cur - ex (pipg.hpp:436-443); k+1 at +kXS
   double* ur_k = sm + L.us + kc * kUS;
   double* phx_k = sm + L.phi + kc * kNX + kR * g;  // extrapolated dynamics dual; k-1 at -kNX
@@ -509,23 +513,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   double* init_on = final_val + 16;
   double* final_on = init_on + 16;
   const int ju1 = g + 5;  // second control entry (g >= 2: a padding slot of its own)
-  const double* remote = nullptr;
-  if constexpr (kCluster) remote = cg::this_cluster().map_shared_rank(sm, cut.rank ^ 1);
-
-  // phase barriers (+ the boundary exchange of a cluster)
-  auto after_dual = [&]() {  // partial sums and extrapolated duals are written
-    if constexpr (kCluster) {
-      cg::this_cluster().sync();
-      if (cut.rank == 1) pull_prev_interval(sm, remote, L.part, L.phi, L.theta, cut.half - 1, tid);
-    }
-    __syncthreads();
-  };
-  auto after_primal = [&]() {  // reflections are written
-    if constexpr (kCluster) {
-      cg::this_cluster().sync();
-      if (cut.rank == 0) pull_next_node(sm, remote, L.xs, L.us, cut.nloc, tid);
-    }
-    __syncthreads();
+  // boundary owners of a cluster: the last node of rank 0 feeds rank 1's "previous interval"
+  // guard entries, the first node of rank 1 feeds rank 0's "next node" entries
+  const bool push_prev = kCluster && cut.rank == 0 && k == cut.half - 1;
+  const bool push_next = kCluster && cut.rank == 1 && k == 0 && node;
+  auto phase_barrier = [&]() {
+    if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
   };
 
   // this CTA's share of the instance-major global arrays
@@ -569,6 +562,19 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
     for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
   if (ival) load_rows(a.sp, b, m, kg, g, aop);
   __syncthreads();
+  auto publish_duals = [&](const double (&phe)[kR], double the) {  // extrapolated duals + partial sums
+#pragma unroll
+    for (int r = 0; r < kR; ++r) phx_k[r] = phe[r];
+    if (g == 4) thx_k[0] = the;
+    if (push_prev) {
+      double* rphx = in_cta(sm + L.phi - kNX + kR * g, 1);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) rphx[r] = phe[r];
+      if (g == 4) *in_cta(sm + L.theta - 1, 1) = the;
+    }
+    store_partials(aop, phe, slot);
+    if (push_prev) push_bp_partials(slot, in_cta(part - kG * kPS + g * kPS, 1));
+  };
 
   // boundary rows of this thread (pipg.hpp:408-413): bit r set when row 3g+r is assigned
   int fix_bits = 0;
@@ -601,20 +607,16 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       vpe[r] = snap0[S.vp + e];
       vne[r] = snap0[S.vn + e];
       phe[r] = snap0[S.ph + e];
-      phx_k[r] = phe[r];
     }
-    if (g == 4) {
-      the = snap0[S.th + k];
-      thx_k[0] = the;
-    }
+    if (g == 4) the = snap0[S.th + k];
   }
-  store_partials(aop, phe, slot);
+  publish_duals(phe, the);
 
   const double sigma = a.sigma[b];
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
   const double one_m_rho = 1.0 - a.rho;
-  after_dual();
+  phase_barrier();
 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into the
   // snapshot `snap` (threads without a node / interval write scratch entries).
@@ -652,7 +654,9 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       const double grad = base[r] + sx[r];
       double xn = x0 + -alpha * grad;
       xn = (fix_bits & (1 << r)) ? fv[r] : xn;
-      xr_k[i] = fma(2.0, xn, -x0);
+      const double xrf = fma(2.0, xn, -x0);
+      xr_k[i] = xrf;
+      if (push_next) *in_cta(sm + L.xs + cut.half * kXS + i, 0) = xrf;
       if (kStore) snap[S.x + kc * kNX + i] = xn;
       xe[r] = one_m_rho * x0 + a.rho * xn;  // extrapolation, pipg.hpp:461-467
     }
@@ -665,13 +669,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
       const double cl = (hi[q] < un) ? hi[q] : un;
       un = (lo[q] < cl) ? cl : lo[q];
-      ur_k[ju] = fma(2.0, un, -u0);
+      const double urf = fma(2.0, un, -u0);
+      ur_k[ju] = urf;
+      if (push_next && (q == 0 || g < 2)) *in_cta(sm + L.us + cut.half * kUS + ju, 0) = urf;
       if (kStore) {
         if (q == 0 || g < 2) snap[S.u + kc * kNU + ju] = un;
       }
       ue[q] = one_m_rho * u0 + a.rho * un;
     }
-    after_primal();
+    phase_barrier();
 
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
     //      extrapolation of the dual groups (:468-472) and the partial sums of H^T phi_ex for
@@ -701,16 +707,14 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         phe[r] = ival ? pe : 0.0;
         vpe[r] = one_m_rho * vp0 + a.rho * vp;
         vne[r] = one_m_rho * vn0 + a.rho * vn;
-        phx_k[r] = phe[r];
       }
       if (g == 4) {
         const double drift = xr_k[kXS + 14] - v[14] - eps_k[0];
         const double tn = fmax(0.0, the + beta * drift);
         if (kStore) snap[S.th + kc] = tn;
         the = ival ? one_m_rho * the + a.rho * tn : 0.0;
-        thx_k[0] = the;
       }
-      store_partials(aop, phe, slot);
+      publish_duals(phe, the);
     }
   };
 
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
       iteration(std::false_type{}, nullptr);
     }
     iters = j;
-    after_dual();
+    phase_barrier();
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
       const double* cur = snap0 + cur_set * S.total;
       const double* prev = snap0 + (cur_set ^ 1) * S.total;
@@ -778,14 +782,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
         for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, w < nwarps ? red[w * 8 + q] : 0.0);
         v[q] = mx;
       }
-      if constexpr (kCluster) {  // combine with the partner's maxima (seven DSMEM loads per thread)
+      if constexpr (kCluster) {  // combine with the partner's maxima
         if (tid == 0) {
+          double* rv = in_cta(red + kFastWarps * 8, cut.rank ^ 1);
 #pragma unroll
-          for (int q = 0; q < 7; ++q) red[kFastWarps * 8 + q] = v[q];
+          for (int q = 0; q < 7; ++q) rv[q] = v[q];
         }
         cg::this_cluster().sync();
 #pragma unroll
-        for (int q = 0; q < 7; ++q) v[q] = fmax(v[q], remote[L.red + kFastWarps * 8 + q]);
+        for (int q = 0; q < 7; ++q) v[q] = fmax(v[q], red[kFastWarps * 8 + q]);
         cg::this_cluster().sync();  // red and the snapshots are rewritten later
       } else {
         __syncthreads();  // red and the snapshots are rewritten later

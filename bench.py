@@ -190,6 +190,7 @@ def run_own_arm(args):
 
     stream = torch.cuda.Stream(device=dev)
     solver = Solver(desc, device=local_rank, stream=stream)
+    solver.set_solver_path(args.solver_path)
 
     # device-resident inputs / outputs for the kernel-only number
     d_init = torch.from_numpy(batch["init_state"]).to(dev)
@@ -393,6 +394,8 @@ def main():
     ap.add_argument("--batch", type=int, default=4096, help="instances per GPU")
     ap.add_argument("--nodes", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--solver-path", choices=("auto", "generic", "split"), default="auto",
+                    help="kernel family for power iteration / PIPG (ptopt_cuda_set_solver_path)")
     ap.add_argument("--cpu-instances", type=int, default=0,
                     help="instances in the CPU sample (default: one per host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

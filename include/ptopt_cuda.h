@@ -205,12 +205,19 @@ int64_t ptopt_cuda_launch_count(const ptopt_cuda_handle* h);
 int ptopt_cuda_create(const ptopt_problem_desc* desc, const double* tau, int device, void* stream,
                       ptopt_cuda_handle** out);
 int ptopt_cuda_destroy(ptopt_cuda_handle* h);
-/* Kernel family used for power iteration and PIPG.  AUTO picks the register-resident kernels
- * for the rocket-shaped subproblem (n_x = 15, n_u = 7, A_plus = -I, e_y = last state,
- * nodes <= 51) and the shape-generic kernels otherwise; GENERIC forces the latter (used by
- * the parity tests to cover both families on the same inputs).  No reference counterpart. */
+/* Kernel family used for power iteration and PIPG.  No reference counterpart.
+ *   AUTO       register-resident kernels for the rocket-shaped subproblem (n_x = 15, n_u = 7,
+ *              A_plus = -I, e_y = last state): one CTA per instance up to 51 nodes, a 2-CTA
+ *              cluster up to 102; the shape-generic kernels for every other shape.
+ *   GENERIC    forces the shape-generic kernels (the parity tests run every family on the same
+ *              inputs).
+ *   FAST_SPLIT register-resident kernels with every instance of 4..50 nodes shared by a 2-CTA
+ *              cluster of 128-thread CTAs, two CTAs (halves of different instances) resident per
+ *              SM; other node counts run as under AUTO.  Experimental: on B200 it is slower
+ *              than AUTO (the cluster barriers cost more than the overlap gains). */
 #define PTOPT_SOLVER_AUTO 0
 #define PTOPT_SOLVER_GENERIC 1
+#define PTOPT_SOLVER_FAST_SPLIT 2
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path);
 /* Blocks until all work enqueued on the handle's stream has finished. */
 int ptopt_cuda_synchronize(ptopt_cuda_handle* h);

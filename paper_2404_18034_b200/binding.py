@@ -132,8 +132,9 @@ class Solver:
         self.close()
 
     def set_solver_path(self, path: str):
-        """'auto' (register-resident kernels where the shape allows) or 'generic'."""
-        _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int({"auto": 0, "generic": 1}[path])))
+        """'auto' (register-resident kernels where the shape allows; split variant for small
+        batches), 'generic' (shape-generic kernels) or 'split' (PTOPT_SOLVER_FAST_SPLIT)."""
+        _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int({"auto": 0, "generic": 1, "split": 2}[path])))
 
     def synchronize(self):
         _check(self.lib.ptopt_cuda_synchronize(self._h))

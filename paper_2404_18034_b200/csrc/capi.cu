@@ -91,6 +91,7 @@ struct ptopt_cuda_handle {
   std::vector<int> stage_of_span;  // stage id of the span that ENDS at event i+1
   bool stage_times_valid = false;
   int solver_path = PTOPT_SOLVER_AUTO;
+  int num_sms = 0;
 };
 
 namespace {
@@ -233,9 +234,17 @@ bool use_fast_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_p
   return h->solver_path != PTOPT_SOLVER_GENERIC && solver_fast_supports(s, has_a_plus);
 }
 
+/// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
+/// handle asks for it (and the node count allows it).  Measured on B200 it loses to one CTA per
+/// instance both in throughput (416 vs 579 solves/s at 4096 x N=50) and in single-solve latency
+/// (277 vs 227 ms): two release/acquire cluster barriers per iteration cost ~1000 cycles.
+bool use_split_solver(const ptopt_cuda_handle* h, int /*batch*/) {
+  return h->solver_path == PTOPT_SOLVER_FAST_SPLIT;
+}
+
 int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
   if (fast) {
-    PT_TRY(check_smem(h, pipg_fast_smem(s)));
+    PT_TRY(check_smem(h, pipg_fast_smem(s, false)));
     PT_CUDA(configure_solver_fast(s));
   } else {
     PT_TRY(check_smem(h, pipg_generic_smem(s, solver_generic_threads(s))));
@@ -247,7 +256,7 @@ int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
 int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  PT_CUDA(fast ? launch_power_fast(a, h->stream) : launch_power_generic(a, h->stream));
+  PT_CUDA(fast ? launch_power_fast(a, use_split_solver(h, a.batch), h->stream) : launch_power_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
 }
@@ -255,7 +264,7 @@ int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
 int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  PT_CUDA(fast ? launch_pipg_fast(a, h->stream) : launch_pipg_generic(a, h->stream));
+  PT_CUDA(fast ? launch_pipg_fast(a, use_split_solver(h, a.batch), h->stream) : launch_pipg_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
 }
@@ -405,9 +414,9 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 2;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    PT_CUDA(fast ? launch_power_fast(pa, h->stream) : launch_power_generic(pa, h->stream));
+    PT_CUDA(fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream) : launch_power_generic(pa, h->stream));
     PT_CUDA(mark(2));
-    PT_CUDA(fast ? launch_pipg_fast(ga, h->stream) : launch_pipg_generic(ga, h->stream));
+    PT_CUDA(fast ? launch_pipg_fast(ga, use_split_solver(h, batch), h->stream) : launch_pipg_generic(ga, h->stream));
     PT_CUDA(mark(3));
     launch_scp_update(sa, h->stream);
     PT_CUDA(mark(4));
@@ -557,6 +566,7 @@ int ptopt_cuda_create(const ptopt_problem_desc* desc, const double* tau, int dev
   h->device = device;
   h->desc = d;
   h->tau = grid;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (!make_model_const(d.vehicle, h->model)) {
     delete h;
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "inverse3: singular matrix");
@@ -604,7 +614,7 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
 
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path) {
   if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
-  if (path != PTOPT_SOLVER_AUTO && path != PTOPT_SOLVER_GENERIC)
+  if (path != PTOPT_SOLVER_AUTO && path != PTOPT_SOLVER_GENERIC && path != PTOPT_SOLVER_FAST_SPLIT)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "unknown solver path");
   if (path != h->solver_path && h->scp_graph) {  // the captured graph names the other kernels
     DeviceGuard guard(h->device);

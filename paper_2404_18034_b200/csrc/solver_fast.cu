@@ -20,6 +20,8 @@
 // change rounding only (measured sensitivity of the whole loop: 1e-13).
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -36,10 +38,20 @@ constexpr int kW = kNX + 2 * kNU;  // 29 columns of [A- | B- | B+]
 constexpr int kXS = 18;      // node stride of x vectors in shared memory (16-byte aligned, conflict-free)
 constexpr int kUS = 10;      // node stride of u vectors
 constexpr int kPS = 35;      // stride of one thread's partial-sum slot (== 3 mod 16: conflict-free)
-constexpr int kFastThreads = 256;
-constexpr int kFastWarps = kFastThreads / 32;
-static_assert((kFastThreads - 1) / kG <= kFastMaxNodes, "every thread needs a (scratch) node inside the layout");
-static_assert(kG * kFastMaxNodes <= kFastThreads, "five threads per node");
+constexpr int kFastWarps = 8;  // slots of the reduction arrays (any variant has at most this many warps)
+
+// Two compile-time shapes of a CTA.  kCap = kFastMaxNodes (51 nodes, 256 threads, one CTA per SM)
+// holds a whole instance of up to 51 nodes, or half of a 2-CTA cluster for up to 102.  kCap =
+// kSplitMaxNodes (25 nodes, 128 threads, 112 KB of shared memory) is half of an instance of up to
+// 50 nodes: two such CTAs -- halves of two different instances -- share one SM, so that the
+// shared-memory phases of one overlap the FP64 phases of the other instead of running in lockstep.
+template <int kCap>
+struct FastCfg {
+  static constexpr int threads = (kG * kCap + 31) / 32 * 32;
+  static constexpr int ctas_per_sm = kCap <= kSplitMaxNodes ? 2 : 1;
+  static_assert((threads - 1) / kG <= kCap, "every thread needs a (scratch) node inside the layout");
+  static_assert(threads / 32 <= kFastWarps, "reduction slots");
+};
 
 // position of a column's partial sum inside a slot: x columns first, then the B- / B+ columns
 // interleaved so that the five owners of a node read with a 3-double spacing (no bank conflicts)
@@ -155,8 +167,9 @@ struct FastLayout {
 struct SnapLayout {
   int x, u, vp, vn, ph, th, total;
 };
+template <int kCap>
 __host__ __device__ constexpr SnapLayout snap_layout() {
-  constexpr int n = kFastMaxNodes + 3;
+  constexpr int n = kCap + 3;
   SnapLayout S{};
   int o = 0;
   S.x = o; o += n * kNX;
@@ -175,8 +188,10 @@ __host__ __device__ constexpr int even_up(int v) { return (v + 1) & ~1; }
 // two extra nodes (n: scratch node of the idle threads, n+1: its right neighbour); interval
 // arrays have one zero interval in front (index -1, read by node 0) and are sized for every
 // thread; partial-sum slots exist for every thread plus five zero slots in front.
+template <int kCap>
 __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
-  constexpr int n = kFastMaxNodes;  // fixed offsets: every address is base + immediate
+  constexpr int n = kCap;  // fixed offsets: every address is base + immediate
+  constexpr int kThreads = FastCfg<kCap>::threads;
   FastLayout L{};
   int o = 0;
   L.xs = o; o += (n + 4) * kXS;
@@ -188,9 +203,9 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
   if (pipg) {
     L.wv = o; o += even_up((n + 3) * kNX);
     L.eps = o; o += even_up(n + 4);
-    L.umin = o; o += 2 * kFastThreads;  // {lo, hi} of each thread's first control entry
-    L.umax = o; o += 2 * kFastThreads;  // {lo, hi} of its second one (+-inf where it has none)
-    L.snap = o; o += 2 * snap_layout().total;
+    L.umin = o; o += 2 * kThreads;  // {lo, hi} of each thread's first control entry
+    L.umax = o; o += 2 * kThreads;  // {lo, hi} of its second one (+-inf where it has none)
+    L.snap = o; o += 2 * snap_layout<kCap>().total;
     L.bnd = o; o += 6 * 16;  // ecost, init_val, final_val, init_on, final_on (as doubles)
   }
   L.total = o;
@@ -248,8 +263,9 @@ __device__ __forceinline__ void push_bp_partials(const double* slot, double* rem
 // ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
-template <bool kCluster>
-__global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a) {
+template <bool kCluster, int kCap>
+__global__ void __launch_bounds__(FastCfg<kCap>::threads, FastCfg<kCap>::ctas_per_sm)
+power_fast_kernel(PowerArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
@@ -263,7 +279,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
   // threads past the last node work on scratch nodes of their own; in a cluster node `nloc` of
   // rank 0 is not scratch (the partner pushes its first node there), so they start one further
   const int kc = (kCluster && k >= cut.nloc) ? k + 1 : k;
-  constexpr FastLayout L = fast_layout(false);
+  constexpr FastLayout L = fast_layout<kCap>(false);
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
   // in a cluster: both CTAs are running and have cleared their memory before any remote store
   if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
@@ -350,7 +366,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
     red[warp] = acc;
     if constexpr (kCluster) *in_cta(redp + warp, cut.rank ^ 1) = acc;
   }
-  phase_barrier();
+  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
   double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (tid == 0 && cut.rank == 0) {
@@ -473,8 +489,9 @@ __global__ void __launch_bounds__(kFastThreads, 1) power_fast_kernel(PowerArgs a
 // ---------------------------------------------------------------------------------------------
 // customized PIPG (pipg.hpp:350-497)
 // ---------------------------------------------------------------------------------------------
-template <bool kCluster>
-__global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) {
+template <bool kCluster, int kCap>
+__global__ void __launch_bounds__(FastCfg<kCap>::threads, FastCfg<kCap>::ctas_per_sm)
+pipg_fast_kernel(PipgArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
@@ -489,8 +506,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   // rank 0 is not scratch (the partner pushes its first node there), so they start one further
   const int kc = (kCluster && k >= cut.nloc) ? k + 1 : k;
   const int mloc = cut.nloc - (cut.node0 + cut.nloc == n ? 1 : 0);  // intervals owned by this CTA
-  constexpr FastLayout L = fast_layout(true);
-  constexpr SnapLayout S = snap_layout();
+  constexpr FastLayout L = fast_layout<kCap>(true);
+  constexpr SnapLayout S = snap_layout<kCap>();
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
   // in a cluster: both CTAs are running and have cleared their memory before any remote store
   if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
@@ -616,7 +633,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) pipg_fast_kernel(PipgArgs a) 
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
   const double one_m_rho = 1.0 - a.rho;
-  phase_barrier();
+  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into the
   // snapshot `snap` (threads without a node / interval write scratch entries).
@@ -846,38 +863,37 @@ bool solver_fast_supports(const SubShape& s, bool has_a_plus) {
   return true;
 }
 
-size_t power_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_layout(false).total; }
-size_t pipg_fast_smem(const SubShape&) { return sizeof(double) * (size_t)fast_layout(true).total; }
-
-cudaError_t configure_solver_fast(const SubShape& s) {
-  const int ps = (int)power_fast_smem(s), gs = (int)pipg_fast_smem(s);
-  cudaError_t e = cudaFuncSetAttribute(power_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(power_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ps);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(pipg_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gs);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(pipg_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gs);
-  return e;
-}
+bool solver_fast_can_split(const SubShape& s) { return s.n >= 4 && s.n <= 2 * kSplitMaxNodes; }
 
 namespace {
 
-/// One CTA per instance up to kFastMaxNodes nodes, a cluster of two above.
-bool needs_cluster(const SubShape& s) { return s.n > kFastMaxNodes; }
+constexpr size_t kPowerSmemFull = sizeof(double) * (size_t)fast_layout<kFastMaxNodes>(false).total;
+constexpr size_t kPipgSmemFull = sizeof(double) * (size_t)fast_layout<kFastMaxNodes>(true).total;
+constexpr size_t kPowerSmemSplit = sizeof(double) * (size_t)fast_layout<kSplitMaxNodes>(false).total;
+constexpr size_t kPipgSmemSplit = sizeof(double) * (size_t)fast_layout<kSplitMaxNodes>(true).total;
+// two co-resident CTAs: 228 KB per SM minus 1 KB reserved per CTA
+static_assert(kPipgSmemSplit <= 113 * 1024, "two split CTAs must fit one SM");
+
+bool use_split(const SubShape& s, bool split) { return split && solver_fast_can_split(s); }
+
+/// One CTA per instance up to kFastMaxNodes nodes, a cluster of two above or when split.
+bool needs_cluster(const SubShape& s, bool split) { return s.n > kFastMaxNodes || use_split(s, split); }
 
 /// Just enough warps for five threads per (local) node; the kernels size their loops by blockDim.
-int fast_threads(const SubShape& s) {
-  const int nodes = needs_cluster(s) ? (s.n + 1) / 2 : s.n;
+int fast_threads(const SubShape& s, bool split) {
+  const int nodes = needs_cluster(s, split) ? (s.n + 1) / 2 : s.n;
   return ((kG * nodes + 31) / 32) * 32;
 }
 
 template <class Args>
-cudaError_t launch_fast(void (*single)(Args), void (*paired)(Args), const Args& a, size_t smem,
-                        cudaStream_t stream) {
+cudaError_t launch_fast(void (*single)(Args), void (*paired)(Args), void (*halves)(Args), const Args& a,
+                        bool split, size_t smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3((unsigned)fast_threads(a.shape));
+  cfg.blockDim = dim3((unsigned)fast_threads(a.shape, split));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr{};
-  if (needs_cluster(a.shape)) {
+  if (needs_cluster(a.shape, split)) {
     cfg.gridDim = dim3(2u * (unsigned)a.batch);
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 2;
@@ -885,7 +901,7 @@ cudaError_t launch_fast(void (*single)(Args), void (*paired)(Args), const Args& 
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, paired, a);
+    return cudaLaunchKernelEx(&cfg, use_split(a.shape, split) ? halves : paired, a);
   }
   cfg.gridDim = dim3((unsigned)a.batch);
   return cudaLaunchKernelEx(&cfg, single, a);
@@ -893,14 +909,44 @@ cudaError_t launch_fast(void (*single)(Args), void (*paired)(Args), const Args& 
 
 }  // namespace
 
-cudaError_t launch_power_fast(const PowerArgs& a, cudaStream_t stream) {
-  return launch_fast<PowerArgs>(power_fast_kernel<false>, power_fast_kernel<true>, a, power_fast_smem(a.shape),
-                                stream);
+size_t power_fast_smem(const SubShape& s, bool split) { return use_split(s, split) ? kPowerSmemSplit : kPowerSmemFull; }
+size_t pipg_fast_smem(const SubShape& s, bool split) { return use_split(s, split) ? kPipgSmemSplit : kPipgSmemFull; }
+
+cudaError_t configure_solver_fast(const SubShape&) {
+  const auto opt_in = [](auto kernel, size_t bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    // two split CTAs per SM need the largest shared-memory carveout
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess && getenv("PTOPT_DEBUG_OCCUPANCY")) {
+      int blocks = -1;
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kernel);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, 128, bytes);
+      fprintf(stderr, "[ptopt] kernel regs=%d smem=%zu maxThreads=%d -> %d CTAs of 128 threads per SM\n",
+              fa.numRegs, bytes, fa.maxThreadsPerBlock, blocks);
+    }
+    return e;
+  };
+  cudaError_t e = opt_in(power_fast_kernel<false, kFastMaxNodes>, kPowerSmemFull);
+  if (e == cudaSuccess) e = opt_in(power_fast_kernel<true, kFastMaxNodes>, kPowerSmemFull);
+  if (e == cudaSuccess) e = opt_in(power_fast_kernel<true, kSplitMaxNodes>, kPowerSmemSplit);
+  if (e == cudaSuccess) e = opt_in(pipg_fast_kernel<false, kFastMaxNodes>, kPipgSmemFull);
+  if (e == cudaSuccess) e = opt_in(pipg_fast_kernel<true, kFastMaxNodes>, kPipgSmemFull);
+  if (e == cudaSuccess) e = opt_in(pipg_fast_kernel<true, kSplitMaxNodes>, kPipgSmemSplit);
+  return e;
 }
 
-cudaError_t launch_pipg_fast(const PipgArgs& a, cudaStream_t stream) {
-  return launch_fast<PipgArgs>(pipg_fast_kernel<false>, pipg_fast_kernel<true>, a, pipg_fast_smem(a.shape),
-                               stream);
+cudaError_t launch_power_fast(const PowerArgs& a, bool split, cudaStream_t stream) {
+  return launch_fast<PowerArgs>(power_fast_kernel<false, kFastMaxNodes>, power_fast_kernel<true, kFastMaxNodes>,
+                                power_fast_kernel<true, kSplitMaxNodes>, a, split,
+                                power_fast_smem(a.shape, split), stream);
+}
+
+cudaError_t launch_pipg_fast(const PipgArgs& a, bool split, cudaStream_t stream) {
+  return launch_fast<PipgArgs>(pipg_fast_kernel<false, kFastMaxNodes>, pipg_fast_kernel<true, kFastMaxNodes>,
+                               pipg_fast_kernel<true, kSplitMaxNodes>, a, split,
+                               pipg_fast_smem(a.shape, split), stream);
 }
 
 }  // namespace ptopt_b200

@@ -19,10 +19,11 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(1.0, np.abs(b).max())
 
 
-@pytest.fixture(scope="module", params=["auto", "generic"])
+@pytest.fixture(scope="module", params=["auto", "generic", "split"])
 def solver15(request):
     """The default-scenario handle, once per kernel family: 'auto' runs the register-resident
-    power/PIPG kernels on rocket-shaped subproblems, 'generic' forces the shape-generic ones."""
+    power/PIPG kernels on rocket-shaped subproblems, 'generic' forces the shape-generic ones,
+    'split' shares every rocket-shaped instance between the two CTAs of a cluster."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(15)
@@ -693,6 +694,27 @@ def test_scp_solve_node_count_edges(ptor, nodes):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
+@pytest.mark.parametrize("nodes", [4, 5, 26, 49, 50, 51])
+def test_scp_solve_split_path_node_counts(ptor, nodes):
+    """The split variant (every instance shared by a 2-CTA cluster of 128-thread CTAs, two CTAs per
+    SM): the smallest and largest node counts it accepts (4, 50), odd counts (uneven halves), a
+    count whose halves leave idle threads (26), and one above its range (51, runs single-CTA)."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(nodes)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 120, 150
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [0, 11, 5])
+    with Solver(d) as s:
+        s.set_solver_path("split")
+        out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+    for b in range(3):
+        rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                                 int(batch["rng_seed"][b]), with_trips=True)
+        assert rc == 0
+        check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+
+
 def test_solver_divergence_inside_the_scp_loop(ptor):
     """A spectral estimate cut off after one power-iteration trip is far too small, the step
     sizes are too large and PIPG blows up: the reference throws SolverDiverged at the stopping
@@ -712,7 +734,7 @@ def test_solver_divergence_inside_the_scp_loop(ptor):
         assert rc == abi.ST_SOLVER_DIVERGED, rc
         refs.append(ref["fail_index"])
     assert refs[0] != refs[1]
-    for path in ("auto", "generic"):
+    for path in ("auto", "generic", "split"):
         with Solver(d) as s:
             s.set_solver_path(path)
             out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])

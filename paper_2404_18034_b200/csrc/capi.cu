@@ -56,12 +56,12 @@ enum BufId {
   B_X, B_U, B_A, B_BM, B_BP, B_W, B_XEND, B_STATUS, B_FAILIDX, B_FAILKEY, B_INIT,
   B_AM, B_AP, B_BMH, B_BPH, B_WH, B_EPS, B_UMIN, B_UMAX, B_INITVAL, B_FINALVAL,
   B_SEEDX, B_SEEDU, B_SEEDP, B_SEEDN, B_SIGMA, B_TRIPS, B_ITERS, B_CONV,
-  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR, B_TAU,
+  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR, B_TAU, B_STAGES,
   // SCP loop state (separate so a stand-alone call never disturbs a captured graph)
   S_ZX, S_ZU, S_INIT, S_SEED, S_A, S_BM, S_BP, S_W, S_XEND, S_AM, S_BMH, S_BPH, S_WH, S_EPS,
   S_UMIN, S_UMAX, S_INITVAL, S_FINALVAL, S_SEEDX, S_SEEDU, S_WSX, S_WSU, S_WSP, S_WSN, S_WSD,
   S_WSR, S_SIGMA, S_PITERS, S_FAILKEY, S_ACTIVE, S_CONV, S_SOLVES, S_LASTSTEP, S_FDEF, S_HIST,
-  S_TRIPS, S_STATUS, S_FAILIDX,
+  S_TRIPS, S_STATUS, S_FAILIDX, S_STAGES,
   // Monte Carlo harness
   R_QTAB, R_INIT, R_XG, R_UG, R_SEED, R_XOUT, R_UOUT, R_ITERS, R_CONV, R_FDEF, R_STATUS, R_FAILIDX,
   R_GMAX, R_DY, R_AKEY, R_PG, R_RECORDS,
@@ -269,14 +269,34 @@ int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
   return PTOPT_OK;
 }
 
-LinearizeArgs linearize_args(ptopt_cuda_handle* h, int batch, const double* x, const double* u,
-                             double* A, double* Bm, double* Bp, double* w, double* x_end,
-                             int* fail_key, const unsigned char* active) {
+/// Upper bound on the stage-record storage of one state/column pass pair; larger batches are
+/// processed in chunks (PTOPT_STAGE_BYTES_MAX overrides the default of 16 GiB).
+size_t stage_bytes_cap() {
+  static const size_t cap = [] {
+    const char* env = getenv("PTOPT_STAGE_BYTES_MAX");
+    const unsigned long long v = env ? strtoull(env, nullptr, 10) : 0ull;
+    return v ? (size_t)v : ((size_t)16 << 30);
+  }();
+  return cap;
+}
+
+/// Intervals per pass pair and bytes of stage records for a linearize over `intervals` intervals.
+long long stage_plan(long long intervals, int steps, size_t* bytes) {
+  const long long chunk = linearize_chunk_intervals(intervals, steps, stage_bytes_cap());
+  *bytes = linearize_stage_doubles(chunk, steps) * sizeof(double);
+  return chunk;
+}
+
+/// The stage-record buffer `stage_buf` must already be large enough when this runs under stream
+/// capture (ensure_scp_state sizes S_STAGES); otherwise it is grown here.
+int linearize_args(ptopt_cuda_handle* h, int batch, int nodes, int steps, const double* x, const double* u,
+                   double* A, double* Bm, double* Bp, double* w, double* x_end, int* fail_key,
+                   const unsigned char* active, BufId stage_buf, LinearizeArgs* out) {
   LinearizeArgs a;
   a.model = h->model;
   a.batch = batch;
-  a.nodes = h->desc.nodes;
-  a.steps = h->desc.integrator_steps;
+  a.nodes = nodes;
+  a.steps = steps;
   a.tau = h->d_tau;
   a.tau_stride = 0;
   a.x = x;
@@ -288,13 +308,20 @@ LinearizeArgs linearize_args(ptopt_cuda_handle* h, int batch, const double* x, c
   a.x_end = x_end;
   a.fail_key = fail_key;
   a.active = active;
-  return a;
+  size_t bytes = 0;
+  a.stage_capacity = stage_plan((long long)batch * (nodes - 1), steps, &bytes);
+  PT_CUDA(h->buf[stage_buf].ensure(bytes));
+  a.stages = h->buf[stage_buf].as<double>();
+  *out = a;
+  return PTOPT_OK;
 }
 
 int ensure_scp_state(ptopt_cuda_handle* h, int batch, ScpState& s) {
   const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
   const size_t nf = h->desc.n_final_fix > 0 ? (size_t)h->desc.n_final_fix : 1;
   const size_t mi = (size_t)h->desc.max_iters;
+  size_t stage_bytes = 0;
+  stage_plan((long long)B * (long long)m, h->desc.integrator_steps, &stage_bytes);
   struct Req { BufId id; size_t bytes; };
   const Req reqs[] = {
       {S_ZX, B * n * kNX * 8}, {S_ZU, B * n * kNU * 8}, {S_INIT, B * kNXI * 8}, {S_SEED, B * 8},
@@ -307,7 +334,8 @@ int ensure_scp_state(ptopt_cuda_handle* h, int batch, ScpState& s) {
       {S_WSP, B * m * kNX * 8}, {S_WSN, B * m * kNX * 8}, {S_WSD, B * m * kNX * 8},
       {S_WSR, B * m * 8}, {S_SIGMA, B * 8}, {S_PITERS, B * 4}, {S_FAILKEY, B * 4},
       {S_ACTIVE, B}, {S_CONV, B}, {S_SOLVES, B * 4}, {S_LASTSTEP, B * 8}, {S_FDEF, B * 8},
-      {S_HIST, B * mi * 5 * 8}, {S_TRIPS, B * mi * 4}, {S_STATUS, B * 4}, {S_FAILIDX, B * 4}};
+      {S_HIST, B * mi * 5 * 8}, {S_TRIPS, B * mi * 4}, {S_STATUS, B * 4}, {S_FAILIDX, B * 4},
+      {S_STAGES, stage_bytes}};
   bool grew = false;
   for (const Req& r : reqs) {
     if (r.bytes > h->buf[r.id].bytes || !h->buf[r.id].p) grew = true;
@@ -404,15 +432,16 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   ga.fail_index = st.fail_index;
   ga.active = st.active;
 
-  const LinearizeArgs la = linearize_args(h, batch, st.zx, st.zu, st.A, st.Bm, st.Bp, st.w,
-                                          st.x_end, st.fail_key, st.active);
+  LinearizeArgs la;
+  PT_TRY(linearize_args(h, batch, h->desc.nodes, h->desc.integrator_steps, st.zx, st.zu, st.A, st.Bm, st.Bp,
+                        st.w, st.x_end, st.fail_key, st.active, S_STAGES, &la));
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
   for (int it = 0; it <= h->desc.max_iters; ++it) {
-    launch_linearize(la, h->stream);
+    kernels += launch_linearize(la, h->stream);
     PT_CUDA(mark(0));
     launch_scp_prepare(sa, h->stream);
     PT_CUDA(mark(1));
-    kernels += 2;
+    kernels += 1;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
     PT_CUDA(fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream) : launch_power_generic(pa, h->stream));
     PT_CUDA(mark(2));
@@ -647,10 +676,11 @@ int ptopt_cuda_linearize_batch_dev(ptopt_cuda_handle* h, int batch, const double
   if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
   int* fail_key = nullptr;
   PT_TRY(device_out(h, B_FAILKEY, (size_t)batch, &fail_key));
+  LinearizeArgs la;
+  PT_TRY(linearize_args(h, batch, h->desc.nodes, h->desc.integrator_steps, x, u, A, Bm, Bp, w, x_end,
+                        fail_key, nullptr, B_STAGES, &la));
   launch_init_fail_key(fail_key, batch, h->stream);
-  launch_linearize(linearize_args(h, batch, x, u, A, Bm, Bp, w, x_end, fail_key, nullptr),
-                   h->stream);
-  h->launches += 2;
+  h->launches += 1 + launch_linearize(la, h->stream);
   if (status || fail_index) {
     launch_decode_fail_key(fail_key, batch, status, fail_index, h->stream);
     h->launches += 1;
@@ -731,15 +761,13 @@ int ptopt_cuda_propagate_interval_batch(ptopt_cuda_handle* h, int batch, const d
   PT_TRY(device_out(h, B_STATUS, B, &dst));
   PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
   PT_TRY(device_out(h, B_FAILKEY, B, &dkey));
-  LinearizeArgs a = linearize_args(h, batch, dx, du, dA, dBm, dBp, dw, dxe, dkey, nullptr);
-  a.nodes = 2;
-  a.steps = steps;
+  LinearizeArgs a;
+  PT_TRY(linearize_args(h, batch, 2, steps, dx, du, dA, dBm, dBp, dw, dxe, dkey, nullptr, B_STAGES, &a));
   a.tau = dt;
   a.tau_stride = 2;
   launch_init_fail_key(dkey, batch, h->stream);
-  launch_linearize(a, h->stream);
+  h->launches += 2 + launch_linearize(a, h->stream);
   launch_decode_fail_key(dkey, batch, dst, dfi, h->stream);
-  h->launches += 3;
   PT_CUDA(cudaGetLastError());
   PT_TRY(download(h, A, dA, B * kNX * kNX));
   PT_TRY(download(h, Bm, dBm, B * kNX * kNU));

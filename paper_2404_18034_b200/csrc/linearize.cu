@@ -1,6 +1,15 @@
-// linearize.cu — exact discretization kernel: batched linearize_all
-// (/root/reference/proj/include/ptopt/discretizer.hpp:191-232) with one warp per
-// (instance, interval).  See rocket_model.cuh for the per-lane algorithm.
+// linearize.cu — exact discretization: batched linearize_all
+// (/root/reference/proj/include/ptopt/discretizer.hpp:191-232) in two passes over every
+// (instance, interval):
+//   * state pass   — one THREAD per interval integrates the 15 augmented states through the
+//                    4 * steps RK4 stages (the only place the model and its Jacobian are
+//                    evaluated) and leaves one 84-double record per stage in HBM;
+//   * column pass  — one WARP per interval, lane j < 29 owns column j of
+//                    [Phi_x | Phi_u- | Phi_u+]; every stage it fetches the record (coalesced,
+//                    prefetched one stage ahead, staged in shared memory) and applies A(tau) and
+//                    the B forcing to its column in registers; then stages the 15 x 29 block in
+//                    shared memory for w = x_end - A x - B- u - B+ u+ and the coalesced write.
+// See rocket_model.cuh for the per-thread / per-lane algorithms.
 #include "kernels.cuh"
 #include "rocket_model.cuh"
 
@@ -10,69 +19,138 @@ namespace {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kStageStride = kCols + 1;  // 30: row stride of the staged [15][29] block
+constexpr int kRecLamLeft = 81;          // spare record slots: the first-order-hold factors
+constexpr int kRecLamRight = 82;
+static_assert(kRecLamRight < kRecSize, "record padding");
+
+// Records of 32 consecutive intervals are interleaved (field-major inside a tile) so that the
+// state pass -- one thread per interval -- writes them coalesced.  The four warps of a
+// column-pass CTA read four neighbouring intervals, i.e. the same 32-byte sectors.
+__host__ __device__ inline size_t record_index(long long local_interval, int nst, int stage_no) {
+  const long long tile = local_interval >> 5;
+  const int r = (int)(local_interval & 31);
+  return (((size_t)tile * nst + stage_no) * kRecSize) * 32 + r;
+}
+
+__global__ void __launch_bounds__(128) state_pass_kernel(LinearizeArgs a, long long first, long long count) {
+  const long long local = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= count) return;
+  const long long widx = first + local;
+  const int M = a.nodes - 1;
+  const int b = (int)(widx / M);
+  const int k = (int)(widx - (long long)b * M);
+  if (a.active && !a.active[b]) return;  // instance already finished (SCP loop)
+  const double* xg = a.x + ((size_t)b * a.nodes + k) * kNX;
+  const double* ug = a.u + ((size_t)b * a.nodes + k) * kNU;
+  double xk[kNX], uk[kNU], uk1[kNU], x_end[kNX];
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) xk[i] = xg[i];
+#pragma unroll
+  for (int i = 0; i < kNU; ++i) {
+    uk[i] = ug[i];
+    uk1[i] = ug[kNU + i];
+  }
+  const double* tau = a.tau + (size_t)b * a.tau_stride;
+  const double tau_k = tau[k], tau_k1 = tau[k + 1];
+  const int nst = 4 * a.steps;
+  double* out = a.stages;
+  const ModelConst& P = a.model;
+  const int rc = propagate_state_pass(
+      P, xk, uk, uk1, tau_k, tau_k1, a.steps, x_end, [&](int stage_no, const Stage& st, const double* u) {
+        double rec[kRecSize];
+        pack_stage_record(P, st, u, rec);
+        const StageTime t = stage_time(tau_k, tau_k1, a.steps, stage_no >> 2, stage_no & 3);
+        rec[kRecLamLeft] = t.lam_left;
+        rec[kRecLamRight] = t.lam_right;
+        double* o = out + record_index(local, nst, stage_no);
+#pragma unroll
+        for (int f = 0; f < kRecSize; ++f) o[(size_t)f * 32] = rec[f];
+      });
+  if (rc != kStOk) {
+    // first failing interval wins, as the serial reference loop would report it
+    atomicMin(&a.fail_key[b], (k << 4) | rc);
+    return;
+  }
+  double* xe = a.x_end + ((size_t)b * M + k) * kNX;
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) xe[i] = x_end[i];
+}
 
 struct __align__(16) WarpSmem {
-  StateScratch sc;
+  double rec[2][kRecSize];           // stage records, double-buffered
   double block[kNX * kStageStride];  // staged [A | B- | B+], row-major
   double xk[kNX], uk[kNU], uk1[kNU], xe[kNX];
 };
 
-struct WarpSync {
-  __device__ __forceinline__ void operator()() const { __syncwarp(); }
-};
-
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
-linearize_kernel(LinearizeArgs a) {
+column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   __shared__ WarpSmem smem[kWarpsPerCta];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const long long widx = (long long)blockIdx.x * kWarpsPerCta + wib;
+  const long long local = (long long)blockIdx.x * kWarpsPerCta + wib;
+  if (local >= count) return;
+  const long long widx = first + local;
   const int M = a.nodes - 1;
-  if (widx >= (long long)a.batch * M) return;
   const int b = (int)(widx / M);
   const int k = (int)(widx - (long long)b * M);
   if (a.active && !a.active[b]) return;  // instance already finished (SCP loop)
+  // an instance with a failed interval has no blocks (its records stop at the failure)
+  if (a.fail_key[b] != kFailKeyNone) return;
 
   WarpSmem& ws = smem[wib];
+  const size_t iv = (size_t)b * M + k;
   const double* xg = a.x + ((size_t)b * a.nodes + k) * kNX;
   const double* ug = a.u + ((size_t)b * a.nodes + k) * kNU;
-  if (lane < kNX) ws.xk[lane] = xg[lane];
+  if (lane < kNX) {
+    ws.xk[lane] = xg[lane];
+    ws.xe[lane] = a.x_end[iv * kNX + lane];
+  }
   if (lane < kNU) {
     ws.uk[lane] = ug[lane];
     ws.uk1[lane] = ug[kNU + lane];
   }
-  __syncwarp();
-  double xk[kNX], uk[kNU], uk1[kNU];
-#pragma unroll
-  for (int i = 0; i < kNX; ++i) xk[i] = ws.xk[i];
-#pragma unroll
-  for (int i = 0; i < kNU; ++i) {
-    uk[i] = ws.uk[i];
-    uk1[i] = ws.uk1[i];
-  }
 
-  double col[kNX], x_end[kNX];
   const double* tau = a.tau + (size_t)b * a.tau_stride;
-  const int rc = propagate_lane(a.model, lane, lane == 0, ws.sc, xk, uk, uk1, tau[k], tau[k + 1],
-                                a.steps, col, x_end, WarpSync());
-  if (rc != kStOk) {
-    // first failing interval wins, as the serial reference loop would report it
-    if (lane == 0) atomicMin(&a.fail_key[b], (k << 4) | rc);
-    return;
+  const double h = (tau[k + 1] - tau[k]) / a.steps;
+  const double h6 = h / 6.0, h3 = h / 3.0, hh = 0.5 * h;  // as stage_time forms them
+  const int nst = 4 * a.steps;
+  const double* recs = a.stages + record_index(local, nst, 0);
+  const size_t rec_stride = (size_t)kRecSize * 32;  // between consecutive stages of an interval
+  const bool third = lane + 64 < kRecSize;
+  double r0 = recs[(size_t)lane * 32], r1 = recs[(size_t)(lane + 32) * 32];
+  double r2 = third ? recs[(size_t)(lane + 64) * 32] : 0.0;
+
+  ColumnLane L;
+  column_init(L, lane);
+  const bool is_col = lane < kCols;
+  for (int sn = 0; sn < nst; ++sn) {
+    double* rec = ws.rec[sn & 1];
+    rec[lane] = r0;
+    rec[lane + 32] = r1;
+    if (third) rec[lane + 64] = r2;
+    __syncwarp();
+    if (sn + 1 < nst) {  // next record: in flight while this stage is computed
+      const double* nx = recs + (size_t)(sn + 1) * rec_stride;
+      r0 = nx[(size_t)lane * 32];
+      r1 = nx[(size_t)(lane + 32) * 32];
+      if (third) r2 = nx[(size_t)(lane + 64) * 32];
+    }
+    const int stage = sn & 3;
+    StageTime t;
+    t.wk = (stage == 0 || stage == 3) ? h6 : h3;
+    t.wn = stage == 2 ? h : hh;
+    t.lam_left = rec[kRecLamLeft];
+    t.lam_right = rec[kRecLamRight];
+    if (is_col) column_stage(a.model, L, rec, t, stage);
   }
 
   // stage the 15x29 block, then w = x_end - A x_k - B- u_k - B+ u_k1 row by row in the
   // reference's order (discretizer.hpp:144-147)
-  if (lane < kCols) {
+  if (is_col) {
 #pragma unroll
-    for (int i = 0; i < kNX; ++i) ws.block[i * kStageStride + lane] = col[i];
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) ws.xe[i] = x_end[i];
+    for (int i = 0; i < kNX; ++i) ws.block[i * kStageStride + lane] = L.s_c[i];
   }
   __syncwarp();
-  const size_t iv = (size_t)b * M + k;
   if (lane < kNX) {
     const double* row = ws.block + lane * kStageStride;
     double acc = 0.0;
@@ -88,7 +166,6 @@ linearize_kernel(LinearizeArgs a) {
     for (int j = 0; j < kNU; ++j) acc += row[kNX + kNU + j] * ws.uk1[j];
     wv += -1.0 * acc;
     a.w[iv * kNX + lane] = wv;
-    a.x_end[iv * kNX + lane] = ws.xe[lane];
   }
   double* Ag = a.A + iv * kNX * kNX;
   for (int e = lane; e < kNX * kNX; e += 32) Ag[e] = ws.block[(e / kNX) * kStageStride + e % kNX];
@@ -132,10 +209,30 @@ void launch_decode_fail_key(const int* fail_key, int batch, int* status, int* fa
                                                                   fail_index);
 }
 
-void launch_linearize(const LinearizeArgs& a, cudaStream_t stream) {
-  const long long warps = (long long)a.batch * (a.nodes - 1);
-  const int ctas = (int)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
-  linearize_kernel<<<ctas, kWarpsPerCta * 32, 0, stream>>>(a);
+size_t linearize_stage_doubles(long long intervals, int steps) {
+  const long long tiles = (intervals + 31) / 32;
+  return (size_t)tiles * 32 * (size_t)(4 * steps) * kRecSize;
+}
+
+long long linearize_chunk_intervals(long long intervals, int steps, size_t max_bytes) {
+  const size_t per_tile = 32 * (size_t)(4 * steps) * kRecSize * sizeof(double);
+  long long tiles = (long long)(max_bytes / per_tile);
+  if (tiles < 1) tiles = 1;
+  const long long cap = tiles * 32;
+  return intervals < cap ? (intervals + 31) / 32 * 32 : cap;
+}
+
+int launch_linearize(const LinearizeArgs& a, cudaStream_t stream) {
+  const long long total = (long long)a.batch * (a.nodes - 1);
+  int launches = 0;
+  for (long long first = 0; first < total; first += a.stage_capacity) {
+    const long long count = total - first < a.stage_capacity ? total - first : a.stage_capacity;
+    state_pass_kernel<<<(unsigned)((count + 127) / 128), 128, 0, stream>>>(a, first, count);
+    column_pass_kernel<<<(unsigned)((count + kWarpsPerCta - 1) / kWarpsPerCta), kWarpsPerCta * 32, 0, stream>>>(
+        a, first, count);
+    launches += 2;
+  }
+  return launches;
 }
 
 }  // namespace ptopt_b200

@@ -288,150 +288,235 @@ PT_HD void b_column(const ModelConst& P, const Stage& st, const double* u, int j
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Stage records.  The state part of the RK4 bundle does not depend on the sensitivity columns, so
+// the model is evaluated once per (interval, stage) by the state pass, which leaves everything
+// the 29 column lanes need in a compact record; the column pass applies A(tau) and the B forcing
+// from it.  (Evaluating the model in every column lane, as a one-pass kernel does, spends 70 % of
+// the FP64 instructions on 32 identical copies of eval_stage.)
+// ---------------------------------------------------------------------------------------------
+constexpr int kRecS = 0;        // dilation factor
+constexpr int kRecSvm = 1;      // [3]
+constexpr int kRecSvq = 4;      // [12]
+constexpr int kRecHw = 16;      // [3]
+constexpr int kRecGq = 19;      // [4]
+constexpr int kRecSww = 23;     // [9]
+constexpr int kRecAy = 32;      // [15] row y of A (zeros unless active)
+constexpr int kRecActive = 47;  // 1.0 when a path inequality is violated
+constexpr int kRecBT = 48;      // [3][5] thrust columns of B: rows 0, 4, 5, 6, 14
+constexpr int kRecBG = 63;      // [3] torque columns of B: row 14
+constexpr int kRecBS = 66;      // [15] dilation column of B
+constexpr int kRecSize = 84;    // padded; a warp moves a record with three coalesced accesses
+
+/// Packs what the column lanes need from an evaluated stage.
+PT_HD void pack_stage_record(const ModelConst& P, const Stage& st, const double* u, double* rec) {
+  rec[kRecS] = st.s;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) rec[kRecSvm + i] = st.svm[i];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) rec[kRecSvq + i] = st.svq[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) rec[kRecHw + i] = st.hw[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) rec[kRecGq + i] = st.gq[i];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) rec[kRecSww + i] = st.sww[i];
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) rec[kRecAy + i] = st.y_active ? st.ay[i] : 0.0;
+  rec[kRecActive] = st.y_active ? 1.0 : 0.0;
+  double b[kNX];
+#pragma unroll
+  for (int jc = 0; jc < 3; ++jc) {
+    b_column(P, st, u, jc, b);
+    rec[kRecBT + 5 * jc] = b[0];
+    rec[kRecBT + 5 * jc + 1] = b[4];
+    rec[kRecBT + 5 * jc + 2] = b[5];
+    rec[kRecBT + 5 * jc + 3] = b[6];
+    rec[kRecBT + 5 * jc + 4] = b[14];
+  }
+#pragma unroll
+  for (int jc = 3; jc < 6; ++jc) {
+    b_column(P, st, u, jc, b);
+    rec[kRecBG + jc - 3] = b[14];
+  }
+  b_column(P, st, u, 6, b);
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) rec[kRecBS + i] = b[i];
+#pragma unroll
+  for (int i = kRecBS + kNX; i < kRecSize; ++i) rec[i] = 0.0;
+}
+
+/// Column jc of B rebuilt from a record: the same values b_column produces.
+PT_HD void b_column_from_record(const ModelConst& P, const double* rec, int jc, double* b) {
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) b[i] = 0.0;
+  const double s = rec[kRecS];
+  if (jc < 3) {
+    const double* r = rec + kRecBT + 5 * jc;
+    b[0] = r[0];
+    b[4] = r[1];
+    b[5] = r[2];
+    b[6] = r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
+      b[11 + i] = s * JR;
+    }
+    b[14] = r[4];
+  } else if (jc < 6) {
+    const int j = jc - 3;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
+      b[11 + i] = s * Ji;
+    }
+    b[14] = rec[kRecBG + j];
+  } else {
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) b[i] = rec[kRecBS + i];
+  }
+}
+
 /// d = A * c in the structural sparsity of A (ascending column order inside every row, as
-/// mat_mat does: smallmat.hpp:115-120).
-PT_HD void apply_A(const Stage& st, const double* c, double* d) {
-  const double s = st.s;
+/// mat_mat does: smallmat.hpp:115-120), A taken from a stage record.
+PT_HD void apply_A(const double* rec, const double* c, double* d) {
+  const double s = rec[kRecS];
+  const double* svm = rec + kRecSvm;
+  const double* svq = rec + kRecSvq;
+  const double* sww = rec + kRecSww;
   d[0] = 0.0;
   d[1] = s * c[4];
   d[2] = s * c[5];
   d[3] = s * c[6];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double acc = st.svm[i] * c[0];
+    double acc = svm[i] * c[0];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc += st.svq[i * 4 + j] * c[7 + j];
+    for (int j = 0; j < 4; ++j) acc += svq[i * 4 + j] * c[7 + j];
     d[4 + i] = acc;
   }
-  const double* h = st.hw;
-  const double* g = st.gq;
+  const double* h = rec + kRecHw;
+  const double* g = rec + kRecGq;
   d[7] = h[2] * c[8] - h[1] * c[9] + h[0] * c[10] + g[3] * c[11] - g[2] * c[12] + g[1] * c[13];
   d[8] = -h[2] * c[7] + h[0] * c[9] + h[1] * c[10] + g[2] * c[11] + g[3] * c[12] - g[0] * c[13];
   d[9] = h[1] * c[7] - h[0] * c[8] + h[2] * c[10] - g[1] * c[11] + g[0] * c[12] + g[3] * c[13];
   d[10] = -h[0] * c[7] - h[1] * c[8] - h[2] * c[9] - g[0] * c[11] - g[1] * c[12] - g[2] * c[13];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
-    d[11 + i] = st.sww[i * 3] * c[11] + st.sww[i * 3 + 1] * c[12] + st.sww[i * 3 + 2] * c[13];
+    d[11 + i] = sww[i * 3] * c[11] + sww[i * 3 + 1] * c[12] + sww[i * 3 + 2] * c[13];
   double dy = 0.0;
-  if (st.y_active) {
+  if (rec[kRecActive] != 0.0) {
+    const double* ay = rec + kRecAy;
 #pragma unroll
-    for (int k = 0; k < kNXI; ++k) dy += st.ay[k] * c[k];
+    for (int k = 0; k < kNXI; ++k) dy += ay[k] * c[k];
   }
   d[14] = dy;
 }
 
-/// Per-warp scratch for the (lane-invariant) state part of the RK4 bundle.
-struct StateScratch {
-  double sx[kNX];  // state at the start of the RK4 step
-  double ax[kNX];  // running RK4 combination
+/// Stage time, RK4 weights and first-order-hold factors of stage `stage` of step `step`
+/// (discretizer.hpp:26-39, 118-135): shared by the state and the column pass.
+struct StageTime {
+  double wk, wn, lam_left, lam_right;
 };
+PT_HD StageTime stage_time(double tau_k, double tau_k1, int steps, int step, int stage) {
+  const double span = tau_k1 - tau_k;
+  const double h = span / steps;
+  const double t0 = tau_k + h * step;
+  const double t_end = (step + 1 == steps) ? tau_k1 : t0 + h;
+  const double tau = stage == 0 ? t0 : (stage == 3 ? t_end : t0 + 0.5 * h);
+  StageTime t;
+  t.wk = (stage == 0 || stage == 3) ? h / 6.0 : h / 3.0;  // RK4 weight
+  t.wn = stage == 2 ? h : 0.5 * h;                         // next-stage offset
+  t.lam_right = (tau - tau_k) / span;
+  t.lam_left = (tau_k1 - tau) / span;
+  return t;
+}
 
-/// Integrates one interval for sensitivity column `lane` (lanes >= 29 only follow the state).
-/// `writer` lanes update the shared state scratch (lane 0 on the GPU; every lane has a private
-/// scratch in the CPU simulation).  SYNC() is __syncwarp() on the device.
-/// On success col[15] holds column `lane` of [A | B- | B+] and x_end[15] the propagated state.
-template <class SyncFn>
-PT_HD int propagate_lane(const ModelConst& P, int lane, bool writer, StateScratch& sc,
-                         const double* xk, const double* uk, const double* uk1, double tau_k,
-                         double tau_k1, int steps, double* col, double* x_end, SyncFn SYNC) {
+/// State pass of one interval (the x part of propagate_interval, discretizer.hpp:82-141):
+/// 4 * steps model evaluations; EMIT(stage_number, const Stage&, const double* u) receives each
+/// one.  On success x_end[15] holds the propagated state.
+template <class EmitFn>
+PT_HD int propagate_state_pass(const ModelConst& P, const double* xk, const double* uk, const double* uk1,
+                               double tau_k, double tau_k1, int steps, double* x_end, EmitFn EMIT) {
   // all_finite(x_k), discretizer.hpp:89
   bool fin = true;
 #pragma unroll
   for (int i = 0; i < kNX; ++i) fin = fin && pt_finite(xk[i]);
   if (!fin) return kStPropDiverged;
-
-  const double span = tau_k1 - tau_k;
-  const double h = span / steps;
-  const bool is_col = lane < kCols;
-  const int jc = lane < kNX ? 0 : (lane - kNX) % kNU;    // control index of this lane's B column
-  const bool minus = lane >= kNX && lane < kNX + kNU;    // Phi_u- lanes get lam_left
-  const bool forced = lane >= kNX && lane < kCols;
-
-  double s_c[kNX], a_c[kNX], c[kNX];  // column: step start, RK4 combination, stage input
-  double xin[kNX];
+  double sx[kNX], ax[kNX], xin[kNX];
 #pragma unroll
-  for (int i = 0; i < kNX; ++i) {
-    s_c[i] = (i == lane) ? 1.0 : 0.0;  // Phi_x(0) = I, Phi_u(0) = 0 (discretizer.hpp:94-96)
-    xin[i] = xk[i];
-  }
-  if (writer) {
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) sc.sx[i] = xk[i];
-  }
-  SYNC();
-
+  for (int i = 0; i < kNX; ++i) sx[i] = xin[i] = ax[i] = xk[i];
   for (int step = 0; step < steps; ++step) {
-    const double t0 = tau_k + h * step;
-    const double t_end = (step + 1 == steps) ? tau_k1 : t0 + h;
 #pragma unroll 1
     for (int stage = 0; stage < 4; ++stage) {
-      const double tau = stage == 0 ? t0 : (stage == 3 ? t_end : t0 + 0.5 * h);
-      const double wk = (stage == 0 || stage == 3) ? h / 6.0 : h / 3.0;       // RK4 weight
-      const double wn = stage == 2 ? h : 0.5 * h;                             // next-stage offset
-      // foh_interp, discretizer.hpp:26-39
-      const double lam_right = (tau - tau_k) / span;
-      const double lam_left = (tau_k1 - tau) / span;
+      const StageTime t = stage_time(tau_k, tau_k1, steps, step, stage);
       double u[kNU];
 #pragma unroll
-      for (int i = 0; i < kNU; ++i) u[i] = lam_left * uk[i] + lam_right * uk1[i];
-      if (stage == 0) {
-#pragma unroll
-        for (int i = 0; i < kNX; ++i) c[i] = s_c[i];
-      }
+      for (int i = 0; i < kNU; ++i) u[i] = t.lam_left * uk[i] + t.lam_right * uk1[i];
       Stage st;
       const int rc = eval_stage(P, xin, u, st);
       if (rc != kStOk) return rc;
-
-      if (is_col) {
-        double d[kNX];
-        apply_A(st, c, d);
-        if (forced) {
-          double b[kNX];
-          b_column(P, st, u, jc, b);
-          const double lam = minus ? lam_left : lam_right;
-#pragma unroll
-          for (int i = 0; i < kNX; ++i) d[i] += lam * b[i];
-        }
-#pragma unroll
-        for (int i = 0; i < kNX; ++i) {
-          a_c[i] = (stage == 0 ? s_c[i] : a_c[i]) + wk * d[i];
-          c[i] = s_c[i] + wn * d[i];  // unused after stage 3
-        }
-      }
-      // state part: identical in every lane; only the writer touches the scratch
-      SYNC();
+      EMIT(step * 4 + stage, st, u);
 #pragma unroll
       for (int i = 0; i < kNX; ++i) {
-        const double sxi = sc.sx[i];
-        const double axi = (stage == 0 ? sxi : sc.ax[i]) + wk * st.f[i];
-        xin[i] = sxi + wn * st.f[i];
-        if (stage == 3) xin[i] = axi;
-        st.f[i] = axi;  // reuse as the value to publish
-      }
-      SYNC();
-      if (writer) {
-#pragma unroll
-        for (int i = 0; i < kNX; ++i) {
-          sc.ax[i] = st.f[i];
-          if (stage == 3) sc.sx[i] = st.f[i];
-        }
+        const double axi = (stage == 0 ? sx[i] : ax[i]) + t.wk * st.f[i];
+        xin[i] = stage == 3 ? axi : sx[i] + t.wn * st.f[i];
+        ax[i] = axi;
+        if (stage == 3) sx[i] = axi;
       }
     }
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) s_c[i] = a_c[i];
     // all_finite(s.x) after every RK4 step, discretizer.hpp:136
     fin = true;
 #pragma unroll
     for (int i = 0; i < kNX; ++i) fin = fin && pt_finite(xin[i]);
     if (!fin) return kStPropDiverged;
-    SYNC();
+  }
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) x_end[i] = xin[i];
+  return kStOk;
+}
+
+/// Per-lane state of the column pass: sensitivity column `lane` of [Phi_x | Phi_u- | Phi_u+].
+struct ColumnLane {
+  double s_c[kNX], a_c[kNX], c[kNX];  // step start, RK4 combination, stage input
+  int jc;                              // control index of this lane's B column
+  bool minus, forced;
+};
+PT_HD void column_init(ColumnLane& L, int lane) {
+  L.jc = lane < kNX ? 0 : (lane - kNX) % kNU;
+  L.minus = lane >= kNX && lane < kNX + kNU;  // Phi_u- lanes get lam_left
+  L.forced = lane >= kNX && lane < kCols;
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) {
+    L.s_c[i] = (i == lane) ? 1.0 : 0.0;  // Phi_x(0) = I, Phi_u(0) = 0 (discretizer.hpp:94-96)
+    L.a_c[i] = L.c[i] = L.s_c[i];
+  }
+}
+/// One RK4 stage of the column (discretizer.hpp:99-135): d = A c (+ lam * b), then the RK4
+/// combination.  After stage 3 the step result is in s_c.
+PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, const StageTime& t, int stage) {
+  if (stage == 0) {
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) L.c[i] = L.s_c[i];
+  }
+  double d[kNX];
+  apply_A(rec, L.c, d);
+  if (L.forced) {
+    double b[kNX];
+    b_column_from_record(P, rec, L.jc, b);
+    const double lam = L.minus ? t.lam_left : t.lam_right;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) d[i] += lam * b[i];
   }
 #pragma unroll
   for (int i = 0; i < kNX; ++i) {
-    col[i] = s_c[i];
-    x_end[i] = xin[i];
+    L.a_c[i] = (stage == 0 ? L.s_c[i] : L.a_c[i]) + t.wk * d[i];
+    L.c[i] = L.s_c[i] + t.wn * d[i];  // unused after stage 3
   }
-  return kStOk;
+  if (stage == 3) {
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) L.s_c[i] = L.a_c[i];
+  }
 }
 
 }  // namespace ptopt_b200

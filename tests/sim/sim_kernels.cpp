@@ -1,8 +1,9 @@
-// sim_kernels.cpp — TEST INFRASTRUCTURE.  Runs the device lane code of
+// sim_kernels.cpp — TEST INFRASTRUCTURE.  Runs the device thread / lane code of
 // paper_2404_18034_b200/csrc/*.cuh on the CPU, one "lane" after another, so the
 // kernel arithmetic can be checked against the oracle without a GPU.  Not part of
 // the product library and never loaded by it.
 #include <cstring>
+#include <vector>
 
 #include "model_const.hpp"
 #include "rocket_model.cuh"
@@ -11,7 +12,8 @@ using namespace ptopt_b200;
 
 extern "C" {
 
-/// One interval through propagate_lane for every lane, then the kernel's epilogue.
+/// One interval through the state pass (records kept in memory) and the column pass of every
+/// lane, then the kernel's epilogue.
 int sim_propagate_interval(const ptopt_vehicle_params* vp, const double* xk, const double* uk,
                            const double* uk1, double tau_k, double tau_k1, int steps, double* A,
                            double* Bm, double* Bp, double* w, double* x_end) {
@@ -19,15 +21,19 @@ int sim_propagate_interval(const ptopt_vehicle_params* vp, const double* xk, con
   if (!make_model_const(*vp, mc)) return -8;
   double block[kNX][kCols];
   double xe[kNX];
-  for (int lane = 0; lane < 32; ++lane) {
-    StateScratch sc;
-    double col[kNX], xel[kNX];
-    const int rc = propagate_lane(mc, lane, true, sc, xk, uk, uk1, tau_k, tau_k1, steps, col, xel,
-                                  [] {});
-    if (rc) return rc;
-    if (lane < kCols)
-      for (int i = 0; i < kNX; ++i) block[i][lane] = col[i];
-    if (lane == 0) std::memcpy(xe, xel, sizeof xe);
+  std::vector<double> recs((size_t)4 * steps * kRecSize);
+  const int rc = propagate_state_pass(mc, xk, uk, uk1, tau_k, tau_k1, steps, xe,
+                                      [&](int stage_no, const Stage& st, const double* u) {
+                                        pack_stage_record(mc, st, u, &recs[(size_t)stage_no * kRecSize]);
+                                      });
+  if (rc) return rc;
+  for (int lane = 0; lane < kCols; ++lane) {
+    ColumnLane L;
+    column_init(L, lane);
+    for (int sn = 0; sn < 4 * steps; ++sn)
+      column_stage(mc, L, &recs[(size_t)sn * kRecSize], stage_time(tau_k, tau_k1, steps, sn >> 2, sn & 3),
+                   sn & 3);
+    for (int i = 0; i < kNX; ++i) block[i][lane] = L.s_c[i];
   }
   for (int i = 0; i < kNX; ++i) {
     double acc = 0.0;

@@ -396,7 +396,8 @@ def test_scp_solve_n50_two_instances(ptor):
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
                           batch["rng_seed"])
         launches = s.launch_count
-    assert launches == 1 + 5 * 25 + 2
+    # init + 25 x (state pass, column pass, prepare, power, PIPG, update) + the final defect pass
+    assert launches == 1 + 6 * 25 + 3
     spec = sc.dispersion
     wall, rec, xr, ur = ptor.run_batch(d, sc.initial_state, spec.r_low, spec.r_high, spec.seed, 2,
                                        2, 8, keep=True)

@@ -10,6 +10,8 @@
 //                    the B forcing to its column in registers; then stages the 15 x 29 block in
 //                    shared memory for w = x_end - A x - B- u - B+ u+ and the coalesced write.
 // See rocket_model.cuh for the per-thread / per-lane algorithms.
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "rocket_model.cuh"
 
@@ -76,8 +78,10 @@ __global__ void __launch_bounds__(128) state_pass_kernel(LinearizeArgs a, long l
   for (int i = 0; i < kNX; ++i) xe[i] = x_end[i];
 }
 
+constexpr int kRecRing = 4;  // stage records in flight per warp (cp.async ring)
+
 struct __align__(16) WarpSmem {
-  double rec[2][kRecSize];           // stage records, double-buffered
+  double rec[kRecRing][kRecSize];    // ring of stage records
   double block[kNX * kStageStride];  // staged [A | B- | B+], row-major
   double xk[kNX], uk[kNU], uk1[kNU], xe[kNX];
 };
@@ -117,31 +121,41 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   const double* recs = a.stages + record_index(local, nst, 0);
   const size_t rec_stride = (size_t)kRecSize * 32;  // between consecutive stages of an interval
   const bool third = lane + 64 < kRecSize;
-  double r0 = recs[(size_t)lane * 32], r1 = recs[(size_t)(lane + 32) * 32];
-  double r2 = third ? recs[(size_t)(lane + 64) * 32] : 0.0;
+  // record `sn` -> ring slot sn % kRecRing, three 8-byte asynchronous copies per lane, one
+  // commit group per record (an empty group past the last record keeps the counting uniform)
+  auto fetch = [&](int sn) {
+    if (sn < nst) {
+      const double* src = recs + (size_t)sn * rec_stride + (size_t)lane * 32;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&ws.rec[sn % kRecRing][lane]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 32 * 8), "l"(src + 32 * 32) : "memory");
+      if (third)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 64 * 8), "l"(src + 64 * 32) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int sn = 0; sn < kRecRing - 1; ++sn) fetch(sn);
 
   ColumnLane L;
   column_init(L, lane);
   const bool is_col = lane < kCols;
-  for (int sn = 0; sn < nst; ++sn) {
-    double* rec = ws.rec[sn & 1];
-    rec[lane] = r0;
-    rec[lane + 32] = r1;
-    if (third) rec[lane + 64] = r2;
+  // one stage: wait for its record, start the copy of the record kRecRing - 1 stages ahead into
+  // the slot everybody finished reading a stage ago, apply the record to the column
+  auto run_stage = [&](auto stage_tag, int sn, double wk, double wn) {
+    constexpr int kStage = decltype(stage_tag)::value;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kRecRing - 2) : "memory");
     __syncwarp();
-    if (sn + 1 < nst) {  // next record: in flight while this stage is computed
-      const double* nx = recs + (size_t)(sn + 1) * rec_stride;
-      r0 = nx[(size_t)lane * 32];
-      r1 = nx[(size_t)(lane + 32) * 32];
-      if (third) r2 = nx[(size_t)(lane + 64) * 32];
-    }
-    const int stage = sn & 3;
-    StageTime t;
-    t.wk = (stage == 0 || stage == 3) ? h6 : h3;
-    t.wn = stage == 2 ? h : hh;
-    t.lam_left = rec[kRecLamLeft];
-    t.lam_right = rec[kRecLamRight];
-    if (is_col) column_stage(a.model, L, rec, t, stage);
+    fetch(sn + kRecRing - 1);
+    const double* rec = ws.rec[sn % kRecRing];
+    // lanes 29..31 carry an all-zero dummy column (no branch around the stage)
+    column_stage<kStage>(a.model, L, rec, wk, wn, rec[kRecLamLeft], rec[kRecLamRight]);
+  };
+  for (int step = 0; step < a.steps; ++step) {
+    run_stage(std::integral_constant<int, 0>{}, 4 * step, h6, hh);
+    run_stage(std::integral_constant<int, 1>{}, 4 * step + 1, h3, hh);
+    run_stage(std::integral_constant<int, 2>{}, 4 * step + 2, h3, h);
+    run_stage(std::integral_constant<int, 3>{}, 4 * step + 3, h6, hh);
   }
 
   // stage the 15x29 block, then w = x_end - A x_k - B- u_k - B+ u_k1 row by row in the

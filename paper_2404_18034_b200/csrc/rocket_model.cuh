@@ -346,37 +346,6 @@ PT_HD void pack_stage_record(const ModelConst& P, const Stage& st, const double*
   for (int i = kRecBS + kNX; i < kRecSize; ++i) rec[i] = 0.0;
 }
 
-/// Column jc of B rebuilt from a record: the same values b_column produces.
-PT_HD void b_column_from_record(const ModelConst& P, const double* rec, int jc, double* b) {
-#pragma unroll
-  for (int i = 0; i < kNX; ++i) b[i] = 0.0;
-  const double s = rec[kRecS];
-  if (jc < 3) {
-    const double* r = rec + kRecBT + 5 * jc;
-    b[0] = r[0];
-    b[4] = r[1];
-    b[5] = r[2];
-    b[6] = r[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
-      b[11 + i] = s * JR;
-    }
-    b[14] = r[4];
-  } else if (jc < 6) {
-    const int j = jc - 3;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
-      b[11 + i] = s * Ji;
-    }
-    b[14] = rec[kRecBG + j];
-  } else {
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) b[i] = rec[kRecBS + i];
-  }
-}
-
 /// d = A * c in the structural sparsity of A (ascending column order inside every row, as
 /// mat_mat does: smallmat.hpp:115-120), A taken from a stage record.
 PT_HD void apply_A(const double* rec, const double* c, double* d) {
@@ -492,30 +461,66 @@ PT_HD void column_init(ColumnLane& L, int lane) {
     L.a_c[i] = L.c[i] = L.s_c[i];
   }
 }
-/// One RK4 stage of the column (discretizer.hpp:99-135): d = A c (+ lam * b), then the RK4
-/// combination.  After stage 3 the step result is in s_c.
-PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, const StageTime& t, int stage) {
-  if (stage == 0) {
+
+/// d += lam * (column jc of B), B taken from a stage record.  Rows where the column is
+/// structurally zero are skipped (the reference adds lam * 0 there, an exact no-op).
+PT_HD void add_b_column(const ModelConst& P, const double* rec, int jc, double lam, double* d) {
+  const double s = rec[kRecS];
+  if (jc < 3) {  // thrust: rows 0, 4..6, 11..13, 14
+    const double* r = rec + kRecBT + 5 * jc;
+    d[0] += lam * r[0];
+    d[4] += lam * r[1];
+    d[5] += lam * r[2];
+    d[6] += lam * r[3];
 #pragma unroll
-    for (int i = 0; i < kNX; ++i) L.c[i] = L.s_c[i];
+    for (int i = 0; i < 3; ++i) {
+      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
+      d[11 + i] += lam * (s * JR);
+    }
+    d[14] += lam * r[4];
+  } else if (jc < 6) {  // torque: rows 11..13, 14
+    const int j = jc - 3;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
+      d[11 + i] += lam * (s * Ji);
+    }
+    d[14] += lam * rec[kRecBG + j];
+  } else {  // dilation: the undilated rate
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) d[i] += lam * rec[kRecBS + i];
   }
+}
+
+/// RK4 stage kStage of the column (discretizer.hpp:99-135): d = A c (+ lam * b), then the RK4
+/// combination.  After stage 3 the step result is in s_c.  wk / wn: RK4 weight and next-stage
+/// offset of the stage (StageTime); lam_left / lam_right: its first-order-hold factors.
+template <int kStage>
+PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, double wk, double wn,
+                        double lam_left, double lam_right) {
   double d[kNX];
-  apply_A(rec, L.c, d);
-  if (L.forced) {
-    double b[kNX];
-    b_column_from_record(P, rec, L.jc, b);
-    const double lam = L.minus ? t.lam_left : t.lam_right;
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) d[i] += lam * b[i];
-  }
+  apply_A(rec, kStage == 0 ? L.s_c : L.c, d);
+  if (L.forced) add_b_column(P, rec, L.jc, L.minus ? lam_left : lam_right, d);
 #pragma unroll
   for (int i = 0; i < kNX; ++i) {
-    L.a_c[i] = (stage == 0 ? L.s_c[i] : L.a_c[i]) + t.wk * d[i];
-    L.c[i] = L.s_c[i] + t.wn * d[i];  // unused after stage 3
+    if (kStage == 0) {
+      L.a_c[i] = L.s_c[i] + wk * d[i];
+      L.c[i] = L.s_c[i] + wn * d[i];
+    } else if (kStage < 3) {
+      L.a_c[i] = L.a_c[i] + wk * d[i];
+      L.c[i] = L.s_c[i] + wn * d[i];
+    } else {
+      L.s_c[i] = L.a_c[i] + wk * d[i];
+    }
   }
-  if (stage == 3) {
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) L.s_c[i] = L.a_c[i];
+}
+/// Run-time stage index (CPU simulation).
+PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, const StageTime& t, int stage) {
+  switch (stage) {
+    case 0: column_stage<0>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
+    case 1: column_stage<1>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
+    case 2: column_stage<2>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
+    default: column_stage<3>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
   }
 }
 

@@ -318,7 +318,7 @@ def run_own_arm(args):
         # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
         # (profiles/ncu_traffic.json: bytes for a 148-instance launch), scaled to this batch
         traffic = None
-        kernel_of = {"linearize": "linearize_kernel", "power_iteration": "power_fast_kernel",
+        kernel_of = {"linearize": "column_pass_kernel", "power_iteration": "power_fast_kernel",
                      "pipg": "pipg_fast_kernel"}
         tpath = ROOT / "profiles" / "ncu_traffic.json"
         if tpath.exists() and n == 50:

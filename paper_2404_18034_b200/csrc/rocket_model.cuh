@@ -1,16 +1,17 @@
-// rocket_model.cuh — 6-DoF vehicle + CTCS augmentation evaluated in registers, and the
-// per-lane RK4 sensitivity propagation used by the discretization kernel.
+// rocket_model.cuh — 6-DoF vehicle + CTCS augmentation evaluated in registers, and the two passes
+// of the exact discretization (propagate_interval,
+// /root/reference/proj/include/ptopt/discretizer.hpp:82-149).
 //
-// One warp integrates one grid interval (propagate_interval,
-// /root/reference/proj/include/ptopt/discretizer.hpp:82-149).  Lane j < 29 owns column j of the
-// sensitivity bundle [Phi_x (15) | Phi_u- (7) | Phi_u+ (7)]; every lane carries the (identical)
-// augmented state, so the model, its Jacobian and the column product A(tau) * col are evaluated
-// entirely in registers with no cross-lane traffic in the inner loop.  The Jacobian
-// (rocket6dof.hpp:303-402 through ctcs.hpp:79-129) is applied in its structural sparsity:
-// skipped entries are exact zeros in the reference's dense product, so results agree with the
-// dense loops up to FMA contraction.
+// The state part of the RK4 bundle does not depend on the sensitivity columns.  The state pass
+// (one thread per interval) therefore evaluates the model, its constraints and the Jacobian
+// scalars (rocket6dof.hpp:245-402 through ctcs.hpp:47-129) once per stage and packs what the
+// columns need into an 84-double stage record.  The column pass (one warp per interval, lane
+// j < 29 owns column j of [Phi_x (15) | Phi_u- (7) | Phi_u+ (7)]) applies A(tau) and the B
+// forcing from the record.  The Jacobian is applied in its structural sparsity: skipped entries
+// are exact zeros in the reference's dense product, so results agree with the dense loops up to
+// FMA contraction.
 //
-// Everything here is `__host__ __device__` so tests/sim can run the same lane code on the CPU.
+// Everything here is `__host__ __device__` so tests/sim can run the same code on the CPU.
 #pragma once
 
 #include <math.h>

@@ -61,6 +61,10 @@ __host__ __device__ constexpr int pos_col(int j) {
   return j < kNX ? j : (j < kNX + kNU ? pos_bm(j - kNX) : pos_bp(j - kNX - kNU));
 }
 
+/// std::max(0.0, v) as the reference evaluates it (pipg.hpp:423-430: `(0.0 < v) ? v : 0.0`, so a
+/// NaN becomes 0): one compare and a select instead of fmax()'s NaN-propagating sequence.
+__device__ __forceinline__ double clip0(double v) { return 0.0 < v ? v : 0.0; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -710,8 +714,8 @@ pipg_fast_kernel(PipgArgs a) {
         resid += pm;
         resid += pp;
         const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
-        const double vp = fmax(0.0, vp0 - alpha * (a.shape.w_ep + p0));
-        const double vn = fmax(0.0, vn0 - alpha * (a.shape.w_ep - p0));
+        const double vp = clip0(vp0 - alpha * (a.shape.w_ep + p0));
+        const double vn = clip0(vn0 - alpha * (a.shape.w_ep - p0));
         resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv_k[r];
         const double pn = p0 + beta * resid;
         if (kStore) {
@@ -727,7 +731,7 @@ pipg_fast_kernel(PipgArgs a) {
       }
       if (g == 4) {
         const double drift = xr_k[kXS + 14] - v[14] - eps_k[0];
-        const double tn = fmax(0.0, the + beta * drift);
+        const double tn = clip0(the + beta * drift);
         if (kStore) snap[S.th + kc] = tn;
         the = ival ? one_m_rho * the + a.rho * tn : 0.0;
       }

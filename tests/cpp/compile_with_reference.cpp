@@ -7,6 +7,7 @@
 #include "ptopt/scp.hpp"
 
 #include "ptopt_b200.hpp"
+#include "ptopt_b200_io.hpp"
 
 namespace b2 = ptopt_b200;
 
@@ -32,6 +33,13 @@ double instantiate_everything(const ptopt::RocketProblem& pb, const ptopt::Rocke
   const auto res = b2::scp_solve(pb, guess);
   const auto audit = b2::dense_violation_audit(pb.model, res.iterate, pb.grid, 64);
   const auto batch = b2::mc::run_batch(pb, bc, spec, 8, 4, 64, true);
+  // output side (csv.hpp:34-96, montecarlo.hpp:177-209) on the reference's records / trajectory
+  const std::vector<ptopt::mc::RunRecord> ref_records(2);
+  const auto summary = b2::mc::aggregate(ref_records, 25, 1.0, 1);
+  b2::csvio::write_runs("/dev/null", ref_records);
+  b2::csvio::write_summary("/dev/null", summary);
+  b2::csvio::write_trajectory("/dev/null", guess, pb.grid);
+  b2::csvio::write_runs("/dev/null", batch.records);
   return blocks[0].A(0, 0) + one.w[0] + sp.w[0][0] + pr.iterations + res.final_defect_inf + audit.max_pointwise_g +
          batch.records[0].propellant_used;
 }

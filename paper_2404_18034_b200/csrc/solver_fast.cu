@@ -39,6 +39,7 @@ constexpr int kXS = 18;      // node stride of x vectors in shared memory (16-by
 constexpr int kUS = 10;      // node stride of u vectors
 constexpr int kPS = 35;      // stride of one thread's partial-sum slot (== 3 mod 16: conflict-free)
 constexpr int kFastWarps = 8;  // slots of the reduction arrays (any variant has at most this many warps)
+constexpr int kPipgClusterSpill = 14;  // operator entries per thread the cluster PIPG kernel keeps in shared memory
 
 // Two compile-time shapes of a CTA.  kCap = kFastMaxNodes (51 nodes, 256 threads, one CTA per SM)
 // holds a whole instance of up to 51 nodes, or half of a 2-CTA cluster for up to 102.  kCap =
@@ -124,17 +125,33 @@ __device__ __forceinline__ void load_node_vectors(const double* xs_k, const doub
   }
 }
 
+// The PIPG kernel of the cluster variants needs a dozen registers more than the 255 a thread can
+// have next to its 174 of operator; ptxas then spills operator entries to local memory and reloads
+// them every iteration.  Those variants keep the last kSpill entries of a thread's third row
+// (B+ columns) in a thread-private shared-memory column instead (`opx[c * stride]`, consecutive
+// threads in consecutive words: conflict-free) -- chosen, not left to the register allocator.
+template <int kSpill>
+struct OpTail {
+  const double* opx;  // this thread's entry of column 0
+  int stride;         // doubles between columns (the CTA's thread count)
+  __device__ __forceinline__ static constexpr bool spilled(int r, int j) { return r == kR - 1 && j >= kW - kSpill; }
+  __device__ __forceinline__ double get(const double (&a)[kR][kW], int r, int j) const {
+    return spilled(r, j) ? opx[(j - (kW - kSpill)) * stride] : a[r][j];
+  }
+};
+
 /// Row r of the forward product: A- x_k, B- u_k, B+ u_{k+1}, each summed in ascending column
 /// order (mat_vec, smallmat.hpp:93-97).
-__device__ __forceinline__ void row_products(const double (&a)[kR][kW], const double (&v)[kW], int r,
-                                             double& pa, double& pm, double& pp) {
+template <int kSpill>
+__device__ __forceinline__ void row_products(const double (&a)[kR][kW], const OpTail<kSpill>& tail,
+                                             const double (&v)[kW], int r, double& pa, double& pm, double& pp) {
   double sa = 0.0, sm = 0.0, sp = 0.0;
 #pragma unroll
-  for (int j = 0; j < kNX; ++j) sa += a[r][j] * v[j];
+  for (int j = 0; j < kNX; ++j) sa += tail.get(a, r, j) * v[j];
 #pragma unroll
   for (int j = 0; j < kNU; ++j) {
-    sm += a[r][kNX + j] * v[kNX + j];
-    sp += a[r][kNX + kNU + j] * v[kNX + kNU + j];
+    sm += tail.get(a, r, kNX + j) * v[kNX + j];
+    sp += tail.get(a, r, kNX + kNU + j) * v[kNX + kNU + j];
   }
   pa = sa;
   pm = sm;
@@ -142,14 +159,25 @@ __device__ __forceinline__ void row_products(const double (&a)[kR][kW], const do
 }
 
 /// Publishes the partial column sums of this thread's three rows against its three dual entries.
-__device__ __forceinline__ void store_partials(const double (&a)[kR][kW], const double (&d)[kR],
-                                               double* slot) {
+template <int kSpill>
+__device__ __forceinline__ void store_partials(const double (&a)[kR][kW], const OpTail<kSpill>& tail,
+                                               const double (&d)[kR], double* slot) {
 #pragma unroll
   for (int j = 0; j < kW; ++j) {
     double p = a[0][j] * d[0];
     p += a[1][j] * d[1];
-    p += a[2][j] * d[2];
+    p += tail.get(a, 2, j) * d[2];
     slot[pos_col(j)] = p;
+  }
+}
+
+/// Moves the entries OpTail serves out of the register copy (after load_rows).
+template <int kSpill>
+__device__ __forceinline__ void park_tail(double (&a)[kR][kW], double* opx, int stride) {
+#pragma unroll
+  for (int c = 0; c < kSpill; ++c) {
+    opx[c * stride] = a[kR - 1][kW - kSpill + c];
+    a[kR - 1][kW - kSpill + c] = 0.0;
   }
 }
 
@@ -163,7 +191,7 @@ __device__ __forceinline__ double column_sum(const double* part_k, int pos) {
 struct FastLayout {
   int xs, us, phi, theta, part, red, total;  // offsets in doubles
   // PIPG only
-  int wv, eps, umin, umax, snap, bnd;
+  int wv, eps, umin, umax, snap, bnd, opx;
 };
 
 // One snapshot of the *_cur groups (pipg.hpp:490-495), with room for the scratch entries the
@@ -211,6 +239,7 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
     L.umax = o; o += 2 * kThreads;  // {lo, hi} of its second one (+-inf where it has none)
     L.snap = o; o += 2 * snap_layout<kCap>().total;
     L.bnd = o; o += 6 * 16;  // ecost, init_val, final_val, init_on, final_on (as doubles)
+    L.opx = o; o += kPipgClusterSpill * kThreads;  // OpTail columns (cluster variants)
   }
   L.total = o;
   return L;
@@ -224,9 +253,83 @@ __host__ __device__ constexpr FastLayout fast_layout(bool pipg) {
 // values store them twice: locally, and through distributed shared memory into the guard entries
 // the partner's single-CTA code already reads — rank 1's first node vectors into rank 0's "next
 // node" slot, rank 0's last interval (B+ partial sums, duals) into rank 1's "previous interval"
-// slots, every warp's share of a reduction into the partner's copy.  Phase barriers become
-// cluster barriers (release / acquire), nothing is ever read remotely.
+// slots, every warp's share of a reduction into the partner's copy.  Nothing is ever read remotely.
+//
+// Hand-off.  A release/acquire cluster barrier costs ~500 cycles on B200 and the hot loops would
+// need two per iteration (tools/probes/cluster_sync_cost.cu).  Instead every remote store is an
+// asynchronous store that completes transaction bytes on an mbarrier in the RECEIVER's shared
+// memory ("mailbox"): the receiver arms the barrier with the byte count of the phase and only the
+// warps that read the guard entries wait for it; phase boundaries inside a CTA stay plain block
+// barriers.  One way, no fence (~150 cycles).  Overwriting a guard entry before the partner has
+// read it is excluded by data dependence: a CTA can only produce the next value after it has
+// received everything the partner computed from the previous one.
 // ---------------------------------------------------------------------------------------------
+enum Mailbox { kBoxPrev = 0, kBoxNext = 1, kBoxNorm = 2 /* and 3: by trip parity */, kBoxes = 4 };
+constexpr int kBoxOffset = 12 * kFastWarps;                 // mbarriers live in the unused tail of `red`
+constexpr int kPrevBytes = 8 * (kNX + 1 + kG * kNU);        // duals + relaxation dual + B+ partial sums
+constexpr int kNextBytes = 8 * (kNX + kNU);                 // first node vectors of rank 1
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+/// Shared-memory address of `local` inside CTA `rank` of the cluster (shared::cluster window).
+__device__ __forceinline__ unsigned partner_u32(const void* local, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+/// Asynchronous remote store of one double; completes 8 transaction bytes on the receiver's mailbox.
+__device__ __forceinline__ void push_f64(unsigned dst, double v, unsigned box) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v),
+               "r"(box)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* bar, int bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int phase) {
+  unsigned ok;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(smem_u32(bar)), "r"((unsigned)(phase & 1))
+                 : "memory");
+  } while (!ok);
+}
+
+/// Per-thread view of the mailboxes of a cluster CTA.
+struct Boxes {
+  unsigned long long* local;  // [kBoxes] in this CTA's shared memory
+  unsigned remote;            // the partner's [kBoxes] (shared::cluster address)
+  bool prev_warp, next_warp;  // this warp reads the "previous interval" / "next node" guard entries
+  bool prev_armer, next_armer, norm_armer;
+  int norm_bytes;
+  __device__ __forceinline__ unsigned box(int which) const { return remote + 8u * (unsigned)which; }
+  /// Arms mailbox `which` for `phase` (one thread) and waits until its bytes have arrived.
+  __device__ __forceinline__ void receive(int which, bool mine, bool armer, int bytes, int phase) const {
+    if (!mine) return;
+    if (armer) mbar_expect(local + which, bytes);
+    mbar_wait(local + which, phase);
+  }
+  __device__ __forceinline__ void recv_prev(int phase) const { receive(kBoxPrev, prev_warp, prev_armer, kPrevBytes, phase); }
+  __device__ __forceinline__ void recv_next(int phase) const { receive(kBoxNext, next_warp, next_armer, kNextBytes, phase); }
+  /// Norm shares of trip `trip` (0: the seed).  This exchange is not a ping-pong -- both CTAs send
+  /// every trip, and rank 0 may run up to one trip ahead of rank 1 (only its NEXT forward map needs
+  /// rank 1's boundary node) -- so one mailbox would see the shares of trip t + 1 before trip t is
+  /// armed or polled (lost bytes, or a phase parity that flips twice under a slow warp).  Two
+  /// mailboxes alternate by trip parity instead: a CTA can never be two trips ahead.
+  __device__ __forceinline__ unsigned norm_box(int trip) const { return box(kBoxNorm + (trip & 1)); }
+  __device__ __forceinline__ void recv_norm(int trip) const {
+    receive(kBoxNorm + (trip & 1), true, norm_armer, norm_bytes, trip >> 1);
+  }
+};
+
+/// Initialises the mailboxes (after the shared memory has been cleared) and meets the partner, so
+/// that both CTAs are running, cleared and armed before any remote store.
+template <bool kCluster>
+__device__ __forceinline__ Boxes open_boxes(double* red, const struct Split& cut, int tid, int warp, int nwarps);
+
 struct Split {
   int rank;   // CTA rank inside the cluster (0 without clusters)
   int node0;  // first global node of this CTA
@@ -257,11 +360,37 @@ __device__ __forceinline__ T* in_cta(T* local, int rank) {
   return cg::this_cluster().map_shared_rank(local, rank);
 }
 
-/// Copies the B+ partial sums a thread has just published in `slot` into `remote_slot` (the
-/// matching "previous interval" guard slot of the partner CTA).
-__device__ __forceinline__ void push_bp_partials(const double* slot, double* remote_slot) {
+template <bool kCluster>
+__device__ __forceinline__ Boxes open_boxes(double* red, const Split& cut, int tid, int warp, int nwarps) {
+  Boxes bx{};
+  if constexpr (kCluster) {
+    bx.local = reinterpret_cast<unsigned long long*>(red + kBoxOffset);
+    __syncthreads();  // the clearing loop is done
+    if (tid == 0) {
 #pragma unroll
-  for (int c = 0; c < kNU; ++c) remote_slot[pos_bp(c)] = slot[pos_bp(c)];
+      for (int i = 0; i < kBoxes; ++i) mbar_init(bx.local + i, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cg::this_cluster().sync();
+    bx.remote = partner_u32(bx.local, cut.rank ^ 1);
+    const int bfirst = kG * (cut.half - 1);  // threads of rank 0's last node: bfirst .. bfirst + kG - 1
+    bx.prev_warp = cut.rank == 1 && warp == 0;
+    bx.next_warp = cut.rank == 0 && (warp == (bfirst >> 5) || warp == ((bfirst + kG - 1) >> 5));
+    bx.prev_armer = cut.rank == 1 && tid == 0;
+    bx.next_armer = cut.rank == 0 && tid == bfirst;
+    bx.norm_armer = tid == 0;
+    bx.norm_bytes = 8 * nwarps;
+  } else {
+    __syncthreads();
+  }
+  return bx;
+}
+
+/// Sends the B+ partial sums a thread has just published in `slot` to `remote_slot` (the matching
+/// "previous interval" guard slot of the partner CTA).
+__device__ __forceinline__ void push_bp_partials(const double* slot, unsigned remote_slot, unsigned box) {
+#pragma unroll
+  for (int c = 0; c < kNU; ++c) push_f64(remote_slot + 8u * pos_bp(c), slot[pos_bp(c)], box);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -285,8 +414,7 @@ power_fast_kernel(PowerArgs a) {
   const int kc = (kCluster && k >= cut.nloc) ? k + 1 : k;
   constexpr FastLayout L = fast_layout<kCap>(false);
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
-  // in a cluster: both CTAs are running and have cleared their memory before any remote store
-  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
+  const Boxes bx = open_boxes<kCluster>(sm + L.red, cut, tid, warp, nwarps);
   double* xs_k = sm + L.xs + kc * kXS;          // x_k; x_{k+1} at +kXS
   double* us_k = sm + L.us + kc * kUS;
   double* phi_k = sm + L.phi + kc * kNX + kR * g;  // own dual entries; interval k-1 at -kNX
@@ -301,9 +429,6 @@ power_fast_kernel(PowerArgs a) {
   // guard entries, the first node of rank 1 feeds rank 0's "next node" entries
   const bool push_prev = kCluster && cut.rank == 0 && k == cut.half - 1;
   const bool push_next = kCluster && cut.rank == 1 && k == 0 && node;
-  auto phase_barrier = [&]() {
-    if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
-  };
   auto norm_sq = [&](int parity) {  // sum of both CTAs' partial sums, rank 0's first
     double own = 0.0, other = 0.0;
 #pragma unroll
@@ -368,9 +493,10 @@ power_fast_kernel(PowerArgs a) {
   acc = warp_sum(acc);
   if (lane == 0) {
     red[warp] = acc;
-    if constexpr (kCluster) *in_cta(redp + warp, cut.rank ^ 1) = acc;
+    if constexpr (kCluster) push_f64(partner_u32(redp + warp, cut.rank ^ 1), acc, bx.norm_box(0));
   }
-  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
+  __syncthreads();
+  if constexpr (kCluster) bx.recv_norm(0);  // the seed's shares
   double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (tid == 0 && cut.rank == 0) {
@@ -390,13 +516,16 @@ power_fast_kernel(PowerArgs a) {
   bool done = false;
   for (int j = 1; j <= a.j_max; ++j) {
     // ---- forward map (pipg.hpp:234-245): products first, then the scale 1/sigma
+    if constexpr (kCluster) {
+      if (j > 1) bx.recv_next(j - 2);  // rank 1's first node of trip j-1 ("next" phase j-2)
+    }
     double v[kW];
     load_node_vectors(xs_k, us_k, v);
     double s[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       double pa, pm, pp;
-      row_products(aop, v, r, pa, pm, pp);
+      row_products(aop, OpTail<0>{}, v, r, pa, pm, pp);
       double t = pa + -xs_k[kXS + kR * g + r];
       t += pm;
       t += pp;
@@ -406,6 +535,7 @@ power_fast_kernel(PowerArgs a) {
     }
     const double dy = xs_k[kXS + 14] - v[14];
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+      if constexpr (kCluster) bx.recv_norm(j - 1);
       const double sigma_star = sqrt(norm_sq((j - 1) & 1));
       if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         sigma = 0.0;
@@ -430,13 +560,13 @@ power_fast_kernel(PowerArgs a) {
     const double th = ival ? dy / sigma : 0.0;
     if (g == 4) th_k[0] = th;
     if (push_prev) {  // the same values into rank 1's guard entries for interval -1
-      double* rphi = in_cta(sm + L.phi - kNX + kR * g, 1);
+      const unsigned rphi = partner_u32(sm + L.phi - kNX + kR * g, 1);
 #pragma unroll
-      for (int r = 0; r < kR; ++r) rphi[r] = phi[r];
-      if (g == 4) *in_cta(sm + L.theta - 1, 1) = th;
+      for (int r = 0; r < kR; ++r) push_f64(rphi + 8u * r, phi[r], bx.box(kBoxPrev));
+      if (g == 4) push_f64(partner_u32(sm + L.theta - 1, 1), th, bx.box(kBoxPrev));
     }
-    store_partials(aop, phi, slot);
-    if (push_prev) push_bp_partials(slot, in_cta(part - kG * kPS + g * kPS, 1));
+    store_partials(aop, OpTail<0>{}, phi, slot);
+    if (push_prev) push_bp_partials(slot, partner_u32(part - kG * kPS + g * kPS, 1), bx.box(kBoxPrev));
     // vc+ = phi, vc- = -phi and their share of the norm (pipg.hpp:268-279)
     double acc_d = 0.0;
 #pragma unroll
@@ -446,7 +576,8 @@ power_fast_kernel(PowerArgs a) {
       acc_d += phi[r] * phi[r];
       acc_d += phi[r] * phi[r];
     }
-    phase_barrier();
+    __syncthreads();
+    if constexpr (kCluster) bx.recv_prev(j - 1);  // rank 0's last interval of this trip
     // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
     double sx[kR];
 #pragma unroll
@@ -462,15 +593,15 @@ power_fast_kernel(PowerArgs a) {
         t += th_k[-1];
       }
       xs_k[kR * g + r] = t;
-      if (push_next) *in_cta(sm + L.xs + cut.half * kXS + kR * g + r, 0) = t;
+      if (push_next) push_f64(partner_u32(sm + L.xs + cut.half * kXS + kR * g + r, 0), t, bx.box(kBoxNext));
       acc_x += t * t;
     }
     us_k[g] = su0;
     us_k[ju1] = su1;
     if (push_next) {
-      double* ru = in_cta(sm + L.us + cut.half * kUS, 0);
-      ru[g] = su0;
-      if (g < 2) ru[g + 5] = su1;
+      const unsigned ru = partner_u32(sm + L.us + cut.half * kUS, 0);
+      push_f64(ru + 8u * g, su0, bx.box(kBoxNext));
+      if (g < 2) push_f64(ru + 8u * (g + 5), su1, bx.box(kBoxNext));
     }
     double acc_u = su0 * su0;
     acc_u += g < 2 ? su1 * su1 : 0.0;
@@ -478,11 +609,20 @@ power_fast_kernel(PowerArgs a) {
     acc = warp_sum(acc);
     if (lane == 0) {
       red[(j & 1) * kFastWarps + warp] = acc;
-      if constexpr (kCluster) *in_cta(redp + (j & 1) * kFastWarps + warp, cut.rank ^ 1) = acc;
+      if constexpr (kCluster)
+        push_f64(partner_u32(redp + (j & 1) * kFastWarps + warp, cut.rank ^ 1), acc, bx.norm_box(j));
     }
-    phase_barrier();
+    __syncthreads();
   }
-  if (!done) sigma = sqrt(norm_sq(a.j_max & 1));  // j_max trips without meeting the tolerance
+  if (!done) {  // j_max trips without meeting the tolerance
+    if constexpr (kCluster) {
+      if (a.j_max >= 1) {  // what the partner sent in the last trip is still on its way
+        bx.recv_next(a.j_max - 1);
+        bx.recv_norm(a.j_max);
+      }
+    }
+    sigma = sqrt(norm_sq(a.j_max & 1));
+  }
   if (tid == 0 && cut.rank == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sigma;
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
@@ -513,8 +653,7 @@ pipg_fast_kernel(PipgArgs a) {
   constexpr FastLayout L = fast_layout<kCap>(true);
   constexpr SnapLayout S = snap_layout<kCap>();
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
-  // in a cluster: both CTAs are running and have cleared their memory before any remote store
-  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
+  const Boxes bx = open_boxes<kCluster>(sm + L.red, cut, tid, warp, nwarps);
   double* xr_k = sm + L.xs + kc * kXS;   // reflections 2*cur - ex (pipg.hpp:436-443); k+1 at +kXS
   double* ur_k = sm + L.us + kc * kUS;
   double* phx_k = sm + L.phi + kc * kNX + kR * g;  // extrapolated dynamics dual; k-1 at -kNX
@@ -538,9 +677,6 @@ pipg_fast_kernel(PipgArgs a) {
   // guard entries, the first node of rank 1 feeds rank 0's "next node" entries
   const bool push_prev = kCluster && cut.rank == 0 && k == cut.half - 1;
   const bool push_next = kCluster && cut.rank == 1 && k == 0 && node;
-  auto phase_barrier = [&]() {
-    if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
-  };
 
   // this CTA's share of the instance-major global arrays
   const size_t gx = ((size_t)b * n + cut.node0) * kNX, gu = ((size_t)b * n + cut.node0) * kNU;
@@ -582,19 +718,22 @@ pipg_fast_kernel(PipgArgs a) {
 #pragma unroll
     for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
   if (ival) load_rows(a.sp, b, m, kg, g, aop);
+  constexpr int kSpill = kCluster ? kPipgClusterSpill : 0;
+  park_tail<kSpill>(aop, sm + L.opx + tid, T);
+  const OpTail<kSpill> tail{sm + L.opx + tid, T};
   __syncthreads();
   auto publish_duals = [&](const double (&phe)[kR], double the) {  // extrapolated duals + partial sums
 #pragma unroll
     for (int r = 0; r < kR; ++r) phx_k[r] = phe[r];
     if (g == 4) thx_k[0] = the;
     if (push_prev) {
-      double* rphx = in_cta(sm + L.phi - kNX + kR * g, 1);
+      const unsigned rphx = partner_u32(sm + L.phi - kNX + kR * g, 1);
 #pragma unroll
-      for (int r = 0; r < kR; ++r) rphx[r] = phe[r];
-      if (g == 4) *in_cta(sm + L.theta - 1, 1) = the;
+      for (int r = 0; r < kR; ++r) push_f64(rphx + 8u * r, phe[r], bx.box(kBoxPrev));
+      if (g == 4) push_f64(partner_u32(sm + L.theta - 1, 1), the, bx.box(kBoxPrev));
     }
-    store_partials(aop, phe, slot);
-    if (push_prev) push_bp_partials(slot, in_cta(part - kG * kPS + g * kPS, 1));
+    store_partials(aop, tail, phe, slot);
+    if (push_prev) push_bp_partials(slot, partner_u32(part - kG * kPS + g * kPS, 1), bx.box(kBoxPrev));
   };
 
   // boundary rows of this thread (pipg.hpp:408-413): bit r set when row 3g+r is assigned
@@ -637,7 +776,9 @@ pipg_fast_kernel(PipgArgs a) {
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
   const double one_m_rho = 1.0 - a.rho;
-  if constexpr (kCluster) cg::this_cluster().sync(); else __syncthreads();
+  __syncthreads();
+  if constexpr (kCluster) bx.recv_prev(0);  // "previous interval" mailbox: phase j = after iteration j (0: warm start)
+  int iter_no = 0;                          // iteration the lambda below is running
 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into the
   // snapshot `snap` (threads without a node / interval write scratch entries).
@@ -677,7 +818,7 @@ pipg_fast_kernel(PipgArgs a) {
       xn = (fix_bits & (1 << r)) ? fv[r] : xn;
       const double xrf = fma(2.0, xn, -x0);
       xr_k[i] = xrf;
-      if (push_next) *in_cta(sm + L.xs + cut.half * kXS + i, 0) = xrf;
+      if (push_next) push_f64(partner_u32(sm + L.xs + cut.half * kXS + i, 0), xrf, bx.box(kBoxNext));
       if (kStore) snap[S.x + kc * kNX + i] = xn;
       xe[r] = one_m_rho * x0 + a.rho * xn;  // extrapolation, pipg.hpp:461-467
     }
@@ -692,13 +833,15 @@ pipg_fast_kernel(PipgArgs a) {
       un = (lo[q] < cl) ? cl : lo[q];
       const double urf = fma(2.0, un, -u0);
       ur_k[ju] = urf;
-      if (push_next && (q == 0 || g < 2)) *in_cta(sm + L.us + cut.half * kUS + ju, 0) = urf;
+      if (push_next && (q == 0 || g < 2))
+        push_f64(partner_u32(sm + L.us + cut.half * kUS + ju, 0), urf, bx.box(kBoxNext));
       if (kStore) {
         if (q == 0 || g < 2) snap[S.u + kc * kNU + ju] = un;
       }
       ue[q] = one_m_rho * u0 + a.rho * un;
     }
-    phase_barrier();
+    __syncthreads();
+    if constexpr (kCluster) bx.recv_next(iter_no - 1);  // rank 1's first node of this iteration
 
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
     //      extrapolation of the dual groups (:468-472) and the partial sums of H^T phi_ex for
@@ -709,7 +852,7 @@ pipg_fast_kernel(PipgArgs a) {
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         double pa, pm, pp;
-        row_products(aop, v, r, pa, pm, pp);
+        row_products(aop, tail, v, r, pa, pm, pp);
         double resid = pa + -xr_k[kXS + kR * g + r];
         resid += pm;
         resid += pp;
@@ -749,6 +892,7 @@ pipg_fast_kernel(PipgArgs a) {
     // checks (a converged exit returns them), and on the last iteration
     const bool keep = to_check <= 1 || j == a.j_max;
     if (check) to_check = a.j_check;
+    iter_no = j;
     if (keep) {
       cur_set ^= 1;
       iteration(std::true_type{}, snap0 + cur_set * S.total);
@@ -756,7 +900,8 @@ pipg_fast_kernel(PipgArgs a) {
       iteration(std::false_type{}, nullptr);
     }
     iters = j;
-    phase_barrier();
+    __syncthreads();
+    if constexpr (kCluster) bx.recv_prev(j);  // rank 0's last interval of this iteration
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
       const double* cur = snap0 + cur_set * S.total;
       const double* prev = snap0 + (cur_set ^ 1) * S.total;

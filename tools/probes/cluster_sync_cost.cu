@@ -28,7 +28,13 @@ __global__ void __launch_bounds__(256, 1) probe(long long* out, int iters, int n
   long long t0 = clock64();
   double v = tid;
   for (int i = 0; i < iters; ++i) {
-    if (tid < nstores) rbuf[256 + tid] = v;  // boundary values pushed to the partner
+    if (kMode == 5) {
+      if (tid < nstores)
+        asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                         remote(saddr(&buf[256 + tid]), rank ^ 1)),
+                     "d"(v), "r"(remote(saddr(&bar[1]), rank ^ 1))
+                     : "memory");
+    } else if (tid < nstores) rbuf[256 + tid] = v;  // boundary values pushed to the partner
     if (kMode == 0) {
       cg::this_cluster().sync();
     } else if (kMode == 1) {
@@ -59,6 +65,21 @@ __global__ void __launch_bounds__(256, 1) probe(long long* out, int iters, int n
           asm volatile(
               "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
               : "=r"(ok) : "r"(saddr(&bar[0])), "r"((unsigned)(i & 1)) : "memory");
+        } while (!ok);
+      }
+      __syncthreads();
+    } else if (kMode == 5) {
+      // no cluster barrier at all: the pushes themselves are asynchronous stores that complete
+      // transaction bytes on the partner's mbarrier; the consumer arms it and waits (one warp)
+      __syncthreads();
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&bar[1])), "r"(nstores * 8) : "memory");
+      if (tid < 32) {
+        unsigned ok;
+        do {
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(ok) : "r"(saddr(&bar[1])), "r"((unsigned)(i & 1)) : "memory");
         } while (!ok);
       }
       __syncthreads();
@@ -95,6 +116,7 @@ int main() {
     run<1>("barrier.cluster arrive.relaxed + wait", ns);
     run<3>("syncthreads + remote mbarrier arrive, all wait", ns);
     run<4>("syncthreads + remote mbarrier, 1 warp waits", ns);
+    if (ns > 0) run<5>("st.async complete_tx pushes, 1 warp waits", ns);
   }
   return 0;
 }

@@ -214,7 +214,8 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h);
  *   FAST_SPLIT register-resident kernels with every instance of 4..50 nodes shared by a 2-CTA
  *              cluster of 128-thread CTAs, two CTAs (halves of different instances) resident per
  *              SM; other node counts run as under AUTO.  Experimental: on B200 it is slower
- *              than AUTO (the cluster barriers cost more than the overlap gains). */
+ *              than AUTO (the flight time of the boundary values costs more than the overlap
+ *              gains). */
 #define PTOPT_SOLVER_AUTO 0
 #define PTOPT_SOLVER_GENERIC 1
 #define PTOPT_SOLVER_FAST_SPLIT 2

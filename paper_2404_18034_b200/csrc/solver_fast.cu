@@ -577,13 +577,16 @@ power_fast_kernel(PowerArgs a) {
       acc_d += phi[r] * phi[r];
     }
     __syncthreads();
-    if constexpr (kCluster) bx.recv_prev(j - 1);  // rank 0's last interval of this trip
-    // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner
+    // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner.  The sums
+    //      over the thread's own interval come first: in a cluster they hide part of the flight
+    //      time of the partner's boundary values, which only the previous-interval terms need.
     double sx[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
-    const double su0 = column_sum(part_k, 15 + 3 * g) + column_sum(part_k - kG * kPS, 17 + 3 * g);
-    const double su1 = column_sum(part_k, 16 + 3 * g) + column_sum(part_k - kG * kPS, 22 + 3 * g);
+    const double su0_own = column_sum(part_k, 15 + 3 * g), su1_own = column_sum(part_k, 16 + 3 * g);
+    if constexpr (kCluster) bx.recv_prev(j - 1);  // rank 0's last interval of this trip
+    const double su0 = su0_own + column_sum(part_k - kG * kPS, 17 + 3 * g);
+    const double su1 = su1_own + column_sum(part_k - kG * kPS, 22 + 3 * g);
     double acc_x = 0.0;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
@@ -777,8 +780,9 @@ pipg_fast_kernel(PipgArgs a) {
   const double beta = a.omega * alpha;
   const double one_m_rho = 1.0 - a.rho;
   __syncthreads();
-  if constexpr (kCluster) bx.recv_prev(0);  // "previous interval" mailbox: phase j = after iteration j (0: warm start)
-  int iter_no = 0;                          // iteration the lambda below is running
+  // "previous interval" mailbox: phase j = what rank 0 sends after iteration j (0: the warm start);
+  // it is received inside the next primal step, or after the loop
+  int iter_no = 0;  // iteration the lambda below is running
 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into the
   // snapshot `snap` (threads without a node / interval write scratch entries).
@@ -788,6 +792,16 @@ pipg_fast_kernel(PipgArgs a) {
     //      terms that do not need the partial sums are gathered first so that the dependent
     //      chain behind the shared-memory loads stays short.
     double base[kR], fv[kR], sx[kR];
+    double su[2], lo[2], hi[2];
+    if constexpr (kCluster) {
+      // the sums over the thread's own interval first: they hide part of the flight time of the
+      // partner's boundary values, which only the previous-interval terms below need
+#pragma unroll
+      for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
+      bx.recv_prev(iter_no - 1);  // rank 0's last interval after iteration iter_no - 1 (0: warm start)
+    }
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const int i = kR * g + r;
@@ -798,16 +812,18 @@ pipg_fast_kernel(PipgArgs a) {
       if (r == kR - 1 && g == 4) t += thx_k[-1] - thx_k[0];
       base[r] = t;
     }
+    if constexpr (!kCluster) {
 #pragma unroll
-    for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
-    double su[2], lo[2], hi[2];
+      for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
+    }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const double2 bq = q == 0 ? *bnd0 : *bnd1;
       lo[q] = bq.x;
       hi[q] = bq.y;
-      su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g) +
-              column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+      const double prev = column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
+      if constexpr (kCluster) su[q] += prev;
+      else su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g) + prev;
     }
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
@@ -901,7 +917,6 @@ pipg_fast_kernel(PipgArgs a) {
     }
     iters = j;
     __syncthreads();
-    if constexpr (kCluster) bx.recv_prev(j);  // rank 0's last interval of this iteration
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
       const double* cur = snap0 + cur_set * S.total;
       const double* prev = snap0 + (cur_set ^ 1) * S.total;
@@ -973,6 +988,7 @@ pipg_fast_kernel(PipgArgs a) {
     }
   }
 
+  if constexpr (kCluster) bx.recv_prev(iters);  // what rank 0 sent after the last iteration
   if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
     if (tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSolverDiverged;

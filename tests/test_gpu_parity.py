@@ -95,6 +95,32 @@ def test_linearize_batch1024_n50_subset_parity(ptor):
     assert np.abs(lin - out["x_end"][:, k]).max() < 1e-11
 
 
+def test_linearize_chunked_stage_records():
+    """Batches whose stage records would exceed PTOPT_STAGE_BYTES_MAX run the state / column passes
+    in chunks that reuse the record buffer (e.g. 8192 x N=100 per GPU in BASELINE config 5).  A cap
+    of 3 record tiles forces 4 chunks for 23 x 14 intervals; blocks, failure codes (one failing
+    instance inside a chunk) and a short SCP solve must be bit-identical to the unchunked run."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    tile_bytes = 32 * 64 * 84 * 8
+
+    def digest(env_extra):
+        env = dict(os.environ, **env_extra)
+        out = subprocess.run([sys.executable, str(root / "tools" / "chunk_probe.py")], cwd=str(root), env=env,
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr
+        return [l for l in out.stdout.splitlines() if l.startswith("digest")][0]
+
+    whole = digest({})
+    chunked = digest({"PTOPT_STAGE_BYTES_MAX": str(3 * tile_bytes)})
+    assert "status [0, 0, 0, 0, 0, 4," in whole  # instance 5 fails with the mass code
+    assert whole == chunked
+
+
 def test_linearize_failure_codes_match_oracle(solver15, ptor):
     sc, s = solver15
     d = sc.problem_desc()

@@ -157,6 +157,62 @@ def workload_config(args, world):
                   "the 126 MB L2; inputs are re-uploaded/re-initialised every step"}
 
 
+def other_configs(device_index, fp64_peak):
+    """Informational timings of the other BASELINE configs' shapes on this GPU (rank 0 only, after
+    the headline measurement; they are parity-test cases, not the metric): config 2 = exact
+    discretization only, 1024 x N=50, device-resident; config 5 shape = full SCP solves at N=100
+    (two waves of 2-CTA clusters)."""
+    import numpy as np
+    import torch
+
+    from paper_2404_18034_b200 import scenario
+    from paper_2404_18034_b200.binding import Solver
+
+    dev = torch.device("cuda", device_index)
+    out = {}
+    # ---- config 2
+    B, n = 1024, 50
+    sc = scenario.default_scenario(n)
+    small = scenario.make_batch(sc, range(64))
+    idx = np.arange(B) % 64
+    x = torch.from_numpy(small["x_guess"][idx]).to(dev)
+    u = torch.from_numpy(small["u_guess"][idx]).to(dev)
+    m = n - 1
+    A = torch.empty((B, m, NX, NX), dtype=torch.float64, device=dev)
+    Bm = torch.empty((B, m, NX, NU), dtype=torch.float64, device=dev)
+    Bp = torch.empty_like(Bm)
+    w = torch.empty((B, m, NX), dtype=torch.float64, device=dev)
+    xe = torch.empty_like(w)
+    stream = torch.cuda.Stream(device=dev)
+    with Solver(sc.problem_desc(), device=device_index, stream=stream) as s, torch.cuda.stream(stream):
+        for _ in range(3):
+            s.linearize_all_dev(x, u, A, Bm, Bp, w, xe)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            s.linearize_all_dev(x, u, A, Bm, Bp, w, xe)
+        e1.record(stream)
+        stream.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+    disc_flop, _ = algorithmic_flops(n)
+    tf = B * disc_flop / (ms * 1e-3) * 1e-12
+    out["config2_discretization_1024xN50"] = {"ms_per_call": ms, "algorithmic_tflops": tf, "frac_fp64_peak": tf / fp64_peak}
+    # ---- config 5 shape
+    n, B = 100, 296
+    sc = scenario.default_scenario(n)
+    batch = scenario.make_batch(sc, range(B))
+    with Solver(sc.problem_desc(), device=device_index) as s:
+        s.scp_solve(batch["init_state"][:4], batch["x_guess"][:4], batch["u_guess"][:4], batch["rng_seed"][:4])
+        res = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+        st = s.scp_stage_times()
+    out["config5_shape_296xN100"] = {
+        "solves_per_s": B / (st["graph_total"] * 1e-3), "graph_ms": st["graph_total"],
+        "power_trips_mean": float(res["power_trips"].sum(axis=1).mean()),
+        "what": "full SCP solves at N=100 on one GPU (2-CTA cluster per instance, two waves), device time of "
+                "the graph"}
+    return out
+
+
 # --------------------------------------------------------------------------- own arm
 def run_own_arm(args):
     import numpy as np
@@ -371,6 +427,8 @@ def run_own_arm(args):
                               for k in ("linearize", "power_iteration", "pipg")},
             },
         }
+        if not args.no_other_configs:
+            line["other_configs"] = other_configs(local_rank, fp64_peak)
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
             inst = args.cpu_instances or cores
@@ -399,6 +457,8 @@ def main():
     ap.add_argument("--cpu-instances", type=int, default=0,
                     help="instances in the CPU sample (default: one per host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the informational timings of the other BASELINE config shapes")
     ap.add_argument("--latency-runs", type=int, default=5,
                     help="batch-of-one solves timed for the p50 single-solve latency (0 = skip)")
     args = ap.parse_args()

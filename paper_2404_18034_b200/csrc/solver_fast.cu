@@ -429,14 +429,20 @@ power_fast_kernel(PowerArgs a) {
   // guard entries, the first node of rank 1 feeds rank 0's "next node" entries
   const bool push_prev = kCluster && cut.rank == 0 && k == cut.half - 1;
   const bool push_next = kCluster && cut.rank == 1 && k == 0 && node;
-  auto norm_sq = [&](int parity) {  // sum of both CTAs' partial sums, rank 0's first
-    double own = 0.0, other = 0.0;
-#pragma unroll
-    for (int w = 0; w < kFastWarps; ++w) {
-      own += w < nwarps ? red[parity * kFastWarps + w] : 0.0;
-      if constexpr (kCluster) other += w < nwarps ? redp[parity * kFastWarps + w] : 0.0;
+  // Sum of the warps' shares of one parity (slots of warps that do not exist stay zero), as a
+  // pairwise tree: three dependent additions instead of seven on every thread's critical path.
+  auto share_sum = [&](const double* shares) {
+    static_assert(kFastWarps == 8, "tree below");
+    const double2* p = reinterpret_cast<const double2*>(shares);
+    const double2 a = p[0], b = p[1], c = p[2], d = p[3];
+    return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (d.x + d.y));
+  };
+  auto norm_sq = [&](int parity) {  // both CTAs' shares, rank 0's first
+    const double own = share_sum(red + parity * kFastWarps);
+    if constexpr (kCluster) {
+      const double other = share_sum(redp + parity * kFastWarps);
+      return cut.rank == 0 ? own + other : other + own;
     }
-    if constexpr (kCluster) return cut.rank == 0 ? own + other : other + own;
     return own;
   };
 
@@ -507,6 +513,9 @@ power_fast_kernel(PowerArgs a) {
     if constexpr (kCluster) cg::this_cluster().sync();  // the partner may still be reading
     return;
   }
+  // sigma and 1 / sigma (pipg.hpp:243 scales by 1.0 / sigma) from the same squared norm: rsqrt
+  // runs beside sqrt instead of a division chain behind it (1 ulp)
+  double inv = rsqrt(sigma);
   sigma = sqrt(sigma);
 
   // The norm of trip j-1 is reduced while trip j's forward products are already running: the
@@ -526,17 +535,16 @@ power_fast_kernel(PowerArgs a) {
     for (int r = 0; r < kR; ++r) {
       double pa, pm, pp;
       row_products(aop, OpTail<0>{}, v, r, pa, pm, pp);
-      double t = pa + -xs_k[kXS + kR * g + r];
-      t += pm;
-      t += pp;
-      t += vcp[r];
-      t += -1.0 * vcn[r];
-      s[r] = t;
+      // pipg.hpp:235-241 adds the six terms one after the other; paired here (three dependent
+      // additions instead of five)
+      s[r] = ((pa - xs_k[kXS + kR * g + r]) + (pm + pp)) + (vcp[r] - vcn[r]);
     }
     const double dy = xs_k[kXS + 14] - v[14];
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
       if constexpr (kCluster) bx.recv_norm(j - 1);
-      const double sigma_star = sqrt(norm_sq((j - 1) & 1));
+      const double ss = norm_sq((j - 1) & 1);
+      const double sigma_star = sqrt(ss);
+      inv = rsqrt(ss);
       if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         sigma = 0.0;
         done = true;
@@ -550,14 +558,15 @@ power_fast_kernel(PowerArgs a) {
       }
     }
     trips = j;
-    const double inv = 1.0 / sigma;
     double phi[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       phi[r] = ival ? s[r] * inv : 0.0;
       phi_k[r] = phi[r];
     }
-    const double th = ival ? dy / sigma : 0.0;
+    // pipg.hpp:244 divides by sigma; the reciprocal is already there (1 ulp, and one division
+    // chain less on every thread's critical path)
+    const double th = ival ? dy * inv : 0.0;
     if (g == 4) th_k[0] = th;
     if (push_prev) {  // the same values into rank 1's guard entries for interval -1
       const unsigned rphi = partner_u32(sm + L.phi - kNX + kR * g, 1);

@@ -447,10 +447,10 @@ power_fast_kernel(PowerArgs a) {
   };
 
   double aop[kR][kW];
-  double vcp[kR], vcn[kR];
+  double vcd[kR];  // vc+ - vc-: the only combination of the two groups the forward map uses
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
-    vcp[r] = vcn[r] = 0.0;
+    vcd[r] = 0.0;
 #pragma unroll
     for (int j = 0; j < kW; ++j) aop[r][j] = 0.0;
   }
@@ -483,10 +483,10 @@ power_fast_kernel(PowerArgs a) {
     const double* sn = a.seed_vcn + ((size_t)b * m + kg) * kNX;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-      vcp[r] = sp[kR * g + r];
-      vcn[r] = sn[kR * g + r];
-      acc += vcp[r] * vcp[r];
-      acc += vcn[r] * vcn[r];
+      const double vp = sp[kR * g + r], vn = sn[kR * g + r];
+      vcd[r] = vp - vn;
+      acc += vp * vp;
+      acc += vn * vn;
     }
   }
   if constexpr (kCluster) {  // rank 0's "next node" is the partner's first node
@@ -537,7 +537,7 @@ power_fast_kernel(PowerArgs a) {
       row_products(aop, OpTail<0>{}, v, r, pa, pm, pp);
       // pipg.hpp:235-241 adds the six terms one after the other; paired here (three dependent
       // additions instead of five)
-      s[r] = ((pa - xs_k[kXS + kR * g + r]) + (pm + pp)) + (vcp[r] - vcn[r]);
+      s[r] = ((pa - xs_k[kXS + kR * g + r]) + (pm + pp)) + vcd[r];
     }
     const double dy = xs_k[kXS + 14] - v[14];
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
@@ -576,14 +576,13 @@ power_fast_kernel(PowerArgs a) {
     }
     store_partials(aop, OpTail<0>{}, phi, slot);
     if (push_prev) push_bp_partials(slot, partner_u32(part - kG * kPS + g * kPS, 1), bx.box(kBoxPrev));
-    // vc+ = phi, vc- = -phi and their share of the norm (pipg.hpp:268-279)
+    // vc+ = phi, vc- = -phi (so vc+ - vc- = 2 phi, exactly) and their share of the norm,
+    // phi^2 + phi^2 (pipg.hpp:268-279)
     double acc_d = 0.0;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-      vcp[r] = phi[r];
-      vcn[r] = -phi[r];
-      acc_d += phi[r] * phi[r];
-      acc_d += phi[r] * phi[r];
+      vcd[r] = 2.0 * phi[r];
+      acc_d = fma(vcd[r], phi[r], acc_d);
     }
     __syncthreads();
     // ---- adjoint map (pipg.hpp:247-275): every primal entry is assembled by its owner.  The sums

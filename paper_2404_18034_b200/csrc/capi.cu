@@ -236,8 +236,8 @@ bool use_fast_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_p
 
 /// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
 /// handle asks for it (and the node count allows it).  Measured on B200 it loses to one CTA per
-/// instance both in throughput (462 vs 617 solves/s at N=50) and in single-solve latency
-/// (255 vs 229 ms): the flight time of the boundary values is paid twice per iteration.
+/// instance both in throughput (493 vs 655 solves/s at N=50) and in single-solve latency
+/// (250 vs 216 ms): the flight time of the boundary values is paid twice per iteration.
 bool use_split_solver(const ptopt_cuda_handle* h, int /*batch*/) {
   return h->solver_path == PTOPT_SOLVER_FAST_SPLIT;
 }

@@ -387,6 +387,17 @@ int ptopt_cuda_dense_audit_batch_dev(ptopt_cuda_handle* h, int batch, int subste
                                      double* interval_y_increase, int32_t* status,
                                      int32_t* fail_index);
 
+/* The same audit with its sample sink (the `samples` argument of dense_violation_audit,
+ * discretizer.hpp:253, 262-276; AuditSample :236-240): samples
+ * [B][M][substeps+1][PTOPT_AUDIT_SAMPLE_DOUBLES] = {interval, tau, g[9], g_max}, in the
+ * reference's order (interval by interval, the node sample first, then one per substep).
+ * Samples of an instance whose propagation fails are unspecified from the failing interval on. */
+#define PTOPT_AUDIT_SAMPLE_DOUBLES 12
+int ptopt_cuda_dense_audit_samples_batch(ptopt_cuda_handle* h, int batch, int substeps, const double* x,
+                                         const double* u, double* samples, double* max_pointwise_g,
+                                         double* interval_y_increase, int32_t* status,
+                                         int32_t* fail_index);
+
 /* mc::run_batch (proj/include/ptopt/montecarlo.hpp:140-175) for run ids
  * first_run_id .. first_run_id+batch-1, everything on the device: generation ->
  * scp_solve -> audit -> records.  Only the records (and, when x_out/u_out are

@@ -783,7 +783,7 @@ int ptor_linearize_all(const ptopt_problem_desc* d, const double* tau, const dou
 /* propagate_state with the audit's sample sink folded in, :153-187 + :262-277 */
 static int propagate_state_audit(const ptor_model* m, const double* x_k, const double* u_k,
                                  const double* u_k1, double tau_k, double tau_k1, int steps,
-                                 double* x_out, double* max_g) {
+                                 double* x_out, double* max_g, int interval, double* samples) {
   const int nx = m->state_dim + 1, nu = m->control_dim + 1;
   double x[PTOR_MAX_X], k1[PTOR_MAX_X], k2[PTOR_MAX_X], k3[PTOR_MAX_X], k4[PTOR_MAX_X],
       tmp[PTOR_MAX_X], uu[PTOR_MAX_U], g[PTOR_MAX_G];
@@ -798,6 +798,13 @@ static int propagate_state_audit(const ptor_model* m, const double* x_k, const d
     m->path_ineq(m->ctx, (xs_), uu, g);                                           \
     for (int i_ = 0; i_ < m->ineq_dim; ++i_) gmax = dmax(gmax, g[i_]);            \
     *max_g = dmax(*max_g, gmax);                                                  \
+    if (samples) { /* AuditSample{interval, tau, g, g_max}, :262-276 */           \
+      samples[0] = (double)interval;                                              \
+      samples[1] = (tau_);                                                        \
+      for (int i_ = 0; i_ < m->ineq_dim; ++i_) samples[2 + i_] = g[i_];           \
+      samples[2 + m->ineq_dim] = gmax;                                            \
+      samples += PTOR_SAMPLE_DOUBLES;                                             \
+    }                                                                             \
   } while (0)
 #define RATE(tau_, xs_, out_)                                                     \
   do {                                                                            \
@@ -832,14 +839,15 @@ static int propagate_state_audit(const ptor_model* m, const double* x_k, const d
 
 static int dense_audit_with(const ptor_model* m, const double* grid, int n, const double* x,
                             const double* u, int substeps, double* max_pointwise_g,
-                            double* total_y_increase, double* interval_y_increase) {
+                            double* total_y_increase, double* interval_y_increase, double* samples) {
   /* :249-285 */
   double total = 0.0, gmax = -INFINITY;
   if (substeps < 1) return -1;
   for (int k = 0; k < n - 1; ++k) {
     double xe[PTOR_MAX_X], dy;
     int rc = propagate_state_audit(m, x + k * NX, u + k * NU, u + (k + 1) * NU, grid[k],
-                                   grid[k + 1], substeps, xe, &gmax);
+                                   grid[k + 1], substeps, xe, &gmax, k,
+                                   samples ? samples + (size_t)k * (substeps + 1) * PTOR_SAMPLE_DOUBLES : NULL);
     if (rc) return rc;
     dy = xe[NX - 1] - x[k * NX + NX - 1];
     if (interval_y_increase) interval_y_increase[k] = dy;
@@ -861,7 +869,23 @@ int ptor_dense_audit(const ptopt_problem_desc* d, const double* tau, const doubl
   m = ptor_rocket_model(&r);
   grid = grid_nodes(d, tau);
   rc = dense_audit_with(&m, grid, d->nodes, x, u, substeps, max_pointwise_g, total_y_increase,
-                        interval_y_increase);
+                        interval_y_increase, NULL);
+  free(grid);
+  return rc;
+}
+
+int ptor_dense_audit_samples(const ptopt_problem_desc* d, const double* tau, const double* x,
+                             const double* u, int substeps, double* max_pointwise_g,
+                             double* total_y_increase, double* interval_y_increase, double* samples) {
+  ptor_rocket r;
+  ptor_model m;
+  double* grid;
+  int rc;
+  if ((rc = ptor_rocket_init(&r, &d->vehicle))) return rc;
+  m = ptor_rocket_model(&r);
+  grid = grid_nodes(d, tau);
+  rc = dense_audit_with(&m, grid, d->nodes, x, u, substeps, max_pointwise_g, total_y_increase,
+                        interval_y_increase, samples);
   free(grid);
   return rc;
 }

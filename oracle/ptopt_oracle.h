@@ -79,6 +79,12 @@ int ptor_linearize_all(const ptopt_problem_desc* d, const double* tau, const dou
 int ptor_dense_audit(const ptopt_problem_desc* d, const double* tau, const double* x,
                      const double* u, int substeps, double* max_pointwise_g,
                      double* total_y_increase, double* interval_y_increase);
+/* The same with the per-sample records of dense_violation_audit (discretizer.hpp:236-240,
+ * 262-276): samples [nodes-1][substeps+1][PTOR_SAMPLE_DOUBLES] = {interval, tau, g[9], g_max}. */
+#define PTOR_SAMPLE_DOUBLES 12
+int ptor_dense_audit_samples(const ptopt_problem_desc* d, const double* tau, const double* x,
+                             const double* u, int substeps, double* max_pointwise_g,
+                             double* total_y_increase, double* interval_y_increase, double* samples);
 
 /* SCP glue */
 int ptor_assemble(const ptopt_problem_desc* d, const double* tau, const double* init_state,

@@ -448,6 +448,31 @@ int ptref_dense_audit(const ptopt_problem_desc* d, const double* tau, const doub
   });
 }
 
+/// dense_violation_audit with its sample sink (discretizer.hpp:236-240, 262-276):
+/// samples [nodes-1][substeps+1][12] = {interval, tau, g[9], g_max}.
+int ptref_dense_audit_samples(const ptopt_problem_desc* d, const double* tau, const double* x,
+                              const double* u, int substeps, double* max_pointwise_g,
+                              double* total_y_increase, double* interval_y_increase, double* samples) {
+  return guarded(nullptr, [&] {
+    const rocket::Rocket6DoF model(vehicle_of(d->vehicle));
+    const Grid grid = grid_of(*d, tau);
+    const auto z = traj_of(d->nodes, x, u);
+    std::vector<AuditSample> got;
+    const auto res = dense_violation_audit(model, z, grid, substeps, &got);
+    *max_pointwise_g = res.max_pointwise_g;
+    *total_y_increase = res.total_y_increase;
+    for (std::size_t k = 0; k < res.interval_y_increase.size(); ++k)
+      interval_y_increase[k] = res.interval_y_increase[k];
+    for (std::size_t i = 0; i < got.size(); ++i) {
+      double* s = samples + i * 12;
+      s[0] = got[i].interval;
+      s[1] = got[i].tau;
+      for (std::size_t q = 0; q < got[i].g.size(); ++q) s[2 + q] = got[i].g[q];
+      s[11] = got[i].g_max;
+    }
+  });
+}
+
 // ---- SCP glue (scp.hpp:139-217, 239-249, 256-364) ----------------------------
 
 int ptref_assemble(const ptopt_problem_desc* d, const double* tau, const double* init_state,

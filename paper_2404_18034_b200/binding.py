@@ -32,6 +32,7 @@ EXPORTS = [
     "ptopt_cuda_scp_solve_batch", "ptopt_cuda_scp_solve_batch_dev",
     "ptopt_cuda_generate_batch", "ptopt_cuda_generate_batch_dev",
     "ptopt_cuda_dense_audit_batch", "ptopt_cuda_dense_audit_batch_dev",
+    "ptopt_cuda_dense_audit_samples_batch",
     "ptopt_cuda_run_batch",
     "ptopt_cuda_scp_stage_times", "ptopt_cuda_measure_fp64_peak",
 ]
@@ -292,6 +293,20 @@ class Solver:
         _check(self.lib.ptopt_cuda_dense_audit_batch(
             self._h, C.c_int(B), C.c_int(substeps), _hp(x), _hp(u), _hp(out["max_pointwise_g"]),
             _hp(out["interval_y_increase"]), _hp(out["status"]), _hp(out["fail_index"])))
+        return out
+
+    def dense_violation_audit_samples(self, x, u, substeps):
+        """dense_violation_audit with its sample sink: adds samples [B, M, substeps+1, 12] =
+        {interval, tau, g[9], g_max} (discretizer.hpp:236-240, 262-276)."""
+        x, u = _np(x), _np(u)
+        B, m = x.shape[0], self.nodes - 1
+        out = dict(samples=np.empty((B, m, substeps + 1, 12)), max_pointwise_g=np.empty(B),
+                   interval_y_increase=np.empty((B, m)), status=np.empty(B, np.int32),
+                   fail_index=np.empty(B, np.int32))
+        _check(self.lib.ptopt_cuda_dense_audit_samples_batch(
+            self._h, C.c_int(B), C.c_int(substeps), _hp(x), _hp(u), _hp(out["samples"]),
+            _hp(out["max_pointwise_g"]), _hp(out["interval_y_increase"]), _hp(out["status"]),
+            _hp(out["fail_index"])))
         return out
 
     def run_batch(self, batch, first_run_id, nominal_init_state, r_low, r_high, seed,

@@ -64,7 +64,7 @@ enum BufId {
   S_TRIPS, S_STATUS, S_FAILIDX, S_STAGES,
   // Monte Carlo harness
   R_QTAB, R_INIT, R_XG, R_UG, R_SEED, R_XOUT, R_UOUT, R_ITERS, R_CONV, R_FDEF, R_STATUS, R_FAILIDX,
-  R_GMAX, R_DY, R_AKEY, R_PG, R_RECORDS,
+  R_GMAX, R_DY, R_AKEY, R_PG, R_RECORDS, R_SAMPLES,
   kNumBufs
 };
 
@@ -1149,7 +1149,7 @@ int generate_dev(ptopt_cuda_handle* h, int batch, int64_t first_run_id, const do
 
 int audit_dev(ptopt_cuda_handle* h, int batch, int substeps, const double* x, const double* u,
               const int* skip, double* max_pointwise_g, double* interval_y_increase,
-              int32_t* status, int32_t* fail_index) {
+              int32_t* status, int32_t* fail_index, double* samples = nullptr) {
   if (substeps < 1)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "dense_violation_audit: substeps must be >= 1");
   const size_t B = (size_t)batch, m = (size_t)h->desc.nodes - 1;
@@ -1162,6 +1162,7 @@ int audit_dev(ptopt_cuda_handle* h, int batch, int substeps, const double* x, co
   a.x = x;
   a.u = u;
   a.skip = skip;
+  a.samples = samples;
   PT_TRY(device_out(h, R_GMAX, B * m, &a.interval_g_max));
   if (interval_y_increase) {
     a.interval_y_increase = interval_y_increase;
@@ -1252,6 +1253,42 @@ int ptopt_cuda_dense_audit_batch(ptopt_cuda_handle* h, int batch, int substeps, 
   PT_TRY(device_out(h, B_STATUS, B, &dst));
   PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
   PT_TRY(ptopt_cuda_dense_audit_batch_dev(h, batch, substeps, dx, du, dg, dy, dst, dfi));
+  PT_TRY(download(h, max_pointwise_g, dg, B));
+  PT_TRY(download(h, interval_y_increase, dy, B * m));
+  PT_TRY(download(h, status, dst, B));
+  PT_TRY(download(h, fail_index, dfi, B));
+  PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_dense_audit_samples_batch(ptopt_cuda_handle* h, int batch, int substeps, const double* x,
+                                         const double* u, double* samples, double* max_pointwise_g,
+                                         double* interval_y_increase, int32_t* status,
+                                         int32_t* fail_index) {
+  if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (!x || !u || !samples) return fail(PTOPT_ERR_INVALID_ARGUMENT, "audit: null array");
+  if (substeps < 1)
+    return fail(PTOPT_ERR_INVALID_ARGUMENT, "dense_violation_audit: substeps must be >= 1");
+  DeviceGuard guard(h->device);
+  if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
+  const size_t B = (size_t)batch, n = (size_t)h->desc.nodes, m = n - 1;
+  const size_t per_instance = m * (size_t)(substeps + 1) * kAuditSampleDoubles;
+  const double *dx, *du;
+  double *dg, *dy, *ds;
+  int *dst, *dfi;
+  PT_TRY(upload(h, B_X, x, B * n * kNX, &dx));
+  PT_TRY(upload(h, B_U, u, B * n * kNU, &du));
+  PT_TRY(device_out(h, R_PG, B, &dg));
+  PT_TRY(device_out(h, R_DY, B * m, &dy));
+  PT_TRY(device_out(h, R_SAMPLES, B * per_instance, &ds));
+  PT_TRY(device_out(h, B_STATUS, B, &dst));
+  PT_TRY(device_out(h, B_FAILIDX, B, &dfi));
+  PT_CUDA(cudaMemsetAsync(ds, 0, sizeof(double) * B * per_instance, h->stream));
+  PT_CUDA(cudaMemsetAsync(dst, 0, sizeof(int32_t) * B, h->stream));
+  PT_CUDA(cudaMemsetAsync(dfi, 0xff, sizeof(int32_t) * B, h->stream));
+  PT_TRY(audit_dev(h, batch, substeps, dx, du, nullptr, dg, dy, dst, dfi, ds));
+  PT_TRY(download(h, samples, ds, B * per_instance));
   PT_TRY(download(h, max_pointwise_g, dg, B));
   PT_TRY(download(h, interval_y_increase, dy, B * m));
   PT_TRY(download(h, status, dst, B));

@@ -179,11 +179,23 @@ __global__ void __launch_bounds__(128) audit_kernel(AuditArgs a) {
 #pragma unroll
     for (int i = 0; i < kNU; ++i) uu[i] = ll * u0[i] + lr * u1[i];
   };
-  auto record = [&](double tau, const double* xs) {  // sample callback, discretizer.hpp:262-270
+  // AuditSample records of this interval (discretizer.hpp:236-240), when the caller wants them
+  double* sample = a.samples ? a.samples + (size_t)idx * (a.substeps + 1) * kAuditSampleDoubles : nullptr;
+  auto record = [&](double tau, const double* xs) {  // sample callback, discretizer.hpp:262-276
     interp(tau);
     eval_constraints(a.model, xs, uu, g);
+    double gs = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) gmax = fmax(gmax, g[i]);
+    for (int i = 0; i < 9; ++i) gs = fmax(gs, g[i]);
+    gmax = fmax(gmax, gs);
+    if (sample) {
+      sample[0] = (double)k;
+      sample[1] = tau;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) sample[2 + i] = g[i];
+      sample[11] = gs;
+      sample += kAuditSampleDoubles;
+    }
   };
   record(tau_k, x);
   for (int step = 0; step < a.substeps && rc == kStOk; ++step) {

@@ -11,7 +11,8 @@
 //   pipg::power_iteration_custom(sp, seeds..., eps, j)    pipg.hpp:206-211
 //   pipg::pipg_custom(sp, cfg, ws)                        pipg.hpp:350-352
 //   scp_solve(pb, guess)                                  scp.hpp:256-258
-//   dense_violation_audit(model, z, grid, substeps)       discretizer.hpp:249-253
+//   dense_violation_audit(model, z, grid, substeps, &samples)  discretizer.hpp:249-253
+//   initial_guess(pb, bc)                                 rocket_problem.hpp:127-163
 //   mc::run_batch(nominal, bc, spec, batch, workers, ..)  montecarlo.hpp:140-142
 //
 // Every function is a template over its container arguments and touches them only through
@@ -390,14 +391,24 @@ RocketBlocks propagate_interval(const Model& model, const VX& x_k, const VU& u_k
   return b;
 }
 
+struct AuditSample {  // discretizer.hpp:236-240
+  int interval = 0;
+  double tau = 0.0;
+  std::vector<double> g;
+  double g_max = 0.0;
+};
+
 struct AuditResult {  // discretizer.hpp:241-245
   double max_pointwise_g = 0.0;
   double total_y_increase = 0.0;
   std::vector<double> interval_y_increase;
 };
 
-template <class Model, class Traj, class GridT>
-AuditResult dense_violation_audit(const Model& model, const Traj& z, const GridT& grid, int substeps) {
+/// dense_violation_audit (discretizer.hpp:249-285).  `samples`, when given, receives one
+/// AuditSample per node / substep in the reference's order (appended, as the reference does).
+template <class Model, class Traj, class GridT, class SampleT = AuditSample>
+AuditResult dense_violation_audit(const Model& model, const Traj& z, const GridT& grid, int substeps,
+                                  std::vector<SampleT>* samples = nullptr) {
   if (substeps < 1) throw std::invalid_argument("dense_violation_audit: substeps must be >= 1");
   const int n = static_cast<int>(grid.nodes.size());
   const ptopt_problem_desc d = detail::discretizer_desc(model.params(), n, 1);
@@ -407,9 +418,28 @@ AuditResult dense_violation_audit(const Model& model, const Traj& z, const GridT
   AuditResult r;
   r.interval_y_increase.resize(static_cast<std::size_t>(n - 1));
   int32_t status = 0, fail_index = -1;
-  detail::check_call(ptopt_cuda_dense_audit_batch(h, 1, substeps, x.data(), u.data(), &r.max_pointwise_g,
-                                                  r.interval_y_increase.data(), &status, &fail_index));
-  if (status != PTOPT_ST_OK) detail::throw_instance(status, fail_index);
+  if (samples) {
+    const std::size_t count = static_cast<std::size_t>(n - 1) * static_cast<std::size_t>(substeps + 1);
+    std::vector<double> flat(count * PTOPT_AUDIT_SAMPLE_DOUBLES);
+    detail::check_call(ptopt_cuda_dense_audit_samples_batch(h, 1, substeps, x.data(), u.data(), flat.data(),
+                                                            &r.max_pointwise_g, r.interval_y_increase.data(),
+                                                            &status, &fail_index));
+    if (status != PTOPT_ST_OK) detail::throw_instance(status, fail_index);
+    samples->reserve(samples->size() + count);
+    for (std::size_t i = 0; i < count; ++i) {
+      const double* f = &flat[i * PTOPT_AUDIT_SAMPLE_DOUBLES];
+      SampleT smp;
+      smp.interval = static_cast<int>(f[0]);
+      smp.tau = f[1];
+      smp.g.assign(f + 2, f + 2 + PTOPT_NG);
+      smp.g_max = f[2 + PTOPT_NG];
+      samples->push_back(std::move(smp));
+    }
+  } else {
+    detail::check_call(ptopt_cuda_dense_audit_batch(h, 1, substeps, x.data(), u.data(), &r.max_pointwise_g,
+                                                    r.interval_y_increase.data(), &status, &fail_index));
+    if (status != PTOPT_ST_OK) detail::throw_instance(status, fail_index);
+  }
   for (double dy : r.interval_y_increase) r.total_y_increase += dy;
   return r;
 }
@@ -937,6 +967,33 @@ inline RocketProblem make_rocket_problem(const rocket::VehicleParams& params, co
   pb.e_cost[rocket::kMass] = -1.0;  // maximise terminal mass
   pb.state_post_update = [](Vec<kNX>&) {};  // marks the quaternion hook as present
   return pb;
+}
+
+/// initial_guess (rocket_problem.hpp:127-163): straight-line state interpolation, slerp of the
+/// attitude and a gravity-cancelling thrust profile.  Evaluated by the device generator that
+/// run_batch uses (ptopt_cuda_generate_batch with a dispersion box of zero width around the
+/// initial position, which leaves it bit-for-bit unchanged), so there is one implementation.
+/// The terminal targets are the ones `pb` was built with (make_rocket_problem).
+template <class Problem, class Boundary>
+RocketTrajectory initial_guess(const Problem& pb, const Boundary& bc) {
+  const int n = static_cast<int>(pb.grid.nodes.size());
+  const ptopt_problem_desc d = detail::to_desc(pb);
+  ptopt_cuda_handle* h = detail::context(d, pb.grid.nodes);
+  const auto init = bc.initial.to_vec();
+  double nominal[kNXI];
+  for (int i = 0; i < kNXI; ++i) nominal[i] = init[i];
+  ptopt_dispersion_spec box{};
+  for (int i = 0; i < 3; ++i) box.r_low[i] = box.r_high[i] = bc.initial.r[static_cast<std::size_t>(i)];
+  std::vector<double> x(static_cast<std::size_t>(n) * kNX), u(static_cast<std::size_t>(n) * kNU);
+  double init_out[kNXI];
+  std::uint64_t seed_out = 0;
+  detail::check_call(ptopt_cuda_generate_batch(h, 1, 0, nominal, &box, init_out, x.data(), u.data(), &seed_out));
+  RocketTrajectory z(n);
+  for (int k = 0; k < n; ++k) {
+    for (int i = 0; i < kNX; ++i) z.x[static_cast<std::size_t>(k)][i] = x[static_cast<std::size_t>(k) * kNX + i];
+    for (int i = 0; i < kNU; ++i) z.u[static_cast<std::size_t>(k)][i] = u[static_cast<std::size_t>(k) * kNU + i];
+  }
+  return z;
 }
 
 namespace mc {

@@ -6,15 +6,14 @@
 //
 //   mc::aggregate(records, max_iters, wall, workers)   montecarlo.hpp:177-209
 //   node_times(z, grid)                                rocket_problem.hpp:166-176
-//   csvio::fmt / write_trajectory / write_runs / write_summary   csv.hpp:20-96
+//   csvio::fmt / write_trajectory / write_dense_audit / write_runs / write_summary   csv.hpp:20-96
 //
 // All functions are templates over the record / trajectory types and only use the member names
 // the reference's types have, so they take the reference's objects as well as this repo's.
 // Numbers are printed with "%.17g" (round-trippable), `wall_time` stays the last column of
 // runs.csv so byte comparisons can strip it (csv.hpp:66).
 //
-// Not mirrored: JSON config ingestion (config.hpp:199-375 needs nlohmann/json, which the
-// reference does not vendor) and write_dense_audit (the device audit keeps maxima, not samples).
+// The JSON configuration on the input side is in ptopt_b200_config.hpp.
 #pragma once
 
 #include <algorithm>
@@ -133,6 +132,19 @@ void trajectory_csv(std::ostream& out, const Traj& z, const GridT& grid) {
   }
 }
 
+template <class Sample>
+void dense_audit_csv(std::ostream& out, const std::vector<Sample>& samples) {
+  out << "interval,tau";
+  const std::size_t ng = samples.empty() ? 0 : samples.front().g.size();
+  for (std::size_t i = 0; i < ng; ++i) out << ",g" << (i + 1);
+  out << ",g_max\n";
+  for (const Sample& s : samples) {
+    out << s.interval << ',' << fmt(s.tau);
+    for (double g : s.g) out << ',' << fmt(g);
+    out << ',' << fmt(s.g_max) << '\n';
+  }
+}
+
 template <class Record>
 void runs_csv(std::ostream& out, const std::vector<Record>& records) {
   out << "run_id,r0_1,r0_2,r0_3,converged,scp_iterations,propellant_used,"
@@ -166,6 +178,11 @@ void summary_csv(std::ostream& out, const SummaryT& s) {
 template <class Traj, class GridT>
 void write_trajectory(const std::string& path, const Traj& z, const GridT& grid) {
   detail::write_file(path, [&](std::ostream& out) { trajectory_csv(out, z, grid); });
+}
+
+template <class Sample>
+void write_dense_audit(const std::string& path, const std::vector<Sample>& samples) {
+  detail::write_file(path, [&](std::ostream& out) { dense_audit_csv(out, samples); });
 }
 
 template <class Record>

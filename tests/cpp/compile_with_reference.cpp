@@ -32,6 +32,9 @@ double instantiate_everything(const ptopt::RocketProblem& pb, const ptopt::Rocke
   // scp.hpp:256-258, discretizer.hpp:249-253, montecarlo.hpp:140-142
   const auto res = b2::scp_solve(pb, guess);
   const auto audit = b2::dense_violation_audit(pb.model, res.iterate, pb.grid, 64);
+  std::vector<ptopt::AuditSample> ref_samples;  // the reference's own sample type
+  b2::dense_violation_audit(pb.model, res.iterate, pb.grid, 64, &ref_samples);
+  b2::csvio::write_dense_audit("/dev/null", ref_samples);
   const auto batch = b2::mc::run_batch(pb, bc, spec, 8, 4, 64, true);
   // output side (csv.hpp:34-96, montecarlo.hpp:177-209) on the reference's records / trajectory
   const std::vector<ptopt::mc::RunRecord> ref_records(2);

@@ -78,5 +78,16 @@ int main(int argc, char** argv) {
     z.u[(std::size_t)k][6] = 4.0 + value(3000 + k);  // dilation
   }
   lib::csvio::write_trajectory(dir + "/trajectory.csv", z, grid);
+
+  std::vector<lib::AuditSample> samples(7);
+  for (int i = 0; i < 7; ++i) {
+    lib::AuditSample& s = samples[(std::size_t)i];
+    s.interval = i / 3;
+    s.tau = 0.125 * i + value(4000 + i);
+    for (int q = 0; q < 9; ++q) s.g.push_back(value(5000 + 9 * i + q));
+    s.g_max = value(6000 + i);
+  }
+  lib::csvio::write_dense_audit(dir + "/dense_audit.csv", samples);
+  lib::csvio::write_dense_audit(dir + "/dense_audit_empty.csv", std::vector<lib::AuditSample>{});
   return 0;
 }

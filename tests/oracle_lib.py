@@ -190,6 +190,18 @@ class CpuOracle:
                                      C.byref(gmax), C.byref(ytot), _p(dy))
         return rc, gmax.value, ytot.value, dy
 
+    def dense_audit_samples(self, desc, x, u, substeps, tau=None):
+        """dense_violation_audit with its sample sink: samples [M][substeps+1][12] =
+        {interval, tau, g[9], g_max}."""
+        x, u = f64(x), f64(u)
+        tau = None if tau is None else f64(tau)
+        gmax, ytot = C.c_double(0), C.c_double(0)
+        dy = np.zeros(desc.nodes - 1)
+        samples = np.zeros((desc.nodes - 1, substeps + 1, 12))
+        rc = self._f("dense_audit_samples")(C.byref(desc), _p(tau), _p(x), _p(u), C.c_int(substeps),
+                                             C.byref(gmax), C.byref(ytot), _p(dy), _p(samples))
+        return rc, gmax.value, ytot.value, dy, samples
+
     # ---- SCP glue
     def assemble(self, desc, init_state, x, u, blocks, tau=None, with_a_plus=False):
         n, m = desc.nodes, desc.nodes - 1

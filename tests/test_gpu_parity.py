@@ -494,6 +494,21 @@ def test_dense_audit_matches_oracle(solver15, ptor):
         assert abs(out["max_pointwise_g"][b] - g) <= TOL_DISC * max(1.0, abs(g))
         assert np.abs(out["interval_y_increase"][b] - dy).max() <= TOL_DISC * max(1.0, np.abs(dy).max())
         assert abs(out["interval_y_increase"][b].sum() - ytot) <= 1e-9 * max(1.0, abs(ytot))
+    # the sample sink of the audit (AuditSample: interval, tau, g[9], g_max), reference order
+    smp = s.dense_violation_audit_samples(bad, bad_u, 6)
+    assert smp["samples"].shape == (6, d.nodes - 1, 7, 12)
+    for b in range(6):
+        rc, g, ytot, dy, ref = ptor.dense_audit_samples(d, bad[b], bad_u[b], 6)
+        if b == 2:
+            assert smp["status"][b] == abi.ST_DILATION_NONPOSITIVE and smp["fail_index"][b] == 6
+            got, ref = smp["samples"][b][:6], ref[:6]   # intervals before the failing one are complete
+        else:
+            assert rc == 0 and smp["status"][b] == 0
+            assert abs(smp["max_pointwise_g"][b] - g) <= TOL_DISC * max(1.0, abs(g))
+            got = smp["samples"][b]
+        assert np.array_equal(got[..., 0], ref[..., 0])                       # interval index
+        assert np.abs(got[..., 1] - ref[..., 1]).max() <= 1e-15               # tau
+        assert np.abs(got[..., 2:] - ref[..., 2:]).max() <= TOL_DISC * max(1.0, np.abs(ref[..., 2:]).max())
 
 
 def test_run_batch_records_match_oracle(ptor):

@@ -52,12 +52,12 @@ def test_host_mirror_against_oracle_on_gpu():
     assert "all host-API checks passed" in out.stdout
 
 
-def build_example():
+def build_example(name="montecarlo_batch"):
     BUILD.mkdir(exist_ok=True)
-    exe = BUILD / "montecarlo_batch"
+    exe = BUILD / name
     subprocess.run(
         ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", f"-I{HOST}",
-         str(ROOT / "examples" / "montecarlo_batch.cpp"), "-o", str(exe), f"-L{LIBDIR}", "-lptopt_cuda",
+         str(ROOT / "examples" / f"{name}.cpp"), "-o", str(exe), f"-L{LIBDIR}", "-lptopt_cuda",
          f"-Wl,-rpath,{LIBDIR}"], check=True)
     return exe
 
@@ -65,6 +65,7 @@ def build_example():
 def test_example_compiles_and_rejects_bad_input(tmp_path):
     """examples/montecarlo_batch.cpp (config -> run_batch -> CSV): builds, and the argument / config
     errors exit with the reference CLI's usage code before any GPU work."""
+    assert subprocess.run([str(build_example("solve_nominal"))], capture_output=True).returncode == 2
     exe = build_example()
     assert subprocess.run([str(exe)], capture_output=True).returncode == 2
     bad = tmp_path / "bad.json"
@@ -113,3 +114,40 @@ def test_example_batch_from_config_matches_the_binding(tmp_path):
     traj = np.array([[float(v) for v in l.split(",")] for l in (tmp_path / "trajectory_0004.csv").read_text().splitlines()[1:]])
     assert traj.shape == (10, 24)
     assert np.array_equal(traj[:, 2:17], x[4]) and np.array_equal(traj[:, 17:24], u[4])
+
+
+@pytest.mark.gpu
+def test_example_single_solve_from_config_matches_the_binding(tmp_path):
+    """examples/solve_nominal.cpp (the reference's `solve` subcommand): config -> initial_guess ->
+    scp_solve -> dense audit with samples -> trajectory.csv / dense_audit.csv / diagnostics.txt, against
+    the same solve through the ctypes harness (identical device path: bit for bit)."""
+    import json
+
+    import numpy as np
+
+    from paper_2404_18034_b200 import scenario
+    from paper_2404_18034_b200.binding import Solver
+
+    exe = build_example("solve_nominal")
+    cfg = {"grid": {"N": 9, "audit_substeps": 5}, "scp": {"max_iters": 3}, "pipg": {"j_max": 150, "power_j_max": 200},
+           "output_dir": str(tmp_path)}
+    path = tmp_path / "run.json"
+    path.write_text(json.dumps(cfg))
+    out = subprocess.run([str(exe), str(path)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 1, out.stdout + out.stderr          # three iterations do not converge
+    assert out.stdout.startswith("converged=0 iterations=3 ")
+    diag = (tmp_path / "diagnostics.txt").read_text().splitlines()
+    assert diag[0] == "non-convergence diagnostics" and diag[1] == "iterations 3" and len(diag) == 4 + 3
+
+    sc = scenario.default_scenario(9)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 3, 150, 200
+    nominal = np.array(sc.initial_state)
+    xg, ug = scenario.initial_guess(sc, nominal)
+    with Solver(sc.problem_desc()) as s:
+        res = s.scp_solve(nominal[None], xg[None], ug[None], np.array([sc.dispersion.seed], np.uint64))
+        smp = s.dense_violation_audit_samples(res["x"], res["u"], 5)
+    traj = np.array([[float(v) for v in l.split(",")] for l in (tmp_path / "trajectory.csv").read_text().splitlines()[1:]])
+    assert np.array_equal(traj[:, 2:17], res["x"][0]) and np.array_equal(traj[:, 17:24], res["u"][0])
+    rows = np.array([[float(v) for v in l.split(",")] for l in (tmp_path / "dense_audit.csv").read_text().splitlines()[1:]])
+    assert rows.shape == (8 * 6, 12)
+    assert np.array_equal(rows, smp["samples"][0].reshape(-1, 12))

@@ -17,7 +17,7 @@ BUILD = ROOT / "tests" / "_build"
 GOLDEN = ROOT / "tests" / "golden" / "io"
 REF_INCLUDE = Path("/root/reference/proj/include")
 SRC = ROOT / "tests" / "cpp" / "io_formats.cpp"
-FILES = ("runs.csv", "summary.csv", "summary_none.csv", "trajectory.csv")
+FILES = ("runs.csv", "summary.csv", "summary_none.csv", "trajectory.csv", "dense_audit.csv", "dense_audit_empty.csv")
 
 
 def run_writer(reference: bool, out_dir: Path):

@@ -251,6 +251,13 @@ def test_dense_audit_and_run_batch_bitwise(ptor, ptref):
     b = ptref.dense_audit(d, x, u, 16)
     assert a[0] == b[0] == 0 and a[1] == b[1] and a[2] == b[2]
     same(a[3], b[3])
+    # the sample sink: {interval, tau, g[9], g_max} per node / substep, in the reference's order
+    sa = ptor.dense_audit_samples(d, x, u, 5)
+    sb = ptref.dense_audit_samples(d, x, u, 5)
+    assert sa[0] == sb[0] == 0 and sa[1] == sb[1]
+    same(sa[4], sb[4])
+    assert sa[4].shape == (5, 6, 12) and (sa[4][:, :, 0] == np.arange(5)[:, None]).all()
+    assert sa[4][:, :, 11].max() == sa[1]
     spec = sc.dispersion
     wa, reca, xa, ua = ptor.run_batch(d, sc.initial_state, spec.r_low, spec.r_high, spec.seed, 4,
                                       2, 16, keep=True)

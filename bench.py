@@ -427,7 +427,7 @@ def run_own_arm(args):
                               for k in ("linearize", "power_iteration", "pipg")},
             },
         }
-        if not args.no_other_configs:
+        if world == 1 and not args.no_other_configs:
             line["other_configs"] = other_configs(local_rank, fp64_peak)
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1

@@ -288,14 +288,18 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
 __device__ __forceinline__ void mbar_expect(unsigned long long* bar, int bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+/// Waits for `phase` of a mailbox.  A wait normally ends within a microsecond; a protocol error
+/// must surface as a failed launch, not as a hung device, so the poll gives up (trap) after
+/// 2^26 attempts (seconds).
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, int phase) {
-  unsigned ok;
+  unsigned ok, polls = 0;
   do {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(ok)
                  : "r"(smem_u32(bar)), "r"((unsigned)(phase & 1))
                  : "memory");
-  } while (!ok);
+  } while (!ok && ++polls < (1u << 26));
+  if (!ok) __trap();
 }
 
 /// Per-thread view of the mailboxes of a cluster CTA.

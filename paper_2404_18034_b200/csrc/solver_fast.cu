@@ -790,7 +790,9 @@ pipg_fast_kernel(PipgArgs a) {
   const double sigma = a.sigma[b];
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
-  const double one_m_rho = 1.0 - a.rho;
+  // extrapolation (pipg.hpp:461-472) (1 - rho) * ex + rho * cur, evaluated as ex + rho * (cur - ex):
+  // the same two operations without a loop-long register pair for 1 - rho
+  auto extrapolate = [&](double ex, double cur) { return fma(a.rho, cur - ex, ex); };
   __syncthreads();
   // "previous interval" mailbox: phase j = what rank 0 sends after iteration j (0: the warm start);
   // it is received inside the next primal step, or after the loop
@@ -848,7 +850,7 @@ pipg_fast_kernel(PipgArgs a) {
       xr_k[i] = xrf;
       if (push_next) push_f64(partner_u32(sm + L.xs + cut.half * kXS + i, 0), xrf, bx.box(kBoxNext));
       if (kStore) snap[S.x + kc * kNX + i] = xn;
-      xe[r] = one_m_rho * x0 + a.rho * xn;  // extrapolation, pipg.hpp:461-467
+      xe[r] = extrapolate(x0, xn);
     }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -866,7 +868,7 @@ pipg_fast_kernel(PipgArgs a) {
       if (kStore) {
         if (q == 0 || g < 2) snap[S.u + kc * kNU + ju] = un;
       }
-      ue[q] = one_m_rho * u0 + a.rho * un;
+      ue[q] = extrapolate(u0, un);
     }
     __syncthreads();
     if constexpr (kCluster) bx.recv_next(iter_no - 1);  // rank 1's first node of this iteration
@@ -895,16 +897,16 @@ pipg_fast_kernel(PipgArgs a) {
           snap[S.vn + e] = vn;
           snap[S.ph + e] = pn;
         }
-        const double pe = one_m_rho * p0 + a.rho * pn;
+        const double pe = extrapolate(p0, pn);
         phe[r] = ival ? pe : 0.0;
-        vpe[r] = one_m_rho * vp0 + a.rho * vp;
-        vne[r] = one_m_rho * vn0 + a.rho * vn;
+        vpe[r] = extrapolate(vp0, vp);
+        vne[r] = extrapolate(vn0, vn);
       }
       if (g == 4) {
         const double drift = xr_k[kXS + 14] - v[14] - eps_k[0];
         const double tn = clip0(the + beta * drift);
         if (kStore) snap[S.th + kc] = tn;
-        the = ival ? one_m_rho * the + a.rho * tn : 0.0;
+        the = ival ? extrapolate(the, tn) : 0.0;
       }
       publish_duals(phe, the);
     }

@@ -807,14 +807,19 @@ pipg_fast_kernel(PipgArgs a) {
     //      chain behind the shared-memory loads stays short.
     double base[kR], fv[kR], sx[kR];
     double su[2], lo[2], hi[2];
-    if constexpr (kCluster) {
-      // the sums over the thread's own interval first: they hide part of the flight time of the
-      // partner's boundary values, which only the previous-interval terms below need
+    // the sums over the thread's own interval first: in a cluster they hide part of the flight
+    // time of the partner's boundary values, which only the previous-interval terms below need
 #pragma unroll
-      for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
+    for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
-      bx.recv_prev(iter_no - 1);  // rank 0's last interval after iteration iter_no - 1 (0: warm start)
+    for (int q = 0; q < 2; ++q) su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
+    if constexpr (kCluster) bx.recv_prev(iter_no - 1);  // rank 0's last interval after iteration iter_no - 1 (0: warm start)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double2 bq = q == 0 ? *bnd0 : *bnd1;
+      lo[q] = bq.x;
+      hi[q] = bq.y;
+      su[q] += column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
     }
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
@@ -825,19 +830,6 @@ pipg_fast_kernel(PipgArgs a) {
       t += -phx_k[r - kNX];
       if (r == kR - 1 && g == 4) t += thx_k[-1] - thx_k[0];
       base[r] = t;
-    }
-    if constexpr (!kCluster) {
-#pragma unroll
-      for (int r = 0; r < kR; ++r) sx[r] = column_sum(part_k, kR * g + r);
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double2 bq = q == 0 ? *bnd0 : *bnd1;
-      lo[q] = bq.x;
-      hi[q] = bq.y;
-      const double prev = column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
-      if constexpr (kCluster) su[q] += prev;
-      else su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g) + prev;
     }
 #pragma unroll
     for (int r = 0; r < kR; ++r) {

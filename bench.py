@@ -387,6 +387,22 @@ def run_own_arm(args):
                       "power_iteration": B * (m_int * 435 + n * 22 + 2 * m_int * 15) * 8,
                       "pipg": B * (m_int * 435 + 2 * (n * 22 + m_int * 46) + m_int * 16 + 2 * n * 7) * 8}
         value = world * B * args.steps / (ms_total * 1e-3)
+        # Shared-memory view of the two solver kernels (one CTA = one instance = one SM): clocks per
+        # trip / iteration from the stage time at the sampled SM clock, against the shared-memory
+        # wavefronts one trip / iteration issues (ncu source counters of the hot loops,
+        # profiles/r01_s3_power_loop_stalls.txt and r01_s3_pipg_loop_stalls.txt: 237.0 and 250.1 per
+        # warp-pass x 8 warps; one wavefront per clock and SM, tools/probes/smem_width.cu)
+        smem_view = None
+        clk_info = clocks.summary()
+        if n == 50 and args.solver_path == "auto" and clk_info.get("sm_mhz"):
+            sms = min(torch.cuda.get_device_properties(dev).multi_processor_count, B)
+            units = {"power_iteration": sum_trips, "pipg": pipg_iters}
+            wavefronts = {"power_iteration": 237.0 * 8, "pipg": 250.1 * 8}
+            smem_view = {}
+            for k in units:
+                clk = stages[k] * 1e-3 * clk_info["sm_mhz"] * 1e6 * sms / units[k]  # stage times: last launch
+                smem_view[k] = {"clk_per_iteration": clk, "smem_wavefronts_per_iteration": wavefronts[k],
+                                "frac_of_smem_floor": wavefronts[k] / clk}
         line = {
             "metric": "SCP solves/sec (batched, N=50)", "value": value, "unit": "solves/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -425,6 +441,7 @@ def run_own_arm(args):
                                   "frac": flop[k] / (stages[k] * 1e-3) * 1e-12 / fp64_peak,
                                   "share_of_step": stages[k] / stages["graph_total"]}
                               for k in ("linearize", "power_iteration", "pipg")},
+                "shared_memory_view": smem_view,
             },
         }
         if world == 1 and not args.no_other_configs:

@@ -390,7 +390,7 @@ def run_own_arm(args):
         # Shared-memory view of the two solver kernels (one CTA = one instance = one SM): clocks per
         # trip / iteration from the stage time at the sampled SM clock, against the shared-memory
         # wavefronts one trip / iteration issues (ncu source counters of the hot loops,
-        # profiles/r01_s3_power_loop_stalls.txt and r01_s3_pipg_loop_stalls.txt: 237.0 and 250.1 per
+        # profiles/r01_s5_power_loop_stalls.txt and r01_s5_pipg_loop_stalls.txt: 237.0 and 250.1 per
         # warp-pass x 8 warps; one wavefront per clock and SM, tools/probes/smem_width.cu)
         smem_view = None
         clk_info = clocks.summary()

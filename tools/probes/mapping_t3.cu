@@ -133,6 +133,12 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
   const double* part_k = part + (size_t)k * T * PS;
   auto pos_x = [](int cc, int r) { return R * cc + r; };
   const long long t0 = clock64();
+#ifdef PHASES
+  long long ph_clk[4] = {0, 0, 0, 0}, tc = t0;  // forward+transposed, barrier 1, owner sums, barrier 2 + norm
+#define PHASE(i) { const long long tn = clock64(); ph_clk[i] += tn - tc; tc = tn; }
+#else
+#define PHASE(i)
+#endif
 #pragma unroll 1
   for (int it = 0; it < iters; ++it) {
     const double inv = 1.0 / sigma;
@@ -248,7 +254,9 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
         }
       }
     }
+    PHASE(0)
     if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst);
+    PHASE(1)
     double nrm = 0.0;
     if (node) {  // owner sums: x = A-^T phi_k - phi_{k-1}, u = B-^T phi_k + B+^T phi_{k-1}
 #pragma unroll
@@ -275,17 +283,24 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
     }
     nrm = warp_sum(nrm);
     if (lane == 0) red[wi] = nrm;
+    PHASE(2)
     if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst);
     double tot = 0.0;
 #pragma unroll
     for (int w = 0; w < TPI / 32; ++w) tot += red[w];
     sigma = sqrt(tot);
+    PHASE(3)
   }
   const long long t1 = clock64();
   if (tt == 0) {
     sigma_out[gid] = sigma;
     clk_out[gid] = t1 - t0;
   }
+#ifdef PHASES
+  if (blockIdx.x == 0 && inst == 0 && lane == 0)
+    printf("  warp %d: forward+transposed %.0f, barrier %.0f, owner sums %.0f, barrier+norm %.0f clk per trip\n", wi,
+           (double)ph_clk[0] / iters, (double)ph_clk[1] / iters, (double)ph_clk[2] / iters, (double)ph_clk[3] / iters);
+#endif
   if constexpr (CT > 0) {
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tm_slot));

@@ -1,10 +1,10 @@
-// mapping_t3.cu — how fast is one power-iteration trip with THREE threads per node (five operator
-// rows each, part of them in tensor memory, two instances per CTA on independent named barriers)
-// against the library's mapping (five threads per node, three rows each, all in registers, one
-// instance per CTA)?  Same data movement and flops per trip as power_fast_kernel (forward product,
-// dual scaling, transposed partial sums, owner sums, norm), none of its boundary handling; both
-// mappings run the same operator and must print the same sigma.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -Xptxas -v -o mapping_t3.bin mapping_t3.cu
+// trip_ablation.cu — where does a power-iteration trip spend its 2 780 clk?  The control of
+// mapping_t3.cu (the library's five-threads-per-node mapping) with pieces removed one at a time
+// (template parameter ABL, bit mask): 1 forward FMAs, 2 transposed FMAs, 4 transposed FMAs and
+// partial-sum stores, 8 four of the five partial-sum loads, 16 forward loads, 32 warp reduction of
+// the norm, 64 sqrt and division, 128 cross-warp sum, 512 / 1024 the two block barriers.  Results
+// are wrong by construction; only the clocks matter.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o trip_ablation.bin trip_ablation.cu
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -71,10 +71,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the next CS in thread-private shared memory, the last CT in tensor memory
 // DEFER: the scale 1/sigma is applied by the owner sums instead of the forward map, so that the
 // warp-level part of the norm reduction moves from the end of a trip to the top of the next one
-// DEFER == 2 (lagged normalisation): the forward map of trip j scales by 1/||z_{j-1}|| instead of
-// 1/||z_j||, so the whole norm -> sqrt -> reciprocal chain leaves the critical path; sigma is the
-// ratio ||z_{j+1}|| ||z_{j-1}|| / ||z_j||, the same number up to rounding
-template <int T, int INST, int CT, int CS, int DEFER = 0>
+template <int T, int INST, int CT, int CS, bool DEFER = false, int ABL = 0>
 __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double* sigma_out, long long* clk_out) {
   using M = Map<T>;
   constexpr int R = M::R, UPT = M::UPT, PS = M::PS, TPI = M::TPI, CREG = kW - CT - CS, CTM = kW - CT, ND = R * CT;
@@ -147,10 +144,9 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
 #pragma unroll 1
   double carry = 0.0;  // DEFER: this thread's share of the squared norm of the last trip
   if (DEFER && tt == 0) red[0] = 1.0;  // sigma of the seed
-  double lag_c = 1.0, lag_next = 1.0, n0 = 1.0, n1 = 1.0, c_used = 1.0;  // DEFER == 2: scale in use, next one, last two squared norms
   for (int it = 0; it < iters; ++it) {
-    const double inv = DEFER >= 2 ? lag_c : (DEFER ? 1.0 : 1.0 / sigma);
-    if (DEFER && DEFER < 3 && it > 0) {
+    const double inv = DEFER ? 1.0 : ((ABL & 64) ? sigma : 1.0 / sigma);
+    if (DEFER && it > 0) {
       const double w = warp_sum(carry);
       if (lane == 0) red[wi] = w;
     }
@@ -161,39 +157,34 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
       double v[kW];
       const double2* x2 = reinterpret_cast<const double2*>(xs + k * kXS);
 #pragma unroll
-      for (int q = 0; q < 7; ++q) { const double2 t = x2[q]; v[2 * q] = t.x; v[2 * q + 1] = t.y; }
-      v[14] = xs[k * kXS + 14];
+      for (int q = 0; q < 7; ++q) { const double2 t = (ABL & 16) ? make_double2(1.0, 1.0) : x2[q]; v[2 * q] = t.x; v[2 * q + 1] = t.y; }
+      v[14] = (ABL & 16) ? 1.0 : xs[k * kXS + 14];
       const double2* u2 = reinterpret_cast<const double2*>(us + k * kUS);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { const double2 t = u2[q]; v[15 + 2 * q] = t.x; if (q < 3) v[16 + 2 * q] = t.y; }
+      for (int q = 0; q < 4; ++q) { const double2 t = (ABL & 16) ? make_double2(1.0, 1.0) : u2[q]; v[15 + 2 * q] = t.x; if (q < 3) v[16 + 2 * q] = t.y; }
       const double2* w2 = reinterpret_cast<const double2*>(us + (k + 1) * kUS);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) { const double2 t = w2[q]; v[22 + 2 * q] = t.x; if (q < 3) v[23 + 2 * q] = t.y; }
+      for (int q = 0; q < 4; ++q) { const double2 t = (ABL & 16) ? make_double2(1.0, 1.0) : w2[q]; v[22 + 2 * q] = t.x; if (q < 3) v[23 + 2 * q] = t.y; }
       double acc[R];
-      if constexpr (DEFER >= 3) {
-        // the five steps of the warp reduction of the previous trip's norm shares, one between
-        // column chunks of the forward product (each step's shuffle latency under six columns of FMAs)
-        double w = carry;
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = 0.0;
-#pragma unroll
-        for (int c5 = 0; c5 < 5; ++c5) {
-          const double t = __shfl_xor_sync(0xffffffffu, w, 16 >> c5);
-#pragma unroll
-          for (int j = 6 * c5; j < (6 * c5 + 6 < CREG ? 6 * c5 + 6 : CREG); ++j)
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = fma(a[r][j], v[j], acc[r]);
-          w += t;
-        }
-        if (it > 0 && lane == 0) red[wi] = w;
-      } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double s = 0.0;
+        if constexpr ((ABL & 17) == 0) {
 #pragma unroll
-        for (int j = 0; j < CREG; ++j) s = fma(a[r][j], v[j], s);
+          for (int j = 0; j < CREG; ++j) s = fma(a[r][j], v[j], s);
+        } else if constexpr ((ABL & 16) == 0) {
+          long long f[kW];
+#pragma unroll
+          for (int j = 0; j < kW; ++j) f[j] = __double_as_longlong(v[j]);
+#pragma unroll
+          for (int st2 = 1; st2 < kW; st2 *= 2)
+#pragma unroll
+            for (int j = 0; j + st2 < kW; j += 2 * st2) f[j] ^= f[j + st2];
+          s = a[r][0] * __longlong_as_double((f[0] & 0xFFFFll) | 0x3FF0000000000000ll);
+        } else {
+          s = a[r][0];
+        }
         acc[r] = s;
-      }
       }
       if constexpr (CS > 0) {
 #pragma unroll
@@ -236,11 +227,13 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
       }
 #pragma unroll
       for (int j = 0; j < CREG; ++j) {
-        double p = a[0][j] * ph[0];
+        double p = (ABL & 6) ? ph[j % R] : a[0][j] * ph[0];
+        if constexpr ((ABL & 6) == 0) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) p = fma(a[r][j], ph[r], p);
+          for (int r = 1; r < R; ++r) p = fma(a[r][j], ph[r], p);
+        }
         const int pos = j < kNX ? j : (j < kNX + kNU ? 15 + (j - kNX) / UPT * R + (j - kNX) % UPT : 30 + (j - 22) / UPT * R + (j - 22) % UPT);
-        slot[pos] = p;
+        if (!(ABL & 4) || j < R) slot[pos] = p;
       }
       if constexpr (CS > 0) {
 #pragma unroll
@@ -285,37 +278,23 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
       }
     }
     PHASE(0)
-    if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst);
+    if constexpr (!(ABL & 1024)) { if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst); }
     PHASE(1)
     double nrm = 0.0, sc = 1.0;
-    if constexpr (DEFER == 1) {
+    if constexpr (DEFER) {
       double tot = 0.0;
 #pragma unroll
       for (int w = 0; w < TPI / 32; ++w) tot += red[w];
       sc = rsqrt(tot);
       sigma = sqrt(tot);
     }
-    if constexpr (DEFER >= 2) {
-      double tot = 0.0;
-#pragma unroll
-      for (int w = 0; w < TPI / 32; ++w) tot += red[w];
-      if constexpr (DEFER == 4) {  // 2^-floor(log2(tot)/2): exact scaling, a handful of integer operations
-        const int e = (__double2hiint(tot) >> 20) - 0x3ff;
-        lag_next = __hiloint2double((0x3ff - (e >> 1)) << 20, 0);
-        n0 = n1;
-      } else {
-        lag_next = rsqrt(tot);  // first needed by the forward map of the next trip
-        n0 = n1;
-      }
-      n1 = tot;
-    }
     if (node) {  // owner sums: x = A-^T phi_k - phi_{k-1}, u = B-^T phi_k + B+^T phi_{k-1}
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < T; ++q) s += part_k[q * PS + pos_x(c, r)];
-        const double x = DEFER == 1 ? (s - phi[(k - 1) * kPH + R * c + r]) * sc : s - phi[(k - 1) * kPH + R * c + r];
+        for (int q = 0; q < ((ABL & 8) ? 1 : T); ++q) s += part_k[q * PS + pos_x(c, r)];
+        const double x = DEFER ? (s - phi[(k - 1) * kPH + R * c + r]) * sc : s - phi[(k - 1) * kPH + R * c + r];
         xs[k * kXS + R * c + r] = x;
         nrm = fma(x, x, nrm);
       }
@@ -323,33 +302,29 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
       for (int q = 0; q < UPT; ++q) {
         double s = 0.0;
 #pragma unroll
-        for (int p = 0; p < T; ++p) s += part_k[p * PS + 15 + R * c + q] + part_k[(p - T) * PS + 30 + R * c + q];
-        if constexpr (DEFER == 1) s *= sc;
+        for (int p = 0; p < ((ABL & 8) ? 1 : T); ++p) s += part_k[p * PS + 15 + R * c + q] + part_k[(p - T) * PS + 30 + R * c + q];
+        if constexpr (DEFER) s *= sc;
         if (UPT * c + q < kNU) {
           us[k * kUS + UPT * c + q] = s;
           nrm = fma(s, s, nrm);
         }
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r) nrm = DEFER == 1 ? fma(2.0 * (ph[r] * sc), ph[r] * sc, nrm) : fma(2.0 * ph[r], ph[r], nrm);
+      for (int r = 0; r < R; ++r) nrm = DEFER ? fma(2.0 * (ph[r] * sc), ph[r] * sc, nrm) : fma(2.0 * ph[r], ph[r], nrm);
     }
     if constexpr (DEFER) {
       carry = nrm;
     } else {
-      nrm = warp_sum(nrm);
+      if (!(ABL & 32)) nrm = warp_sum(nrm);
       if (lane == 0) red[wi] = nrm;
     }
     PHASE(2)
-    if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst);
+    if constexpr (!(ABL & 512)) { if constexpr (INST == 1) __syncthreads(); else inst_barrier<TPI>(inst); }
     if constexpr (!DEFER) {
       double tot = 0.0;
 #pragma unroll
-      for (int w = 0; w < TPI / 32; ++w) tot += red[w];
-      sigma = sqrt(tot);
-    }
-    if constexpr (DEFER >= 2) {
-      c_used = lag_c;
-      lag_c = lag_next;
+      for (int w = 0; w < ((ABL & 128) ? 1 : TPI / 32); ++w) tot += red[w];
+      sigma = (ABL & 64) ? tot * 1e-3 : sqrt(tot);
     }
     PHASE(3)
   }
@@ -360,7 +335,7 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
     double tot = 0.0;
 #pragma unroll
     for (int w2 = 0; w2 < TPI / 32; ++w2) tot += red[w2];
-    sigma = DEFER == 4 ? sqrt(tot) / (c_used * sqrt(n1)) : (DEFER >= 2 ? sqrt(tot) * sqrt(n0) / sqrt(n1) : sqrt(tot));
+    sigma = sqrt(tot);
   }
   const long long t1 = clock64();
   if (tt == 0) {
@@ -378,12 +353,12 @@ __global__ void __launch_bounds__(INST * Map<T>::TPI, 1) trips(int iters, double
   }
 }
 
-template <int T, int INST, int CT, int CS, int DEFER = 0>
+template <int T, int INST, int CT, int CS, bool DEFER = false, int ABL = 0>
 void run(const char* name, int iters, double* d_sigma, long long* d_clk, double* ref) {
   using M = Map<T>;
   constexpr int kInst = (kN + 6) * (kXS + kUS + kPH) + (M::TPI + 2 * T) * M::PS + 16 + M::R * CS * M::TPI;
   const size_t smem = (size_t)INST * kInst * sizeof(double);
-  auto kern = trips<T, INST, CT, CS, DEFER>;
+  auto kern = trips<T, INST, CT, CS, DEFER, ABL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = 148;
   kern<<<grid, INST * M::TPI, smem>>>(iters, d_sigma, d_clk);
@@ -408,16 +383,20 @@ int main() {
   cudaMalloc(&d_clk, sizeof(long long) * 296);
   static double ref[148] = {0};
   const int iters = 3000;
-  run<5, 1, 0, 0>("T=5: 3 rows x 29 cols in registers, 1 instance/SM", iters, d_sigma, d_clk, ref);
-  run<5, 1, 0, 0, 1>("T=5, scale deferred to the owner sums (no warp reduction before the barrier)", iters, d_sigma, d_clk, ref);
-  run<5, 1, 0, 0, 2>("T=5, normalisation lagged by one trip (norm chain off the critical path)", iters, d_sigma, d_clk, ref);
-  run<5, 1, 0, 0, 3>("T=5, lagged normalisation, reduction steps interleaved with the forward product", iters, d_sigma, d_clk, ref);
-  run<5, 1, 0, 0, 4>("T=5, lagged power-of-two scale, interleaved reduction, no sqrt in the loop", iters, d_sigma, d_clk, ref);
-  run<3, 1, 17, 0>("T=3: 12 reg + 17 TMEM cols, 1 instance", iters, d_sigma, d_clk, ref);
-  run<3, 2, 17, 0>("T=3: 12 reg + 17 TMEM cols, 2 instances", iters, d_sigma, d_clk, ref);
-  run<3, 2, 17, 3>("T=3: 9 reg + 3 smem + 17 TMEM cols, 2 instances", iters, d_sigma, d_clk, ref);
-  run<3, 2, 17, 4>("T=3: 8 reg + 4 smem + 17 TMEM cols, 2 instances", iters, d_sigma, d_clk, ref);
-  run<3, 2, 16, 4>("T=3: 9 reg + 4 smem + 16 TMEM cols, 2 instances", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0>("control", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 1>("forward FMAs removed (loads kept)", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 2>("transposed FMAs removed (stores kept)", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 3>("all FMAs removed", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 4>("transposed FMAs and partial stores removed", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 8>("1 of 5 partial loads", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 17>("forward loads and FMAs removed", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 29>("skeleton: barriers, norm, owner stores only", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 29 + 32>("skeleton, no warp reduction", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 29 + 64>("skeleton, no sqrt / division", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 29 + 32 + 64 + 128>("bare skeleton (no norm chain)", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 29 + 32 + 64 + 128 + 512 + 1024>("bare skeleton, both barriers removed", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 32 + 64 + 128>("full work, no norm chain", iters, d_sigma, d_clk, ref);
+  run<5, 1, 0, 0, false, 512 + 1024>("full work, both barriers removed", iters, d_sigma, d_clk, ref);
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

@@ -224,12 +224,20 @@ def run_own_arm(args):
     rank, local_rank, world = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device — the product path has no CPU fallback")
+    # PTOPT_BENCH_SHARE_GPU=1 (plumbing check only, numbers meaningless): all ranks time-slice the
+    # GPUs that exist and rendezvous over gloo, so the multi-rank path can be exercised on one GPU
+    share_gpu = os.environ.get("PTOPT_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     use_dist = world > 1
     if use_dist:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if use_dist:
@@ -355,7 +363,7 @@ def run_own_arm(args):
         ms_total = sharding.max_over_ranks(ms_total)
         e2e_s = sharding.max_over_ranks(e2e_s)
         rb_s = sharding.max_over_ranks(rb_s)
-        bad = torch.tensor([int((status != 0).sum())], device=dev)
+        bad = torch.tensor([int((status != 0).sum())], device=torch.device("cpu") if share_gpu else dev)
         dist.all_reduce(bad)
         n_bad = int(bad[0])
     else:

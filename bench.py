@@ -210,6 +210,20 @@ def other_configs(device_index, fp64_peak):
         "power_trips_mean": float(res["power_trips"].sum(axis=1).mean()),
         "what": "full SCP solves at N=100 on one GPU (2-CTA cluster per instance, two waves), device time of "
                 "the graph"}
+    # ---- config 1 shape: the default scenario (N=15), one instance, full SCP loop
+    sc = scenario.default_scenario(15)
+    one = scenario.make_batch(sc, range(1))
+    with Solver(sc.problem_desc(), device=device_index) as s:
+        s.scp_solve(one["init_state"], one["x_guess"], one["u_guess"], one["rng_seed"])
+        lat = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            s.scp_solve(one["init_state"], one["x_guess"], one["u_guess"], one["rng_seed"])
+            lat.append(1e3 * (time.perf_counter() - t0))
+    out["config1_default_scenario_single_instance_N15"] = {
+        "latency_ms_p50": statistics.median(lat),
+        "what": "SPEC default 6-DoF landing scenario, one instance, full SCP loop, host buffers "
+                "(the reference takes 3.3-3.8 s on one core, SURVEY 8d)"}
     return out
 
 

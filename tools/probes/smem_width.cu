@@ -12,7 +12,8 @@ template <> __device__ __forceinline__ uint32_t fold<uint4>(const uint4& t) { re
 
 // pattern 0: lane-contiguous; 1: element stride 3 (conflict-free, scattered over 3x the span);
 // 2: groups of 5 lanes read the same element (broadcast, like the node vectors);
-// 3: element index 35*(lane%5)*0 + 175*(lane/5) + 3*(lane%5)  (the partial-sum read pattern, in units of T)
+// 3: element index 175*(lane/5) + 3*(lane%5)  (the partial-sum read pattern, in units of T);
+// 4: the whole warp reads one element; 5: each quarter warp reads one element
 template <class T>
 __global__ void __launch_bounds__(256, 1) probe(int pattern, int iters, long long* clk_out, uint32_t* sink) {
   extern __shared__ __align__(16) unsigned char raw[];
@@ -25,7 +26,11 @@ __global__ void __launch_bounds__(256, 1) probe(int pattern, int iters, long lon
   if (pattern == 0) idx = threadIdx.x;
   else if (pattern == 1) idx = 3 * threadIdx.x;
   else if (pattern == 2) idx = threadIdx.x / 5;
-  else idx = 175 * (threadIdx.x / 5) + 3 * (threadIdx.x % 5);
+  else if (pattern == 3) idx = 175 * (threadIdx.x / 5) + 3 * (threadIdx.x % 5);
+  else if (pattern == 4) idx = warp;          // one address per warp
+  else if (pattern == 5) idx = threadIdx.x / 8;  // one address per quarter warp
+  else if (pattern == 6) idx = threadIdx.x / 4;  // two addresses per quarter warp
+  else idx = 2 * (threadIdx.x / 8) + ((threadIdx.x & 7) >= 5);  // five lanes + three lanes per quarter warp
   (void)lane; (void)warp;
   uint32_t acc = 0;
   const long long t0 = clock64();
@@ -41,8 +46,8 @@ __global__ void __launch_bounds__(256, 1) probe(int pattern, int iters, long lon
 template <class T>
 void run(const char* name, long long* d_clk, uint32_t* d_sink) {
   cudaFuncSetAttribute(probe<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  const char* pats[] = {"contiguous", "stride 3", "broadcast x5", "partial-sum pattern"};
-  for (int p = 0; p < 4; ++p) {
+  const char* pats[] = {"contiguous", "stride 3", "broadcast x5", "partial-sum pattern", "one address per warp", "one address per 8 lanes", "two addresses per 8 lanes (4+4)", "two addresses per 8 lanes (5+3)"};
+  for (int p = 0; p < 8; ++p) {
     const int iters = 4096;
     probe<T><<<148, 256, 64 * 1024>>>(p, iters, d_clk, d_sink);
     probe<T><<<148, 256, 64 * 1024>>>(p, iters, d_clk, d_sink);

@@ -107,6 +107,7 @@ class Solver:
         self.desc = desc
         self.nodes = int(desc.nodes)
         self.device = device
+        self.solver_path = "auto"
         self._h = C.c_void_p()
         tau_arr = None if tau is None else _np(tau)
         stream_ptr = None
@@ -136,6 +137,7 @@ class Solver:
         """'auto' (register-resident kernels where the shape allows; split variant for small
         batches), 'generic' (shape-generic kernels) or 'split' (PTOPT_SOLVER_FAST_SPLIT)."""
         _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int({"auto": 0, "generic": 1, "split": 2}[path])))
+        self.solver_path = path
 
     def synchronize(self):
         _check(self.lib.ptopt_cuda_synchronize(self._h))

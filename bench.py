@@ -115,12 +115,79 @@ def cpu_reference_run(nodes: int, instances: int, workers: int):
     return instances / wall, kind, wall
 
 
+def cpu_stage_timings(nodes: int = 50):
+    """the reference's CPU time of the stages BASELINE configs 2 and 3
+    isolate -- linearize_all (N=50) and pipg_custom with j_max = 2000, j_check = 2001 at the initial
+    guess -- on one core and on all cores (independent instances on a thread pool; ctypes releases
+    the GIL).  Bounded: a few seconds."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import NU as _NU, NX as _NX, CpuOracle, SubArrays, Workspace, ref_available, rocket_shape
+    from paper_2404_18034_b200 import abi, scenario
+
+    cores = os.cpu_count() or 1
+    cpu, kind = (CpuOracle("ptref", fast=True), "reference") if ref_available() else (CpuOracle("ptor"), "port")
+    sc = scenario.default_scenario(nodes)
+    d = sc.problem_desc()
+    shape = rocket_shape(d)
+    ids = list(range(2 * cores))
+    batch = scenario.make_batch(sc, ids)
+
+    def lin(b):
+        return cpu.linearize_all(d, batch["x_guess"][b], batch["u_guess"][b])
+
+    t0 = time.perf_counter()
+    blocks = [lin(b) for b in range(4)]
+    lin_1 = (time.perf_counter() - t0) / 4
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        t0 = time.perf_counter()
+        rest = list(pool.map(lin, ids * 2))
+        lin_all = len(ids) * 2 / (time.perf_counter() - t0)
+    # config 3: subproblem at the initial guess, sigma from the CPU power iteration, cold start
+    cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=2000, j_check=2001, eps_abs=1e-11, eps_rel=1e-11,
+                         eps_buff=0.05)
+    subs = []
+    for b in range(min(cores, len(ids))):
+        rc, blk = rest[b]
+        rc2, sub, _ = cpu.assemble(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b], blk)
+        sx, su = cpu.scp_seed(int(batch["rng_seed"][b]), nodes)
+        z = np.zeros((nodes - 1, _NX))
+        rc3, sigma = cpu.power_iteration(shape, sub, sx, su, z, z, 1e-12, 1e-12, 0.05, 10000)[:2]
+        subs.append((sub, sigma))
+
+    def pipg(i):
+        sub, sigma = subs[i % len(subs)]
+        return cpu.pipg(shape, sub, cfg, sigma, Workspace(_NX, _NU, nodes))
+
+    t0 = time.perf_counter()
+    for i in range(2):
+        pipg(i)
+    pipg_1 = (time.perf_counter() - t0) / 2
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        t0 = time.perf_counter()
+        list(pool.map(pipg, range(2 * cores)))
+        pipg_all = 2 * cores / (time.perf_counter() - t0)
+    return {"kind": kind, "cores": cores, "nodes": nodes,
+            "linearize_all": {"ms_per_call_1_core": 1e3 * lin_1, "calls_per_s_all_cores": lin_all},
+            "pipg_custom_2000_iterations": {"ms_per_solve_1_core": 1e3 * pipg_1,
+                                            "solves_per_s_all_cores": pipg_all}}
+
+
+def cpu_sample_size(args, cores):
+    """B_cpu = 2 * nproc instances on nproc workers."""
+    return args.cpu_instances or 2 * cores
+
+
 def run_reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    inst = args.cpu_instances or cores
+    inst = cpu_sample_size(args, cores)
     walls = []
     kind = "reference"
     for i in range(args.warmup + args.steps):
@@ -197,6 +264,88 @@ def other_configs(device_index, fp64_peak):
     disc_flop, _ = algorithmic_flops(n)
     tf = B * disc_flop / (ms * 1e-3) * 1e-12
     out["config2_discretization_1024xN50"] = {"ms_per_call": ms, "algorithmic_tflops": tf, "frac_fp64_peak": tf / fp64_peak}
+    # single-instance discretization latency (north_star: sub-millisecond): one N=50 instance,
+    # device-resident (CUDA events around 20 calls) and through the host-pointer call (wall clock,
+    # H2D of the iterate and D2H of the blocks included)
+    with Solver(sc.problem_desc(), device=device_index, stream=stream) as s, torch.cuda.stream(stream):
+        x1, u1 = x[:1].contiguous(), u[:1].contiguous()
+        for _ in range(3):
+            s.linearize_all_dev(x1, u1, A[:1], Bm[:1], Bp[:1], w[:1], xe[:1])
+        e0.record(stream)
+        for _ in range(20):
+            s.linearize_all_dev(x1, u1, A[:1], Bm[:1], Bp[:1], w[:1], xe[:1])
+        e1.record(stream)
+        stream.synchronize()
+        dev_ms = e0.elapsed_time(e1) / 20
+        hx, hu = small["x_guess"][:1], small["u_guess"][:1]
+        s.linearize_all(hx, hu)
+        lat = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            s.linearize_all(hx, hu)
+            lat.append(1e3 * (time.perf_counter() - t0))
+    out["single_instance_discretization_N50"] = {
+        "device_ms_per_call": dev_ms, "host_buffers_ms_p50": statistics.median(lat),
+        "what": "linearize_all of ONE N=50 instance (49 intervals x 16 RK4 steps): device-resident inputs "
+                "timed with CUDA events, and ptopt_cuda_linearize_batch with host buffers timed by wall clock "
+                "(the reference takes 26 ms on one core, BASELINE.md section 2)"}
+    # ---- config 3: PIPG only, fixed 2000 iterations (j_check = 2001 disables the stop test), batch
+    #      1024, N=50, subproblems assembled at the initial guess, sigma from the power iteration,
+    #      cold start; device-resident, CUDA events on the handle's stream
+    import ctypes as C
+
+    from paper_2404_18034_b200 import abi
+    from paper_2404_18034_b200.binding import _check, _dp
+    with Solver(sc.problem_desc(), device=device_index, stream=stream) as s, torch.cuda.stream(stream):
+        base = 64
+        blk = s.linearize_all(small["x_guess"], small["u_guess"])
+        sub = s.assemble_subproblem(small["init_state"], small["x_guess"], small["u_guess"], blk)
+        shape = s.subproblem_shape()
+        sx = np.full((base, n, NX), 1.0 / np.sqrt(n * (NX + NU)))
+        su = np.full((base, n, NU), 1.0 / np.sqrt(n * (NX + NU)))
+        zz = np.zeros((base, m, NX))
+        sigma, _, st = s.power_iteration_custom(shape, sub, sx, su, zz, zz, 1e-12, 1e-12, 0.05, 10000)
+        assert (st == 0).all()
+        dsub = {k: torch.from_numpy(np.ascontiguousarray(v[idx])).to(dev) for k, v in sub.items() if v is not None}
+        arrs = abi.SubproblemArrays()
+        for f, _ in abi.SubproblemArrays._fields_:
+            setattr(arrs, f, dsub[f].data_ptr() if f in dsub else None)
+        dsig = torch.from_numpy(sigma[idx]).to(dev)
+        ws = {"x": torch.zeros((B, n, NX), dtype=torch.float64, device=dev),
+              "u": torch.zeros((B, n, NU), dtype=torch.float64, device=dev),
+              "vc_pos": torch.zeros((B, m, NX), dtype=torch.float64, device=dev),
+              "vc_neg": torch.zeros((B, m, NX), dtype=torch.float64, device=dev),
+              "dyn_dual": torch.zeros((B, m, NX), dtype=torch.float64, device=dev),
+              "relax_dual": torch.zeros((B, m), dtype=torch.float64, device=dev)}
+        wsa = abi.WorkspaceArrays()
+        for f, _ in abi.WorkspaceArrays._fields_:
+            setattr(wsa, f, ws[f].data_ptr())
+        cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=2000, j_check=2001, eps_abs=1e-11, eps_rel=1e-11,
+                             eps_buff=0.05)
+        its = torch.zeros(B, dtype=torch.int32, device=dev)
+
+        def pipg_once():
+            for t in ws.values():
+                t.zero_()
+            _check(s.lib.ptopt_cuda_pipg_batch_dev(s._h, C.c_int(B), C.byref(shape), C.byref(arrs), C.byref(cfg),
+                                                   _dp(dsig), C.byref(wsa), _dp(its), None, None, None))
+
+        pipg_once()
+        stream.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            pipg_once()
+        e1.record(stream)
+        stream.synchronize()
+        ms3 = e0.elapsed_time(e1) / 3
+        assert int(its.min()) == 2000 and int(its.max()) == 2000
+    _, op_flop = algorithmic_flops(n)
+    tf3 = B * 2000 * op_flop / (ms3 * 1e-3) * 1e-12
+    out["config3_pipg_2000_iterations_1024xN50"] = {
+        "ms_per_call": ms3, "solves_per_s": B / (ms3 * 1e-3), "algorithmic_tflops": tf3,
+        "frac_fp64_peak": tf3 / fp64_peak,
+        "what": "pipg_custom only, j_max = 2000 with the stop test disabled, cold start, 1024 subproblems "
+                "assembled at the initial guess (64 distinct, tiled), device-resident"}
     # ---- config 5 shape
     n, B = 100, 296
     sc = scenario.default_scenario(n)
@@ -399,10 +548,11 @@ def run_own_arm(args):
         kernel_of = {"linearize": "column_pass_kernel", "power_iteration": "power_fast_kernel",
                      "pipg": "pipg_fast_kernel"}
         tpath = ROOT / "profiles" / "ncu_traffic.json"
-        if tpath.exists() and n == 50:
-            tk = json.loads(tpath.read_text())["kernels"].get(kernel_of[dom])
+        if tpath.exists() and n in (50, 100):
+            tj = json.loads(tpath.read_text())
+            tk = (tj["kernels"] if n == 50 else tj.get("kernels_n100", {}).get("kernels", {})).get(kernel_of[dom])
             if tk:
-                per_instance = (tk["dram_read_bytes"] + tk["dram_write_bytes"]) / 148.0
+                per_instance = (tk["dram_read_bytes"] + tk["dram_write_bytes"]) / float(tk.get("instances", 148))
                 traffic = per_instance * B
         m_int = n - 1
         compulsory = {"linearize": B * (n * 22 + m_int * 465) * 8,
@@ -456,7 +606,11 @@ def run_own_arm(args):
                 "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": "DFMA microbenchmark measured in this run (MEASURED_PEAKS.json has "
                                "no fp64 entry)",
-                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, scaled from a "
+                "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of a "
+                                  "committed ncu --set full capture (148 instances, first launch), scaled to "
+                                  "this batch; not re-measured in this run",
+                "traffic_unit": "bytes per launch (ncu dram read+write, scaled from a "
                                                     "148-instance capture)",
                 "compulsory_hbm_bytes_per_launch": compulsory[dom],
                 "per_stage": {k: {"tflops": flop[k] / (stages[k] * 1e-3) * 1e-12,
@@ -470,12 +624,19 @@ def run_own_arm(args):
             line["other_configs"] = other_configs(local_rank, fp64_peak)
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            inst = args.cpu_instances or cores
+            inst = cpu_sample_size(args, cores)
             v, kind, wall = cpu_reference_run(n, inst, cores)
+            v1, _, wall1 = cpu_reference_run(n, 1, 1)
             line["cpu_baseline"] = {
                 "value": v, "unit": "solves/s", "cores": cores, "kind": kind,
                 "sample": f"run ids 0..{inst - 1} of the same batch ({inst} full N={n} solves, "
-                          f"mc::run_batch on {cores} threads, {wall:.1f} s)"}
+                          f"mc::run_batch on {cores} threads, {wall:.1f} s)",
+                "workers_1": {"value": v1, "unit": "solves/s", "cores": 1,
+                              "sample": f"run id 0, mc::run_batch with workers = 1, {wall1:.1f} s"},
+                "build": "g++ -O3 -march=x86-64-v3 (AVX2 + FMA): the library is built where /root/reference "
+                         "exists and shipped to the GPU box, so -march=native of the build container is not "
+                         "portable to the box's host CPU",
+                "stages": cpu_stage_timings(n)}
         print(json.dumps(line), flush=True)
     solver.close()
     if use_dist:

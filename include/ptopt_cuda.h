@@ -410,6 +410,28 @@ int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
                          int audit_substeps, ptopt_run_record* records, double* x_out,
                          double* u_out);
 
+/* mc::run_batch over several devices of one node.  The reference's batch entry
+ * owns its parallelism -- a pool of `workers` threads pulling run ids, results
+ * written into slots indexed by run id so the output does not depend on the
+ * worker count (proj/include/ptopt/montecarlo.hpp:153-171).  Here a worker is
+ * one device: the call creates one handle and one host thread per entry of
+ * `devices` (an ordinal may be listed more than once: several handles then share
+ * that GPU), gives entry g the contiguous run ids
+ *   first_run_id + [g*batch/G .. (g+1)*batch/G)      (sizes differ by at most one)
+ * and every thread writes its records (and trajectories, when x_out/u_out are
+ * non-NULL) straight into the caller's arrays at the slots of its run ids, so the
+ * result is bit-identical to one ptopt_cuda_run_batch over the whole range.  No
+ * data-path collective: instances are independent (BASELINE north_star).
+ * `device_ms` (NULL or [n_devices]) receives each worker's wall time of its
+ * ptopt_cuda_run_batch call in milliseconds; the slowest one is the batch time.
+ * An entry whose range is empty (batch < n_devices) does nothing.  The first
+ * failing worker's error becomes the call's error. */
+int ptopt_cuda_run_batch_multi(const ptopt_problem_desc* desc, const double* tau, const int* devices,
+                               int n_devices, int batch, int64_t first_run_id,
+                               const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                               int audit_substeps, ptopt_run_record* records, double* x_out,
+                               double* u_out, double* device_ms);
+
 /* ---- measurement --------------------------------------------------------- */
 
 #define PTOPT_STAGE_COUNT 6

@@ -1621,12 +1621,13 @@ static void solve_instance(batch_job* job, int run_id) { /* montecarlo.hpp:100-1
                       &conv, &fdef, hist, &fail);
   if (!rc) {
     double gmax = 0.0, ytot = 0.0, dy_max = 0.0;
+    /* assigned before the audit runs (montecarlo.hpp:115-118): they survive an audit failure */
+    rec[2] = iters;
+    rec[3] = init[K_MASS] - xo[(n - 1) * NX + K_MASS];
+    rec[4] = fdef;
     rc = ptor_dense_audit(d, job->tau, xo, uo, job->audit_substeps, &gmax, &ytot, dyk);
     if (!rc) {
       rec[1] = conv;
-      rec[2] = iters;
-      rec[3] = init[K_MASS] - xo[(n - 1) * NX + K_MASS];
-      rec[4] = fdef;
       rec[5] = gmax;
       for (int k = 0; k + 1 < n; ++k)
         dy_max = dmax(dy_max, xo[(k + 1) * NX + NX - 1] - xo[k * NX + NX - 1]);

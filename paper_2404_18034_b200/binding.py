@@ -33,7 +33,7 @@ EXPORTS = [
     "ptopt_cuda_generate_batch", "ptopt_cuda_generate_batch_dev",
     "ptopt_cuda_dense_audit_batch", "ptopt_cuda_dense_audit_batch_dev",
     "ptopt_cuda_dense_audit_samples_batch",
-    "ptopt_cuda_run_batch",
+    "ptopt_cuda_run_batch", "ptopt_cuda_run_batch_multi",
     "ptopt_cuda_scp_stage_times", "ptopt_cuda_measure_fp64_peak",
 ]
 
@@ -362,3 +362,26 @@ class Solver:
             self._h, C.c_int(x_guess.shape[0]), _dp(init_state), _dp(x_guess), _dp(u_guess),
             _dp(rng_seed), _dp(x_out), _dp(u_out), _dp(scp_iterations), _dp(converged),
             _dp(final_defect_inf), _dp(history), _dp(power_trips), _dp(status), _dp(fail_index)))
+
+
+def run_batch_multi(desc: abi.ProblemDesc, devices, batch, first_run_id, nominal_init_state, r_low,
+                    r_high, seed, audit_substeps=64, keep_trajectories=False, tau=None,
+                    records=None):
+    """ptopt_cuda_run_batch_multi: mc::run_batch with one worker (handle + host thread) per entry
+    of `devices`, contiguous run-id ranges, records written into their run-id slots.  Returns
+    (records, per-device wall ms) or (records, x, u, per-device wall ms)."""
+    lib = load_library()
+    n = int(desc.nodes)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    rec = np.empty(batch, RECORD_DTYPE) if records is None else records
+    x_out = u_out = None
+    if keep_trajectories:
+        x_out, u_out = np.empty((batch, n, abi.NX)), np.empty((batch, n, abi.NU))
+    ms = np.zeros(len(devices))
+    sp = Solver._spec(r_low, r_high, seed)
+    tau_arr = None if tau is None else _np(tau)
+    _check(lib.ptopt_cuda_run_batch_multi(
+        C.byref(desc), _hp(tau_arr), devs, C.c_int(len(devices)), C.c_int(batch),
+        C.c_int64(first_run_id), _hp(_np(nominal_init_state)), C.byref(sp), C.c_int(audit_substeps),
+        _hp(rec), _hp(x_out), _hp(u_out), _hp(ms)))
+    return (rec, x_out, u_out, ms) if keep_trajectories else (rec, ms)

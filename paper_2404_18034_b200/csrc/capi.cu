@@ -5,6 +5,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -732,6 +734,8 @@ int ptopt_cuda_propagate_interval_batch(ptopt_cuda_handle* h, int batch, const d
   if (steps < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "propagate_interval: steps must be >= 1");
   if (!x_k || !u_k || !u_k1 || !tau_k || !tau_k1 || !A || !Bm || !Bp || !w || !x_end)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "propagate_interval: null array");
+  for (int b = 0; b < batch; ++b)  // discretizer.hpp:29 (also rejects NaN bounds, as the reference's !(a < b) does)
+    if (!(tau_k[b] < tau_k1[b])) return fail(PTOPT_ERR_INVALID_ARGUMENT, "foh_interp: empty interval");
   DeviceGuard guard(h->device);
   if (!guard.ok) return fail(PTOPT_ERR_CUDA, "cudaSetDevice failed");
   const size_t B = (size_t)batch;
@@ -1149,7 +1153,8 @@ int generate_dev(ptopt_cuda_handle* h, int batch, int64_t first_run_id, const do
 
 int audit_dev(ptopt_cuda_handle* h, int batch, int substeps, const double* x, const double* u,
               const int* skip, double* max_pointwise_g, double* interval_y_increase,
-              int32_t* status, int32_t* fail_index, double* samples = nullptr) {
+              int32_t* status, int32_t* fail_index, double* samples = nullptr,
+              const int** fail_key_out = nullptr) {
   if (substeps < 1)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "dense_violation_audit: substeps must be >= 1");
   const size_t B = (size_t)batch, m = (size_t)h->desc.nodes - 1;
@@ -1171,6 +1176,7 @@ int audit_dev(ptopt_cuda_handle* h, int batch, int substeps, const double* x, co
   }
   PT_TRY(device_out(h, R_AKEY, B, &a.fail_key));
   launch_init_fail_key(a.fail_key, batch, h->stream);
+  if (fail_key_out) *fail_key_out = a.fail_key;
   launch_audit(a, max_pointwise_g, status, fail_index, h->stream);
   h->launches += 3;
   PT_CUDA(cudaGetLastError());
@@ -1331,8 +1337,10 @@ int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
   PT_TRY(generate_dev(h, batch, first_run_id, nominal_init_state, spec, di, dxg, dug, ds));
   PT_TRY(scp_solve_common(h, batch, di, dxg, dug, ds, dxo, duo, dit, dcv, dfd, nullptr, nullptr,
                           dst, dfi, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice));
-  PT_TRY(audit_dev(h, batch, audit_substeps, dxo, duo, dst, dpg, nullptr, dst, dfi));
+  const int* audit_key = nullptr;
+  PT_TRY(audit_dev(h, batch, audit_substeps, dxo, duo, dst, dpg, nullptr, dst, dfi, nullptr, &audit_key));
   RecordArgs ra;
+  ra.audit_fail_key = audit_key;
   ra.batch = batch;
   ra.nodes = h->desc.nodes;
   ra.first_run_id = first_run_id;
@@ -1353,6 +1361,54 @@ int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
   PT_TRY(download(h, x_out, dxo, B * n * kNX));
   PT_TRY(download(h, u_out, duo, B * n * kNU));
   PT_CUDA(cudaStreamSynchronize(h->stream));
+  return PTOPT_OK;
+}
+
+int ptopt_cuda_run_batch_multi(const ptopt_problem_desc* desc, const double* tau, const int* devices,
+                               int n_devices, int batch, int64_t first_run_id,
+                               const double* nominal_init_state, const ptopt_dispersion_spec* spec,
+                               int audit_substeps, ptopt_run_record* records, double* x_out,
+                               double* u_out, double* device_ms) {
+  if (!desc || !devices) return fail(PTOPT_ERR_INVALID_ARGUMENT, "run_batch_multi: null argument");
+  if (n_devices < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "run_batch_multi: n_devices must be >= 1");
+  if (batch < 1) return fail(PTOPT_ERR_INVALID_ARGUMENT, "montecarlo.batch_size must be >= 1");
+  if (!records) return fail(PTOPT_ERR_INVALID_ARGUMENT, "run_batch: null records");
+  const size_t n = (size_t)desc->nodes;
+  const int G = n_devices;
+  std::vector<int> rc(G, PTOPT_OK);
+  std::vector<std::string> err(G);
+  std::vector<double> ms(G, 0.0);
+  // handles first, on this thread: a bad description or device fails the call before any work
+  std::vector<ptopt_cuda_handle*> hs(G, nullptr);
+  int created = PTOPT_OK;
+  for (int g = 0; g < G && created == PTOPT_OK; ++g) {
+    const int64_t lo = (int64_t)g * batch / G, hi = (int64_t)(g + 1) * batch / G;
+    if (hi > lo) created = ptopt_cuda_create(desc, tau, devices[g], nullptr, &hs[g]);
+  }
+  if (created == PTOPT_OK) {
+    std::vector<std::thread> pool;
+    for (int g = 0; g < G; ++g) {
+      if (!hs[g]) continue;
+      pool.emplace_back([&, g] {
+        const int64_t lo = (int64_t)g * batch / G, hi = (int64_t)(g + 1) * batch / G;
+        const auto t0 = std::chrono::steady_clock::now();
+        rc[g] = ptopt_cuda_run_batch(hs[g], (int)(hi - lo), first_run_id + lo, nominal_init_state, spec,
+                                     audit_substeps, records + lo, x_out ? x_out + (size_t)lo * n * kNX : nullptr,
+                                     u_out ? u_out + (size_t)lo * n * kNU : nullptr);
+        ms[g] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (rc[g] != PTOPT_OK) err[g] = g_last_error;  // thread-local: carry it to the caller
+      });
+    }
+    for (auto& t : pool) t.join();
+  }
+  const std::string create_err = created == PTOPT_OK ? std::string() : g_last_error;
+  for (auto* h : hs)
+    if (h) ptopt_cuda_destroy(h);
+  if (created != PTOPT_OK) return fail(created, create_err);
+  if (device_ms)
+    for (int g = 0; g < G; ++g) device_ms[g] = ms[g];
+  for (int g = 0; g < G; ++g)
+    if (rc[g] != PTOPT_OK) return fail(rc[g], "device entry " + std::to_string(g) + ": " + err[g]);
   return PTOPT_OK;
 }
 

@@ -272,21 +272,26 @@ __global__ void records_kernel(RecordArgs a) {
   r.reserved_ = 0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) r.initial_position[i] = a.init_state[(size_t)b * kNXI + 1 + i];
-  if (r.status != kStOk) {  // the reference leaves a failed record at its defaults
-    r.converged = 0;
-    r.scp_iterations = 0;
-    r.propellant_used = r.final_defect_inf = r.max_pointwise_g = r.max_node_y_increase = 0.0;
-  } else {
+  // montecarlo.hpp:115-132: a throw inside scp_solve leaves the record at its defaults; a throw
+  // inside the dense audit comes after scp_iterations, final_defect_inf and propellant_used were
+  // assigned, so those stay and only `converged` is cleared.
+  const bool audit_failed = r.status != kStOk && a.audit_fail_key && a.audit_fail_key[b] != kFailKeyNone;
+  r.converged = 0;
+  r.scp_iterations = 0;
+  r.propellant_used = r.final_defect_inf = r.max_pointwise_g = r.max_node_y_increase = 0.0;
+  if (r.status == kStOk || audit_failed) {
     const double* x = a.x + (size_t)b * a.nodes * kNX;
-    r.converged = a.converged[b] ? 1 : 0;
     r.scp_iterations = a.scp_iterations[b];
     r.final_defect_inf = a.final_defect[b];
     r.propellant_used = a.init_state[(size_t)b * kNXI] - x[(size_t)(a.nodes - 1) * kNX];
-    r.max_pointwise_g = a.max_pointwise_g[b];
-    double dy_max = 0.0;
-    for (int k = 0; k + 1 < a.nodes; ++k)
-      dy_max = fmax(dy_max, x[(size_t)(k + 1) * kNX + kNX - 1] - x[(size_t)k * kNX + kNX - 1]);
-    r.max_node_y_increase = dy_max;
+    if (!audit_failed) {
+      r.converged = a.converged[b] ? 1 : 0;
+      r.max_pointwise_g = a.max_pointwise_g[b];
+      double dy_max = 0.0;
+      for (int k = 0; k + 1 < a.nodes; ++k)
+        dy_max = fmax(dy_max, x[(size_t)(k + 1) * kNX + kNX - 1] - x[(size_t)k * kNX + kNX - 1]);
+      r.max_node_y_increase = dy_max;
+    }
   }
   a.records[b] = r;
 }

@@ -154,7 +154,7 @@ inline void check_call(int rc) {
   switch (status) {
     case PTOPT_ST_PROPAGATION_DIVERGED: throw PropagationDiverged(fail_index);
     case PTOPT_ST_SOLVER_DIVERGED: throw pipg::SolverDiverged(fail_index);
-    case PTOPT_ST_DILATION_NONPOSITIVE: throw std::domain_error("dilation factor must be positive");
+    case PTOPT_ST_DILATION_NONPOSITIVE: throw std::domain_error("augmented dynamics: dilation factor must be positive");  // ctcs.hpp:66
     case PTOPT_ST_MASS_NONPOSITIVE: throw std::domain_error("rocket dynamics: nonpositive mass");
     case PTOPT_ST_THRUST_SINGULAR:
       throw std::domain_error("rocket jacobians: thrust magnitude below singular-point tolerance");
@@ -682,7 +682,8 @@ PipgResult pipg_custom(const Sub& sp, const Cfg& cfg, Ws& ws) {
   cfg.validate();
   if (ws.n_x != sp.n_x || ws.n_u != sp.n_u || ws.nodes != sp.nodes)
     throw std::invalid_argument("pipg: workspace shape does not match the subproblem");
-  if (!(ws.sigma > 0.0)) throw std::invalid_argument("pipg: workspace sigma must be set by the power iteration");
+  // the reference accepts any sigma (Workspace::init leaves 0, and the power iteration returns 0
+  // for an iterate in the operator's null space, pipg.hpp:280-284): alpha = 1 / w_prox then
   const detail::FlatSub f = detail::flatten(sp, true);
   const int n = sp.nodes, m = n - 1, nx = sp.n_x, nu = sp.n_u;
   std::vector<double> x = detail::flatten_group(ws.x, n, nx), u = detail::flatten_group(ws.u, n, nu);
@@ -1020,6 +1021,54 @@ struct BatchResult {  // montecarlo.hpp:80-85
   int workers = 0;
 };
 
+namespace detail {
+
+template <class Spec>
+inline ptopt_dispersion_spec to_c_spec(const Spec& spec) {
+  ptopt_dispersion_spec cs{};
+  for (int i = 0; i < 3; ++i) {
+    cs.r_low[i] = spec.r_low[static_cast<std::size_t>(i)];
+    cs.r_high[i] = spec.r_high[static_cast<std::size_t>(i)];
+  }
+  cs.seed = spec.seed;
+  return cs;
+}
+
+/// ptopt_run_record[] (+ flat trajectories) -> BatchResult, montecarlo.hpp:67-85.
+inline BatchResult to_batch_result(const std::vector<ptopt_run_record>& rec, const std::vector<double>& xo,
+                                   const std::vector<double>& uo, int n, bool keep_trajectories, int workers,
+                                   double wall_s) {
+  BatchResult out;
+  out.workers = workers;
+  out.total_wall_time = wall_s;
+  out.records.resize(rec.size());
+  if (keep_trajectories) out.trajectories.resize(rec.size());
+  for (std::size_t b = 0; b < rec.size(); ++b) {
+    RunRecord& r = out.records[b];
+    r.run_id = rec[b].run_id;
+    for (int i = 0; i < 3; ++i) r.initial_position[static_cast<std::size_t>(i)] = rec[b].initial_position[i];
+    r.converged = rec[b].converged != 0;
+    r.scp_iterations = rec[b].scp_iterations;
+    r.propellant_used = rec[b].propellant_used;
+    r.final_defect_inf = rec[b].final_defect_inf;
+    r.max_pointwise_g = rec[b].max_pointwise_g;
+    r.max_node_y_increase = rec[b].max_node_y_increase;
+    if (rec[b].status != PTOPT_ST_OK) r.failure = ptopt_b200::detail::failure_text(rec[b].status, rec[b].fail_index);
+    r.wall_time = wall_s / static_cast<double>(rec.size());
+    if (keep_trajectories && rec[b].status == PTOPT_ST_OK) {
+      RocketTrajectory z(n);
+      for (int k = 0; k < n; ++k) {
+        for (int i = 0; i < kNX; ++i) z.x[static_cast<std::size_t>(k)][i] = xo[(b * n + k) * kNX + i];
+        for (int i = 0; i < kNU; ++i) z.u[static_cast<std::size_t>(k)][i] = uo[(b * n + k) * kNU + i];
+      }
+      out.trajectories[b] = std::move(z);
+    }
+  }
+  return out;
+}
+
+}  // namespace detail
+
 /// run_batch (montecarlo.hpp:140-175): instance generation, solve, audit and records all on
 /// the device, one CTA per instance.  `workers` is validated and echoed only; `first_run_id`
 /// (an extension) lets several GPUs / processes take disjoint run-id ranges of one batch.
@@ -1035,12 +1084,7 @@ BatchResult run_batch(const Problem& nominal, const Boundary& nominal_bc, const 
   const auto init = nominal_bc.initial.to_vec();
   double nominal_init[kNXI];
   for (int i = 0; i < kNXI; ++i) nominal_init[i] = init[i];
-  ptopt_dispersion_spec cs{};
-  for (int i = 0; i < 3; ++i) {
-    cs.r_low[i] = spec.r_low[static_cast<std::size_t>(i)];
-    cs.r_high[i] = spec.r_high[static_cast<std::size_t>(i)];
-  }
-  cs.seed = spec.seed;
+  const ptopt_dispersion_spec cs = detail::to_c_spec(spec);
   std::vector<ptopt_run_record> rec(static_cast<std::size_t>(batch_size));
   std::vector<double> xo, uo;
   if (keep_trajectories) {
@@ -1051,33 +1095,43 @@ BatchResult run_batch(const Problem& nominal, const Boundary& nominal_bc, const 
   ptopt_b200::detail::check_call(ptopt_cuda_run_batch(h, batch_size, first_run_id, nominal_init, &cs, audit_substeps,
                                                       rec.data(), keep_trajectories ? xo.data() : nullptr,
                                                       keep_trajectories ? uo.data() : nullptr));
-  BatchResult out;
-  out.workers = workers;
-  out.total_wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  out.records.resize(rec.size());
-  if (keep_trajectories) out.trajectories.resize(rec.size());
-  for (std::size_t b = 0; b < rec.size(); ++b) {
-    RunRecord& r = out.records[b];
-    r.run_id = rec[b].run_id;
-    for (int i = 0; i < 3; ++i) r.initial_position[static_cast<std::size_t>(i)] = rec[b].initial_position[i];
-    r.converged = rec[b].converged != 0;
-    r.scp_iterations = rec[b].scp_iterations;
-    r.propellant_used = rec[b].propellant_used;
-    r.final_defect_inf = rec[b].final_defect_inf;
-    r.max_pointwise_g = rec[b].max_pointwise_g;
-    r.max_node_y_increase = rec[b].max_node_y_increase;
-    if (rec[b].status != PTOPT_ST_OK) r.failure = ptopt_b200::detail::failure_text(rec[b].status, rec[b].fail_index);
-    r.wall_time = out.total_wall_time / batch_size;
-    if (keep_trajectories && rec[b].status == PTOPT_ST_OK) {
-      RocketTrajectory z(n);
-      for (int k = 0; k < n; ++k) {
-        for (int i = 0; i < kNX; ++i) z.x[static_cast<std::size_t>(k)][i] = xo[(b * n + k) * kNX + i];
-        for (int i = 0; i < kNU; ++i) z.u[static_cast<std::size_t>(k)][i] = uo[(b * n + k) * kNU + i];
-      }
-      out.trajectories[b] = std::move(z);
-    }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return detail::to_batch_result(rec, xo, uo, n, keep_trajectories, workers, wall);
+}
+
+/// run_batch over the listed devices of this node: the reference's worker pool
+/// (montecarlo.hpp:153-171) with one worker per device.  Entry g of `devices` solves the
+/// contiguous run ids [g*batch/G, (g+1)*batch/G) on its own handle and host thread and writes
+/// into the record slots of those ids, so the result equals the single-device batch bit for
+/// bit whatever the device list (an ordinal may repeat).  `workers` of the result is the
+/// number of device entries.
+template <class Problem, class Boundary, class Spec>
+BatchResult run_batch(const Problem& nominal, const Boundary& nominal_bc, const Spec& spec, int batch_size,
+                      const std::vector<int>& devices, int audit_substeps = 64, bool keep_trajectories = false,
+                      std::int64_t first_run_id = 0, std::vector<double>* device_ms = nullptr) {
+  if (batch_size < 1) throw std::invalid_argument("montecarlo.batch_size must be >= 1");
+  if (devices.empty()) throw std::invalid_argument("montecarlo.workers must be >= 1");
+  const int n = static_cast<int>(nominal.grid.nodes.size());
+  const ptopt_problem_desc d = ptopt_b200::detail::to_desc(nominal);
+  const auto init = nominal_bc.initial.to_vec();
+  double nominal_init[kNXI];
+  for (int i = 0; i < kNXI; ++i) nominal_init[i] = init[i];
+  const ptopt_dispersion_spec cs = detail::to_c_spec(spec);
+  std::vector<ptopt_run_record> rec(static_cast<std::size_t>(batch_size));
+  std::vector<double> xo, uo;
+  if (keep_trajectories) {
+    xo.resize(static_cast<std::size_t>(batch_size) * n * kNX);
+    uo.resize(static_cast<std::size_t>(batch_size) * n * kNU);
   }
-  return out;
+  std::vector<double> tau(nominal.grid.nodes.begin(), nominal.grid.nodes.end());
+  if (device_ms) device_ms->assign(devices.size(), 0.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  ptopt_b200::detail::check_call(ptopt_cuda_run_batch_multi(
+      &d, tau.data(), devices.data(), static_cast<int>(devices.size()), batch_size, first_run_id, nominal_init, &cs,
+      audit_substeps, rec.data(), keep_trajectories ? xo.data() : nullptr, keep_trajectories ? uo.data() : nullptr,
+      device_ms ? device_ms->data() : nullptr));
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return detail::to_batch_result(rec, xo, uo, n, keep_trajectories, static_cast<int>(devices.size()), wall);
 }
 
 }  // namespace mc

@@ -71,14 +71,21 @@ def max_over_ranks(value: float, group=None) -> float:
     return float(t[0])
 
 
-def run_batch_sharded(run_fn, total: int, group=None, dst: int = 0):
+def run_batch_sharded(run_fn, total: int, group=None, dst: int = 0, dtype=None):
     """mc::run_batch over all ranks: rank r solves run ids shard_range(total, world, r) with
     `run_fn(count, first_run_id) -> records` (e.g. ``Solver.run_batch`` bound to this rank's
-    GPU) and the records are gathered on `dst` in run-id order."""
+    GPU) and the records are gathered on `dst` in run-id order.  A rank whose range is empty
+    (total < world size) contributes an empty array of `dtype` (default: the run-record dtype)
+    without calling `run_fn`."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     first, count = shard_range(total, world, rank)
-    local = run_fn(count, first)
+    if count == 0:
+        if dtype is None:
+            from .binding import RECORD_DTYPE as dtype
+        local = np.empty(0, dtype=dtype)
+    else:
+        local = run_fn(count, first)
     return gather_records(local, total, group=group, dst=dst)

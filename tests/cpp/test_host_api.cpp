@@ -247,6 +247,52 @@ int main() {
   }
   CHECK(worst <= 1e-6);
   std::printf("power_iteration_custom / pipg_custom ok (sigma %.12f, max |diff| %.2e)\n", sigma, worst);
+  {
+    // sigma = 0 is a valid workspace (Workspace::init leaves it at 0, and the power iteration returns
+    // 0 for an iterate in the operator's null space, pipg.hpp:280-284): alpha = 1 / w_prox, no throw
+    pb::pipg::Workspace ws0;
+    ws0.init(15, 7, n);
+    ws0.sigma = 0.0;
+    pb::pipg::PipgConfig c0;
+    c0.j_max = 10;
+    c0.j_check = 5;
+    std::vector<double> zx(n * 15, 0.0), zu(n * 7, 0.0), zvp(m * 15, 0.0), zvn(m * 15, 0.0), zdd(m * 15, 0.0), zrd(m, 0.0);
+    ptopt_workspace_arrays zw{zx.data(), zu.data(), zvp.data(), zvn.data(), zdd.data(), zrd.data()};
+    const ptopt_pipg_config cc0{c0.omega, c0.rho, c0.j_max, c0.j_check, c0.eps_abs, c0.eps_rel, c0.eps_buff};
+    int it0 = 0, cv0 = 0, fl0 = -1;
+    const int rc0 = ptor_pipg(&shape, &arr, &cc0, 0.0, &zw, &it0, &cv0, &fl0);
+    double w0 = 0.0, scale = 1.0;
+    if (rc0 == 0) {
+      const pb::pipg::PipgResult r0 = pb::pipg::pipg_custom(sp, c0, ws0);
+      CHECK(r0.iterations == it0 && r0.converged == (cv0 != 0));
+      for (int k = 0; k < n; ++k)
+        for (int i = 0; i < 15; ++i) {
+          w0 = std::fmax(w0, std::fabs(ws0.x[k][i] - zx[k * 15 + i]));
+          scale = std::fmax(scale, std::fabs(zx[k * 15 + i]));
+        }
+      CHECK(w0 <= 1e-9 * scale);
+    } else {  // steps this large may blow up: then both sides report SolverDiverged at the same check
+      CHECK(rc0 == PTOPT_ST_SOLVER_DIVERGED);
+      int at = -1;
+      try {
+        pb::pipg::pipg_custom(sp, c0, ws0);
+      } catch (const pb::pipg::SolverDiverged& e) {
+        at = e.iteration;
+      }
+      CHECK(at == fl0);
+    }
+    std::printf("pipg_custom with sigma = 0 ok (%d iterations, max |diff| %.2e, |x| %.2e)\n", it0, w0, scale);
+  }
+  {
+    // the texts RunRecord::failure carries are the reference's exception messages
+    CHECK(ptopt_b200::detail::failure_text(PTOPT_ST_DILATION_NONPOSITIVE, 0) ==
+          "augmented dynamics: dilation factor must be positive");                       // ctcs.hpp:66
+    CHECK(ptopt_b200::detail::failure_text(PTOPT_ST_MASS_NONPOSITIVE, 0) == "rocket dynamics: nonpositive mass");
+    CHECK(ptopt_b200::detail::failure_text(PTOPT_ST_THRUST_SINGULAR, 0) ==
+          "rocket jacobians: thrust magnitude below singular-point tolerance");           // rocket6dof.hpp:307
+    CHECK(ptopt_b200::detail::failure_text(PTOPT_ST_POWER_SEED_ZERO, 0) ==
+          "power iteration: seed point must not be all zero");                            // pipg.hpp:225
+  }
 
   // ---- scp_solve
   const pb::ScpResult sr = pb::scp_solve(prob, z);
@@ -304,6 +350,26 @@ int main() {
         for (int i = 0; i < 15; ++i)
           wdiff = std::fmax(wdiff, std::fabs(br.trajectories[b].x[k][i] - bx[(b * n + k) * 15 + i]));
       CHECK(wdiff <= 1e-6);
+    }
+    // the same batch over a device list (two handles + two host threads on device 0; three entries
+    // for a batch of two leaves one worker without work): bit-identical records and trajectories
+    for (const std::vector<int>& devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0}}) {
+      const int Bm = devs.size() == 2 ? B : 2;
+      std::vector<double> ms;
+      const pb::mc::BatchResult bm = pb::mc::run_batch(prob, default_boundary(), spec, Bm, devs, 16, true, 0, &ms);
+      CHECK((int)bm.records.size() == Bm && bm.workers == (int)devs.size() && ms.size() == devs.size());
+      for (int b = 0; b < Bm; ++b) {
+        const auto &r = bm.records[b], &q = br.records[b];
+        CHECK(r.run_id == q.run_id && r.converged == q.converged && r.scp_iterations == q.scp_iterations);
+        CHECK(r.propellant_used == q.propellant_used && r.final_defect_inf == q.final_defect_inf);
+        CHECK(r.max_pointwise_g == q.max_pointwise_g && r.max_node_y_increase == q.max_node_y_increase);
+        bool same = true;
+        for (int k = 0; k < n; ++k) {
+          for (int i = 0; i < 15; ++i) same = same && bm.trajectories[b].x[k][i] == br.trajectories[b].x[k][i];
+          for (int i = 0; i < 7; ++i) same = same && bm.trajectories[b].u[k][i] == br.trajectories[b].u[k][i];
+        }
+        CHECK(same);
+      }
     }
     bool caught = false;
     try {

@@ -880,3 +880,30 @@ def test_scp_converged_early_exit_mixed_batch(solver15, ptor):
     assert len(set(its)) >= 4 and min(its) < 12          # different exit iterations ...
     assert sum(conv) >= 6 and sum(not c for c in conv) >= 2  # ... and some that never converge
     assert [bool(c) for c in out["converged"]] == conv
+
+
+def test_run_batch_multi_device_list_is_bit_identical():
+    """ptopt_cuda_run_batch_multi (the reference's worker pool, montecarlo.hpp:153-171, with one
+    worker per device entry): two and three handles on device 0, each with its own host thread and
+    contiguous run-id range, reproduce the single-handle batch bit for bit -- records written into
+    their run-id slots, trajectories too; an entry with an empty range is skipped; a bad device
+    ordinal fails the call."""
+    from paper_2404_18034_b200.binding import PtoptError, Solver, run_batch_multi
+
+    sc = scenario.default_scenario(11)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max, sc.audit_substeps = 3, 150, 200, 8
+    d = sc.problem_desc()
+    spec = sc.dispersion
+    B, first = 9, 40
+    with Solver(d) as s:
+        rec, x, u = s.run_batch(B, first, sc.initial_state, spec.r_low, spec.r_high, spec.seed,
+                                audit_substeps=8, keep_trajectories=True)
+    for devices, batch in (([0, 0], B), ([0, 0, 0], B), ([0, 0, 0], 2)):
+        rm, xm, um, ms = run_batch_multi(d, devices, batch, first, sc.initial_state, spec.r_low, spec.r_high,
+                                         spec.seed, audit_substeps=8, keep_trajectories=True)
+        assert rm.tobytes() == rec[:batch].tobytes()
+        np.testing.assert_array_equal(xm, x[:batch])
+        np.testing.assert_array_equal(um, u[:batch])
+        assert len(ms) == len(devices) and (ms > 0).sum() == min(batch, len(devices))
+    with pytest.raises(PtoptError):
+        run_batch_multi(d, [0, 99], B, first, sc.initial_state, spec.r_low, spec.r_high, spec.seed)

@@ -62,7 +62,7 @@ dist.destroy_process_group()
 '''
 
 
-@pytest.mark.parametrize("total", [9, 16])
+@pytest.mark.parametrize("total", [1, 9, 16])  # 1: rank 1 has an empty range
 def test_two_rank_gloo_gather_matches_single_process(tmp_path, total):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

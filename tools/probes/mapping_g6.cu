@@ -42,10 +42,11 @@ struct Lay {
   static constexpr int php = uin + kNodes * kP;       // phi_k          [node][15]
   static constexpr int csp = php + kNodes * kP;       // column sums of the ch-1 lanes [node][15]
   static constexpr int red = csp + kNodes * kP;
-  static constexpr int total = red + 32;
+  static constexpr int opx = red + 32;                 // thread-private operator overflow: entry e at opx[e * kThreads + tid]
+  static constexpr int total = opx;
 };
 
-template <int ABL>
+template <int ABL, int CS = 0>
 __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma_out, long long* clk_out) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -55,8 +56,12 @@ __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma
   const int k = idle ? kN + 1 : 5 * warp + p;  // idle lanes: scratch node
   const bool node = !idle && k < kN, ival = !idle && k < kM;
   const int gid = blockIdx.x;
-  for (int e = tid; e < Lay::total; e += kThreads) sm[e] = 0.0;
+  for (int e = tid; e < Lay::total + 5 * CS * kThreads; e += kThreads) sm[e] = 0.0;
   __syncthreads();
+  // CS > 0: the last CS column slots of group 2 live in thread-private shared memory, not in registers
+  double* opx = sm + Lay::opx + tid;
+  auto in_smem = [](int g, int i) { return g == 2 && i >= 5 - CS; };
+  auto opx_at = [&](int r, int i) -> double& { return opx[(5 * (i - (5 - CS)) + r) * kThreads]; };
   // operator block: rows 5rg..5rg+4, column slot (g, i) <-> column 5 * ((rg + g) % 3) + i of this half
   double a[5][3][5];
 #pragma unroll
@@ -68,6 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma
         const int c = 5 * ((rg + g) % 3) + i;  // 0..14 inside the half
         double v = 0.0;
         if (ival && (ch == 0 || c < 14)) v = op_entry(gid, k, 5 * rg + r, ch == 0 ? c : 15 + c);
+        if (in_smem(g, i)) { opx_at(r, i) = v; v = 0.0; }
         a[r][g][i] = v;
       }
   // per-thread addresses
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma
 #pragma unroll
       for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int i = 0; i < 5; ++i) acc[r] = fma(a[r][g][i], v[i], acc[r]);
+        for (int i = 0; i < 5; ++i) acc[r] = fma(in_smem(g, i) ? opx_at(r, i) : a[r][g][i], v[i], acc[r]);
     }
     double ph[5];
 #pragma unroll
@@ -128,12 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma
     double cs[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      double q0 = a[0][0][i] * ph[0], q1 = a[0][1][i] * ph[0], q2 = a[0][2][i] * ph[0];
+      double q0 = a[0][0][i] * ph[0], q1 = a[0][1][i] * ph[0], q2 = (in_smem(2, i) ? opx_at(0, i) : a[0][2][i]) * ph[0];
 #pragma unroll
       for (int r = 1; r < 5; ++r) {
         q0 = fma(a[r][0][i], ph[r], q0);
         q1 = fma(a[r][1][i], ph[r], q1);
-        q2 = fma(a[r][2][i], ph[r], q2);
+        q2 = fma(in_smem(2, i) ? opx_at(r, i) : a[r][2][i], ph[r], q2);
       }
       const double r1 = (ABL & 2) ? q1 : __shfl_sync(0xffffffffu, q1, prev_lane);
       const double r2 = (ABL & 2) ? q2 : __shfl_sync(0xffffffffu, q2, next_lane);
@@ -176,10 +182,10 @@ __global__ void __launch_bounds__(kThreads, 1) trips_g6(int iters, double* sigma
   }
 }
 
-template <int ABL>
+template <int ABL, int CS = 0>
 void run(const char* name, int iters, double* d_sigma, long long* d_clk, double* ref) {
-  const size_t smem = (size_t)Lay::total * sizeof(double);
-  auto kern = trips_g6<ABL>;
+  const size_t smem = (size_t)(Lay::total + 5 * CS * kThreads) * sizeof(double);
+  auto kern = trips_g6<ABL, CS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = 148;
   kern<<<grid, kThreads, smem>>>(iters, d_sigma, d_clk);
@@ -205,6 +211,9 @@ int main() {
   static double ref[148] = {0};
   const int iters = 3000;
   run<0>("g6: 6 threads per node, shuffle reductions", iters, d_sigma, d_clk, ref);
+  run<0, 2>("g6, 10 of 75 operator entries in shared memory", iters, d_sigma, d_clk, ref);
+  run<0, 3>("g6, 15 of 75 operator entries in shared memory", iters, d_sigma, d_clk, ref);
+  run<0, 5>("g6, 25 of 75 operator entries in shared memory", iters, d_sigma, d_clk, ref);
   run<16>("g6, forward loads removed", iters, d_sigma, d_clk, ref);
   run<32>("g6, x_{k+1} loads removed", iters, d_sigma, d_clk, ref);
   run<1>("g6, xor-16 exchange removed", iters, d_sigma, d_clk, ref);

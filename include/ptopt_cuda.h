@@ -206,19 +206,28 @@ int ptopt_cuda_create(const ptopt_problem_desc* desc, const double* tau, int dev
                       ptopt_cuda_handle** out);
 int ptopt_cuda_destroy(ptopt_cuda_handle* h);
 /* Kernel family used for power iteration and PIPG.  No reference counterpart.
- *   AUTO       register-resident kernels for the rocket-shaped subproblem (n_x = 15, n_u = 7,
- *              A_plus = -I, e_y = last state): one CTA per instance up to 51 nodes, a 2-CTA
- *              cluster up to 102; the shape-generic kernels for every other shape.
+ *   AUTO       for the rocket-shaped subproblem (n_x = 15, n_u = 7, A_plus = -I, e_y = last
+ *              state): the latency-mode kernels whenever the whole batch fits the chip in one
+ *              wave (batch x cluster size <= SM count, i.e. up to 18 / 37 / 74 instances with
+ *              8 / 4 / 2 CTAs per instance), else the throughput kernels; the shape-generic
+ *              kernels for every other shape.
  *   GENERIC    forces the shape-generic kernels (the parity tests run every family on the same
  *              inputs).
- *   FAST_SPLIT register-resident kernels with every instance of 4..50 nodes shared by a 2-CTA
+ *   FAST_SPLIT throughput kernels with every instance of 4..50 nodes shared by a 2-CTA
  *              cluster of 128-thread CTAs, two CTAs (halves of different instances) resident per
- *              SM; other node counts run as under AUTO.  Experimental: on B200 it is slower
- *              than AUTO (the flight time of the boundary values costs more than the overlap
- *              gains). */
+ *              SM; other node counts run as under FAST_THROUGHPUT.  Experimental: slower than
+ *              FAST_THROUGHPUT on B200.
+ *   FAST_LATENCY    latency mode whatever the batch size: one instance spread over a cluster of
+ *              up to eight CTAs, sixteen threads per node (a short dependent instruction
+ *              stream per thread); up to 128 nodes.  Lowest single-solve latency, lower
+ *              throughput per SM.
+ *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size: five threads
+ *              per node, one CTA per instance up to 51 nodes, a 2-CTA cluster up to 102. */
 #define PTOPT_SOLVER_AUTO 0
 #define PTOPT_SOLVER_GENERIC 1
 #define PTOPT_SOLVER_FAST_SPLIT 2
+#define PTOPT_SOLVER_FAST_LATENCY 3
+#define PTOPT_SOLVER_FAST_THROUGHPUT 4
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path);
 /* Blocks until all work enqueued on the handle's stream has finished. */
 int ptopt_cuda_synchronize(ptopt_cuda_handle* h);

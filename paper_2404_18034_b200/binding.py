@@ -134,9 +134,12 @@ class Solver:
         self.close()
 
     def set_solver_path(self, path: str):
-        """'auto' (register-resident kernels where the shape allows; split variant for small
-        batches), 'generic' (shape-generic kernels) or 'split' (PTOPT_SOLVER_FAST_SPLIT)."""
-        _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int({"auto": 0, "generic": 1, "split": 2}[path])))
+        """'auto' (latency-mode kernels when the batch fits the chip in one wave, else the
+        throughput kernels; generic kernels for non-rocket shapes), 'generic', 'split'
+        (PTOPT_SOLVER_FAST_SPLIT), 'latency' (PTOPT_SOLVER_FAST_LATENCY) or 'fast'
+        (PTOPT_SOLVER_FAST_THROUGHPUT)."""
+        code = {"auto": 0, "generic": 1, "split": 2, "latency": 3, "fast": 4}[path]
+        _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int(code)))
         self.solver_path = path
 
     def synchronize(self):

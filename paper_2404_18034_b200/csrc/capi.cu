@@ -94,6 +94,11 @@ struct ptopt_cuda_handle {
   bool stage_times_valid = false;
   int solver_path = PTOPT_SOLVER_AUTO;
   int num_sms = 0;
+  // mc::run_batch promises records that do not depend on how a batch is sharded (run ids are all
+  // that matter), so under AUTO it always runs the throughput family: the latency kernels round
+  // differently, and choosing them by batch size would make a shard's bits depend on its size.
+  bool batch_entry = false;
+  int scp_graph_lat = -1;  // latency cluster size the cached SCP graph was captured with
 };
 
 namespace {
@@ -244,6 +249,14 @@ bool use_split_solver(const ptopt_cuda_handle* h, int /*batch*/) {
   return h->solver_path == PTOPT_SOLVER_FAST_SPLIT;
 }
 
+/// Cluster size of the latency-mode kernels (solver_lat.cu) for this launch, 0 = not used: forced
+/// by PTOPT_SOLVER_FAST_LATENCY, chosen under AUTO when the whole batch fits the chip in one wave.
+int latency_ranks(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus, int batch) {
+  if (h->solver_path == PTOPT_SOLVER_FAST_LATENCY) return solver_lat_ranks(s, has_a_plus, 0, h->num_sms);
+  if (h->solver_path == PTOPT_SOLVER_AUTO && !h->batch_entry) return solver_lat_ranks(s, has_a_plus, batch, h->num_sms);
+  return 0;
+}
+
 int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
   if (fast) {
     PT_TRY(check_smem(h, pipg_fast_smem(s, false)));
@@ -256,6 +269,11 @@ int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
 }
 
 int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
+  if (const int ranks = latency_ranks(h, a.shape, a.sp.A_plus != nullptr, a.batch)) {
+    PT_CUDA(launch_power_lat(a, ranks, h->stream));
+    h->launches += 1;
+    return PTOPT_OK;
+  }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
   PT_CUDA(fast ? launch_power_fast(a, use_split_solver(h, a.batch), h->stream) : launch_power_generic(a, h->stream));
@@ -264,6 +282,11 @@ int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
 }
 
 int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
+  if (const int ranks = latency_ranks(h, a.shape, a.sp.A_plus != nullptr, a.batch)) {
+    PT_CUDA(launch_pipg_lat(a, ranks, h->stream));
+    h->launches += 1;
+    return PTOPT_OK;
+  }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
   PT_CUDA(fast ? launch_pipg_fast(a, use_split_solver(h, a.batch), h->stream) : launch_pipg_generic(a, h->stream));
@@ -438,6 +461,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   PT_TRY(linearize_args(h, batch, h->desc.nodes, h->desc.integrator_steps, st.zx, st.zu, st.A, st.Bm, st.Bp,
                         st.w, st.x_end, st.fail_key, st.active, S_STAGES, &la));
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
+  const int lat = latency_ranks(h, h->rocket_shape, false, batch);
   for (int it = 0; it <= h->desc.max_iters; ++it) {
     kernels += launch_linearize(la, h->stream);
     PT_CUDA(mark(0));
@@ -445,9 +469,13 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 1;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    PT_CUDA(fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream) : launch_power_generic(pa, h->stream));
+    PT_CUDA(lat    ? launch_power_lat(pa, lat, h->stream)
+            : fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream)
+                   : launch_power_generic(pa, h->stream));
     PT_CUDA(mark(2));
-    PT_CUDA(fast ? launch_pipg_fast(ga, use_split_solver(h, batch), h->stream) : launch_pipg_generic(ga, h->stream));
+    PT_CUDA(lat    ? launch_pipg_lat(ga, lat, h->stream)
+            : fast ? launch_pipg_fast(ga, use_split_solver(h, batch), h->stream)
+                   : launch_pipg_generic(ga, h->stream));
     PT_CUDA(mark(3));
     launch_scp_update(sa, h->stream);
     PT_CUDA(mark(4));
@@ -459,7 +487,8 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
 }
 
 int ensure_scp_graph(ptopt_cuda_handle* h, int batch, const ScpState& st) {
-  if (h->scp_graph && h->scp_graph_batch == batch) return PTOPT_OK;
+  const int lat = latency_ranks(h, h->rocket_shape, false, batch);
+  if (h->scp_graph && h->scp_graph_batch == batch && h->scp_graph_lat == lat) return PTOPT_OK;
   if (h->scp_graph) {
     cudaGraphExecDestroy(h->scp_graph);
     h->scp_graph = nullptr;
@@ -481,6 +510,7 @@ int ensure_scp_graph(ptopt_cuda_handle* h, int batch, const ScpState& st) {
   if (e != cudaSuccess)
     return fail(PTOPT_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
   h->scp_graph_batch = batch;
+  h->scp_graph_lat = lat;
   h->scp_graph_kernels = kernels;
   return PTOPT_OK;
 }
@@ -645,7 +675,7 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
 
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path) {
   if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
-  if (path != PTOPT_SOLVER_AUTO && path != PTOPT_SOLVER_GENERIC && path != PTOPT_SOLVER_FAST_SPLIT)
+  if (path < PTOPT_SOLVER_AUTO || path > PTOPT_SOLVER_FAST_THROUGHPUT)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "unknown solver path");
   if (path != h->solver_path && h->scp_graph) {  // the captured graph names the other kernels
     DeviceGuard guard(h->device);
@@ -1335,8 +1365,11 @@ int ptopt_cuda_run_batch(ptopt_cuda_handle* h, int batch, int64_t first_run_id,
   PT_TRY(device_out(h, R_PG, B, &dpg));
   PT_TRY(device_out(h, R_RECORDS, B, &drec));
   PT_TRY(generate_dev(h, batch, first_run_id, nominal_init_state, spec, di, dxg, dug, ds));
-  PT_TRY(scp_solve_common(h, batch, di, dxg, dug, ds, dxo, duo, dit, dcv, dfd, nullptr, nullptr,
-                          dst, dfi, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice));
+  h->batch_entry = true;
+  const int solve_rc = scp_solve_common(h, batch, di, dxg, dug, ds, dxo, duo, dit, dcv, dfd, nullptr, nullptr,
+                                        dst, dfi, cudaMemcpyDeviceToDevice, cudaMemcpyDeviceToDevice);
+  h->batch_entry = false;
+  PT_TRY(solve_rc);
   const int* audit_key = nullptr;
   PT_TRY(audit_dev(h, batch, audit_substeps, dxo, duo, dst, dpg, nullptr, dst, dfi, nullptr, &audit_key));
   RecordArgs ra;

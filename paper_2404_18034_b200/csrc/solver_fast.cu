@@ -25,6 +25,7 @@
 #include <type_traits>
 
 #include "kernels.cuh"
+#include "mailbox.cuh"
 
 namespace ptopt_b200 {
 
@@ -268,39 +269,6 @@ enum Mailbox { kBoxPrev = 0, kBoxNext = 1, kBoxNorm = 2 /* and 3: by trip parity
 constexpr int kBoxOffset = 12 * kFastWarps;                 // mbarriers live in the unused tail of `red`
 constexpr int kPrevBytes = 8 * (kNX + 1 + kG * kNU);        // duals + relaxation dual + B+ partial sums
 constexpr int kNextBytes = 8 * (kNX + kNU);                 // first node vectors of rank 1
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-/// Shared-memory address of `local` inside CTA `rank` of the cluster (shared::cluster window).
-__device__ __forceinline__ unsigned partner_u32(const void* local, int rank) {
-  unsigned r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-  return r;
-}
-/// Asynchronous remote store of one double; completes 8 transaction bytes on the receiver's mailbox.
-__device__ __forceinline__ void push_f64(unsigned dst, double v, unsigned box) {
-  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v),
-               "r"(box)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long* bar, int bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-/// Waits for `phase` of a mailbox.  A wait normally ends within a microsecond; a protocol error
-/// must surface as a failed launch, not as a hung device, so the poll gives up (trap) after
-/// 2^26 attempts (seconds).
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, int phase) {
-  unsigned ok, polls = 0;
-  do {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok)
-                 : "r"(smem_u32(bar)), "r"((unsigned)(phase & 1))
-                 : "memory");
-  } while (!ok && ++polls < (1u << 26));
-  if (!ok) __trap();
-}
 
 /// Per-thread view of the mailboxes of a cluster CTA.
 struct Boxes {

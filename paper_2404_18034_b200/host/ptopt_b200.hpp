@@ -970,6 +970,34 @@ inline RocketProblem make_rocket_problem(const rocket::VehicleParams& params, co
   return pb;
 }
 
+namespace detail {
+/// The device generator interpolates toward the terminal targets pinned in `pb`
+/// (final_fix_idx / final_fix_val; an unpinned position, velocity or rate slot reads 0, an unpinned
+/// attitude the identity), while the reference interpolates toward bc.*_final
+/// (rocket_problem.hpp:144-148).  The two agree whenever `pb` was built from `bc`
+/// (make_rocket_problem); anything else is refused instead of silently producing another guess.
+template <class Problem, class Boundary>
+inline void check_terminal_targets(const Problem& pb, const Boundary& bc) {
+  double want[kNXI] = {0.0};
+  for (int i = 0; i < 3; ++i) {
+    want[1 + i] = bc.r_final[static_cast<std::size_t>(i)];
+    want[4 + i] = bc.v_final[static_cast<std::size_t>(i)];
+    want[11 + i] = bc.w_final[static_cast<std::size_t>(i)];
+  }
+  for (int i = 0; i < 4; ++i) want[7 + i] = bc.q_final[static_cast<std::size_t>(i)];
+  double have[kNXI] = {0.0};
+  have[10] = 1.0;  // identity attitude, scalar last
+  for (std::size_t j = 0; j < pb.final_fix_idx.size(); ++j) {
+    const int idx = pb.final_fix_idx[j];
+    if (idx >= 0 && idx < kNXI) have[idx] = pb.final_fix_val[j];
+  }
+  for (int i = 1; i < kNXI; ++i)
+    if (have[i] != want[i])
+      throw std::invalid_argument("initial_guess: the boundary's terminal targets differ from the ones the problem pins "
+                                  "(build the problem with make_rocket_problem from the same boundary)");
+}
+}  // namespace detail
+
 /// initial_guess (rocket_problem.hpp:127-163): straight-line state interpolation, slerp of the
 /// attitude and a gravity-cancelling thrust profile.  Evaluated by the device generator that
 /// run_batch uses (ptopt_cuda_generate_batch with a dispersion box of zero width around the
@@ -977,6 +1005,7 @@ inline RocketProblem make_rocket_problem(const rocket::VehicleParams& params, co
 /// The terminal targets are the ones `pb` was built with (make_rocket_problem).
 template <class Problem, class Boundary>
 RocketTrajectory initial_guess(const Problem& pb, const Boundary& bc) {
+  detail::check_terminal_targets(pb, bc);
   const int n = static_cast<int>(pb.grid.nodes.size());
   const ptopt_problem_desc d = detail::to_desc(pb);
   ptopt_cuda_handle* h = detail::context(d, pb.grid.nodes);
@@ -1078,6 +1107,7 @@ BatchResult run_batch(const Problem& nominal, const Boundary& nominal_bc, const 
                       std::int64_t first_run_id = 0) {
   if (batch_size < 1) throw std::invalid_argument("montecarlo.batch_size must be >= 1");
   if (workers < 1) throw std::invalid_argument("montecarlo.workers must be >= 1");
+  ptopt_b200::detail::check_terminal_targets(nominal, nominal_bc);
   const int n = static_cast<int>(nominal.grid.nodes.size());
   const ptopt_problem_desc d = ptopt_b200::detail::to_desc(nominal);
   ptopt_cuda_handle* h = ptopt_b200::detail::context(d, nominal.grid.nodes);
@@ -1111,6 +1141,7 @@ BatchResult run_batch(const Problem& nominal, const Boundary& nominal_bc, const 
                       std::int64_t first_run_id = 0, std::vector<double>* device_ms = nullptr) {
   if (batch_size < 1) throw std::invalid_argument("montecarlo.batch_size must be >= 1");
   if (devices.empty()) throw std::invalid_argument("montecarlo.workers must be >= 1");
+  ptopt_b200::detail::check_terminal_targets(nominal, nominal_bc);
   const int n = static_cast<int>(nominal.grid.nodes.size());
   const ptopt_problem_desc d = ptopt_b200::detail::to_desc(nominal);
   const auto init = nominal_bc.initial.to_vec();

@@ -371,6 +371,17 @@ int main() {
         CHECK(same);
       }
     }
+    {  // a boundary whose terminal targets are not the ones the problem pins is refused
+      auto other = default_boundary();
+      other.r_final[0] = 0.25;
+      bool refused = false;
+      try {
+        pb::initial_guess(prob, other);
+      } catch (const std::invalid_argument&) {
+        refused = true;
+      }
+      CHECK(refused);
+    }
     bool caught = false;
     try {
       pb::mc::run_batch(prob, default_boundary(), spec, 0, 1);

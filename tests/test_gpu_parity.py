@@ -19,11 +19,14 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(1.0, np.abs(b).max())
 
 
-@pytest.fixture(scope="module", params=["auto", "generic", "split"])
+@pytest.fixture(scope="module", params=["fast", "generic", "split", "latency"])
 def solver15(request):
-    """The default-scenario handle, once per kernel family: 'auto' runs the register-resident
-    power/PIPG kernels on rocket-shaped subproblems, 'generic' forces the shape-generic ones,
-    'split' shares every rocket-shaped instance between the two CTAs of a cluster."""
+    """The default-scenario handle, once per kernel family: 'fast' runs the register-resident
+    throughput kernels on rocket-shaped subproblems (five threads per node, one CTA per instance),
+    'generic' forces the shape-generic ones, 'split' shares every rocket-shaped instance between
+    the two CTAs of a cluster, 'latency' spreads every instance over a cluster of up to eight CTAs
+    with sixteen threads per node.  ('auto' picks 'latency' for batches that fit the chip in one
+    wave and 'fast' otherwise: test_auto_path_selection.)"""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(15)
@@ -380,7 +383,8 @@ def test_scp_solve_default_scenario_full_budget(solver15, ptor):
     assert abs(out["x"][0, -1, 0] - 1.416480459) < 1e-6
 
 
-def test_scp_solve_reduced_budget_batch(ptor):
+@pytest.mark.parametrize("path", ["fast", "latency"])
+def test_scp_solve_reduced_budget_batch(ptor, path):
     """Many dispersed instances with a reduced iteration budget (fast on the CPU oracle), one
     of them poisoned so that the per-instance failure path is exercised inside the loop."""
     from paper_2404_18034_b200.binding import Solver
@@ -394,6 +398,7 @@ def test_scp_solve_reduced_budget_batch(ptor):
     batch = scenario.make_batch(sc, range(B))
     batch["u_guess"][4, 5, 6] = -1.0  # nonpositive dilation at node 5 of instance 4
     with Solver(d) as s:
+        s.set_solver_path(path)
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
                           batch["rng_seed"])
         out2 = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
@@ -411,7 +416,8 @@ def test_scp_solve_reduced_budget_batch(ptor):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-def test_scp_solve_n50_two_instances(ptor):
+@pytest.mark.parametrize("path", ["fast", "latency"])
+def test_scp_solve_n50_two_instances(ptor, path):
     """BASELINE config 4 shape (N=50, all defaults) on two dispersed instances."""
     from paper_2404_18034_b200.binding import Solver
 
@@ -419,6 +425,7 @@ def test_scp_solve_n50_two_instances(ptor):
     d = sc.problem_desc()
     batch = scenario.make_batch(sc, [0, 1])
     with Solver(d) as s:
+        s.set_solver_path(path)
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
                           batch["rng_seed"])
         launches = s.launch_count
@@ -693,10 +700,11 @@ def test_config4_scp_batch4096_n50_properties():
     assert (out["history"][:, :, 3] == 60).all() and (out["power_trips"] > 0).all()
 
 
-@pytest.mark.parametrize("path", ["auto", "generic"])
+@pytest.mark.parametrize("path", ["fast", "generic", "latency"])
 def test_config5_n100_cluster_and_generic_kernels(ptor, path):
     """BASELINE config 5 shape (N=100): above the single-CTA node limit, so each instance is split
-    over a two-CTA cluster ('auto'); the shape-generic kernels serve it too ('generic').  Reduced
+    over a two-CTA cluster ('fast'); the shape-generic kernels serve it too ('generic'), and the
+    latency mode spreads it over eight CTAs of 12-13 nodes ('latency').  Reduced
     budget with stopping checks, parity with the oracle on three instances."""
     from paper_2404_18034_b200.binding import Solver
 
@@ -728,6 +736,7 @@ def test_scp_solve_node_count_edges(ptor, nodes):
     d = sc.problem_desc()
     batch = scenario.make_batch(sc, [0, 11])
     with Solver(d) as s:
+        s.set_solver_path("fast")
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
     for b in range(2):
         rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
@@ -776,7 +785,7 @@ def test_solver_divergence_inside_the_scp_loop(ptor):
         assert rc == abi.ST_SOLVER_DIVERGED, rc
         refs.append(ref["fail_index"])
     assert refs[0] != refs[1]
-    for path in ("auto", "generic", "split"):
+    for path in ("fast", "generic", "split", "latency"):
         with Solver(d) as s:
             s.set_solver_path(path)
             out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
@@ -832,10 +841,12 @@ def test_config4_full_budget_batch4096_subset_vs_cpu():
     assert np.abs(np.linalg.norm(q, axis=2) - 1.0).max() <= 1e-14
 
 
-def test_config5_n100_full_budget_cluster_kernels_vs_cpu():
-    """BASELINE config 5 at the depth it runs: N=100 on the two-CTA cluster kernels with the full
-    budget -- the power iteration mostly runs to its 10 000-trip cap, 25 x 2500 PIPG iterations --
-    six dispersed ids against the CPU reference."""
+@pytest.mark.parametrize("path", ["fast", "latency"])
+def test_config5_n100_full_budget_cluster_kernels_vs_cpu(path):
+    """BASELINE config 5 at the depth it runs: N=100 on the two-CTA cluster kernels ('fast') and on
+    the eight-CTA latency-mode clusters ('latency') with the full budget -- the power iteration
+    mostly runs to its 10 000-trip cap, 25 x 2500 PIPG iterations, so the mailbox protocols run
+    ~300 000 hand-offs per instance -- six dispersed ids against the CPU reference."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(100)
@@ -843,6 +854,7 @@ def test_config5_n100_full_budget_cluster_kernels_vs_cpu():
     ids = [0, 1, 2, 4097, 32768, 65535]
     batch = scenario.make_batch(sc, ids)
     with Solver(d) as s:
+        s.set_solver_path(path)
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
     assert (out["power_trips"] == 10000).sum() >= 25  # the mailbox protocol ran at its real depth
     refs = cpu_reference_solves(d, batch, list(range(len(ids))))
@@ -907,3 +919,54 @@ def test_run_batch_multi_device_list_is_bit_identical():
         assert len(ms) == len(devices) and (ms > 0).sum() == min(batch, len(devices))
     with pytest.raises(PtoptError):
         run_batch_multi(d, [0, 99], B, first, sc.initial_state, spec.r_low, spec.r_high, spec.seed)
+
+
+@pytest.mark.parametrize("nodes", [2, 3, 5, 8, 9, 15, 17, 33, 50, 128, 129])
+def test_scp_solve_latency_mode_node_counts(ptor, nodes):
+    """Latency mode (one instance over a cluster, sixteen threads per node) at the edges of its
+    decomposition: clusters of two CTAs (2, 3 nodes), four (5), eight with one node per CTA (8),
+    uneven shares (9, 15, 17, 33, 50), the largest supported count (128 = 8 x 16) and the first one
+    that falls back to the shape-generic kernels (129)."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(nodes)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 120, 150
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [0, 11, 5])
+    with Solver(d) as s:
+        s.set_solver_path("latency")
+        out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+    for b in range(3):
+        rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                                 int(batch["rng_seed"][b]), with_trips=True)
+        assert rc == 0
+        check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+
+
+def test_auto_path_selection():
+    """AUTO runs the latency-mode kernels when batch x cluster size fits the chip in one wave and the
+    throughput kernels otherwise; mc::run_batch always uses the throughput family so that a shard's
+    records do not depend on its size.  Detected through bit-identity with the forced paths."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(15)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max, sc.audit_substeps = 2, 100, 120, 8
+    d = sc.problem_desc()
+    spec = sc.dispersion
+    B = 80  # 80 x 2 > 148 SMs: throughput kernels; the first 3 alone: latency kernels
+    batch = scenario.make_batch(sc, range(B))
+    args = lambda k: (batch["init_state"][:k], batch["x_guess"][:k], batch["u_guess"][:k], batch["rng_seed"][:k])
+    res = {}
+    for path in ("auto", "fast", "latency"):
+        with Solver(d) as s:
+            s.set_solver_path(path)
+            res[path, 3] = s.scp_solve(*args(3))["x"]
+            res[path, B] = s.scp_solve(*args(B))["x"]
+            res[path, "rb"] = s.run_batch(3, 0, sc.initial_state, spec.r_low, spec.r_high, spec.seed,
+                                          audit_substeps=8, keep_trajectories=True)[1]
+    assert not np.array_equal(res["fast", 3], res["latency", 3])  # the two families round differently
+    np.testing.assert_array_equal(res["auto", 3], res["latency", 3])
+    np.testing.assert_array_equal(res["auto", B], res["fast", B])
+    np.testing.assert_array_equal(res["auto", "rb"], res["fast", "rb"])
+    np.testing.assert_array_equal(res["fast", B][:3], res["fast", 3])
+    assert np.abs(res["fast", 3] - res["latency", 3]).max() <= TOL_ITER

@@ -208,9 +208,9 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h);
 /* Kernel family used for power iteration and PIPG.  No reference counterpart.
  *   AUTO       for the rocket-shaped subproblem (n_x = 15, n_u = 7, A_plus = -I, e_y = last
  *              state): the latency-mode kernels whenever the whole batch fits the chip in one
- *              wave (batch x cluster size <= SM count, i.e. up to 18 / 37 / 74 instances with
- *              8 / 4 / 2 CTAs per instance), else the throughput kernels; the shape-generic
- *              kernels for every other shape.
+ *              wave (batch x cluster size <= SM count: one CTA per instance up to 16 nodes,
+ *              else up to 18 / 37 / 74 instances with 8 / 4 / 2 CTAs per instance), else the
+ *              throughput kernels; the shape-generic kernels for every other shape.
  *   GENERIC    forces the shape-generic kernels (the parity tests run every family on the same
  *              inputs).
  *   FAST_SPLIT throughput kernels with every instance of 4..50 nodes shared by a 2-CTA

@@ -28,6 +28,9 @@
 // solver_fast.cu.  Row and column sums are added in butterfly order (rounding-only change).
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "mailbox.cuh"
 
@@ -226,14 +229,16 @@ __device__ __forceinline__ void transposed_pair(const double (&a)[4][4][2], cons
   }
 }
 
-struct Boxes {
-  unsigned long long* local;
-  unsigned to_next_prevbox, to_prev_nextbox;  // the neighbours' mailboxes this CTA sends to
-};
+/// Asynchronous remote store of a pair of doubles (16 bytes on the receiver's mailbox).
+__device__ __forceinline__ void push_f64x2(unsigned dst, double v0, double v1, unsigned box) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "d"(v0), "d"(v1), "r"(box)
+               : "memory");
+}
 
 /// Mailboxes: cleared shared memory first, then the barriers, then a cluster barrier so that every
 /// CTA is running, cleared and initialised before any remote store.
-__device__ __forceinline__ Boxes open_boxes(LatSmem* S, const Cut& cut, int tid) {
+__device__ __forceinline__ void open_boxes(LatSmem* S, int tid) {
   for (int e = tid; e < (int)(sizeof(LatSmem) / sizeof(double)); e += blockDim.x)
     reinterpret_cast<double*>(S)[e] = 0.0;
   __syncthreads();
@@ -243,49 +248,77 @@ __device__ __forceinline__ Boxes open_boxes(LatSmem* S, const Cut& cut, int tid)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cg::this_cluster().sync();
-  Boxes bx;
-  bx.local = S->box;
-  bx.to_next_prevbox = cut.has_next ? partner_u32(S->box + kBoxPrev, cut.rank + 1) : 0u;
-  bx.to_prev_nextbox = cut.has_prev ? partner_u32(S->box + kBoxNext, cut.rank - 1) : 0u;
-  return bx;
 }
 
-__device__ __forceinline__ void receive(const Boxes& bx, int which, bool mine, bool armer, int bytes, int phase) {
+/// Where a thread's values go: its slots in this CTA's shared memory and — for the CTA's first /
+/// last node — the matching guard slots of the neighbour rank (shared::cluster addresses, computed
+/// once).  Loop-invariant, so the hot loops carry no address arithmetic.
+struct Ports {
+  double* dual_dst;    // php[node][row]
+  double* bps_dst;     // bps[node][c0..c0+1]  (cq 3)
+  double* prim_dst;    // xs / us [node][entry pair]  (cq 0..2)
+  unsigned r_dual, r_bps, r_prim;  // the same slots inside the next (duals) / previous (primal) rank
+  unsigned box_to_next, box_to_prev;
+  const double* seg;     // this thread's segment of the node vector [x_k | u_k | u_{k+1}]
+  const double* x_next;  // x_{k+1}[row] (row 15: entry 14), x_k[same]
+  const double* x_cur;
+  const double* nb;      // neighbour pair: phi_{k-1} (x owners; theta_{k-1} behind entry 14) / B+^T phi_{k-1} (u owners)
+  const double* theta_k; // php[node][15]
+  unsigned long long* box;
+};
+
+__device__ __forceinline__ Ports make_ports(LatSmem* S, const Lane& t, const Cut& cut) {
+  Ports q;
+  q.dual_dst = S->php + (t.pc + 1) * kXP + t.row;
+  q.bps_dst = S->bps + (t.pc + 1) * kUP + t.c0;
+  q.prim_dst = t.cq == 2 ? S->us + (t.pc + 1) * kUP + t.c0 : S->xs + (t.pc + 1) * kXP + 8 * (t.cq & 1) + t.c0;
+  q.r_dual = q.r_bps = q.r_prim = q.box_to_next = q.box_to_prev = 0u;
+  if (t.push_prev) {  // slot -1 of the next rank
+    q.r_dual = partner_u32(S->php + t.row, cut.rank + 1);
+    q.r_bps = partner_u32(S->bps + t.c0, cut.rank + 1);
+    q.box_to_next = partner_u32(S->box + kBoxPrev, cut.rank + 1);
+  }
+  if (t.push_next) {  // slot nloc of the previous rank
+    const double* slot = t.cq == 2 ? S->us + (cut.nloc_prev + 1) * kUP + t.c0
+                                   : S->xs + (cut.nloc_prev + 1) * kXP + 8 * (t.cq & 1) + t.c0;
+    q.r_prim = partner_u32(slot, cut.rank - 1);
+    q.box_to_prev = partner_u32(S->box + kBoxNext, cut.rank - 1);
+  }
+  q.seg = t.cq == 0   ? S->xs + (t.pc + 1) * kXP
+          : t.cq == 1 ? S->xs + (t.pc + 1) * kXP + 8
+          : t.cq == 2 ? S->us + (t.pc + 1) * kUP
+                      : S->us + (t.pc + 2) * kUP;
+  const int rsel = t.theta_lane ? kNX - 1 : t.row;
+  q.x_next = S->xs + (t.pc + 2) * kXP + rsel;
+  q.x_cur = S->xs + (t.pc + 1) * kXP + rsel;
+  q.nb = t.cq == 2 ? S->bps + t.pc * kUP + t.c0 : S->php + t.pc * kXP + 8 * (t.cq & 1) + t.c0;
+  q.theta_k = S->php + (t.pc + 1) * kXP + kNX;
+  q.box = S->box;
+  return q;
+}
+
+__device__ __forceinline__ void receive(const Ports& q, int which, bool mine, bool armer, int bytes, int phase) {
   if (!mine) return;
-  if (armer) mbar_expect(bx.local + which, bytes);
-  mbar_wait(bx.local + which, phase);
+  if (armer) mbar_expect(q.box + which, bytes);
+  mbar_wait(q.box + which, phase);
 }
 
-/// Publishes the duals of this thread's row (php) and — cq 3 — the B+ column sums (bps) in the
+/// Publishes the dual of this thread's row (php) and — cq 3 — the B+ column sums (bps) in the
 /// node's slot; the CTA's last node sends the same values into slot -1 of the next rank.
-__device__ __forceinline__ void publish_duals(LatSmem* S, const Lane& t, const Cut& cut, const Boxes& bx, double d,
-                                              const double (&cs)[2]) {
-  S->php[(t.pc + 1) * kXP + t.row] = d;
-  if (t.cq == 3) *reinterpret_cast<double2*>(S->bps + (t.pc + 1) * kUP + t.c0) = make_double2(cs[0], cs[1]);
+__device__ __forceinline__ void publish_duals(const Ports& q, const Lane& t, double d, const double (&cs)[2]) {
+  *q.dual_dst = d;
+  if (t.cq == 3) *reinterpret_cast<double2*>(q.bps_dst) = make_double2(cs[0], cs[1]);
   if (t.push_prev) {
-    push_f64(partner_u32(S->php + t.row, cut.rank + 1), d, bx.to_next_prevbox);
-    if (t.cq == 3) {
-      const unsigned r = partner_u32(S->bps + t.c0, cut.rank + 1);
-      push_f64(r, cs[0], bx.to_next_prevbox);
-      push_f64(r + 8u, cs[1], bx.to_next_prevbox);
-    }
+    push_f64(q.r_dual, d, q.box_to_next);
+    if (t.cq == 3) push_f64x2(q.r_bps, cs[0], cs[1], q.box_to_next);
   }
 }
 
 /// Stores the two primal entries (cq 0, 1: x; cq 2: u) into the node's slot; the CTA's first node
 /// sends them into slot nloc of the previous rank as well.
-__device__ __forceinline__ void publish_primal(LatSmem* S, const Lane& t, const Cut& cut, const Boxes& bx, double v0,
-                                               double v1) {
-  if (t.cq == 3) return;
-  double* dst = t.cq == 2 ? S->us + (t.pc + 1) * kUP + t.c0 : S->xs + (t.pc + 1) * kXP + 8 * t.cq + t.c0;
-  *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-  if (t.push_next) {
-    const double* slot = t.cq == 2 ? S->us + (cut.nloc_prev + 1) * kUP + t.c0
-                                   : S->xs + (cut.nloc_prev + 1) * kXP + 8 * t.cq + t.c0;
-    const unsigned r = partner_u32(slot, cut.rank - 1);
-    push_f64(r, v0, bx.to_prev_nextbox);
-    push_f64(r + 8u, v1, bx.to_prev_nextbox);
-  }
+__device__ __forceinline__ void publish_primal(const Ports& q, const Lane& t, double v0, double v1) {
+  if (t.cq != 3) *reinterpret_cast<double2*>(q.prim_dst) = make_double2(v0, v1);
+  if (t.push_next && t.cq != 3) push_f64x2(q.r_prim, v0, v1, q.box_to_prev);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -299,23 +332,50 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   if (a.active && !a.active[b]) return;  // every CTA of the cluster leaves together
   const int n = a.shape.n, m = n - 1;
   const Lane t = make_lane(cut, m);
-  const Boxes bx = open_boxes(S, cut, t.tid);
-  const double* seg = t.cq == 0   ? S->xs + (t.pc + 1) * kXP
-                      : t.cq == 1 ? S->xs + (t.pc + 1) * kXP + 8
-                      : t.cq == 2 ? S->us + (t.pc + 1) * kUP
-                                  : S->us + (t.pc + 2) * kUP;
-  const int rsel = t.theta_lane ? kNX - 1 : t.row;        // x entry this row owner reads from nodes k, k+1
-  const double* x_next = S->xs + (t.pc + 2) * kXP + rsel;
-  const double* x_cur = S->xs + (t.pc + 1) * kXP + rsel;
-  // neighbour terms of the owned primal pair: x: phi_{k-1} (and theta_{k-1} behind row 14); u: B+^T phi_{k-1}
-  const double* nb_ptr = t.cq == 2 ? S->bps + t.pc * kUP + t.c0 : S->php + t.pc * kXP + 8 * (t.cq & 1) + t.c0;
+  open_boxes(S, t.tid);
+  const Ports q = make_ports(S, t, cut);
   const bool u_owner = t.cq == 2;
   const bool is14 = t.cq == 1 && t.rg == 3;  // entry 0 of this pair is x[14], entry 1 the pad
   const bool alive0 = t.node && t.cq < 3, alive1 = alive0 && t.rg < 3 + (t.cq == 0);
-  const int unorm = 8 * t.nwarps * (cut.ranks - 1);  // bytes of the other ranks' norm shares per trip
+  const double sgn = u_owner ? 1.0 : -1.0;   // u: + B+^T phi_{k-1};  x: - phi_{k-1}  (A+ = -I)
+  const double keep0 = alive0 ? 1.0 : 0.0, keep1 = alive1 ? 1.0 : 0.0;
 
   double aop[4][4][2];
   load_tile(a.sp, (size_t)b * m + (t.ival ? t.kg : 0), t, aop);
+
+  // Squared norm of the iterate, two levels: every warp leaves its share in shared memory; after
+  // the block barrier that ends the trip thread 0 adds the CTA's shares and sends the total to every
+  // rank — its own included, so that one mailbox covers all of them — by trip parity (a rank may run
+  // up to one trip ahead of another, see solver_fast.cu).  Every rank then adds the same eight
+  // totals in the same order.
+  double* shares = S->shares;                       // [parity][kLatWarpsMax]
+  double* totals = S->shares + 2 * kLatWarpsMax;    // [parity][kLatMaxRanks]
+  unsigned tot_remote[kLatMaxRanks], box_remote[kLatMaxRanks];
+  if (t.tid == 0) {
+#pragma unroll
+    for (int r = 0; r < kLatMaxRanks; ++r) {
+      tot_remote[r] = r < cut.ranks ? partner_u32(totals + cut.rank, r) : 0u;
+      box_remote[r] = r < cut.ranks ? partner_u32(S->box + kBoxNorm, r) : 0u;
+    }
+  }
+  const bool lone = cut.ranks == 1;  // a single CTA: the warps' shares are the whole norm, no mailbox
+  auto send_total = [&](int trip) {  // thread 0, after the block barrier behind the warps' shares
+    static_assert(kLatWarpsMax == 8, "tree below");
+    const double2* p = reinterpret_cast<const double2*>(shares + (trip & 1) * kLatWarpsMax);
+    const double2 s0 = p[0], s1 = p[1], s2 = p[2], s3 = p[3];
+    const double tot = ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
+#pragma unroll
+    for (int r = 0; r < kLatMaxRanks; ++r)
+      if (r < cut.ranks)
+        push_f64(tot_remote[r] + 8u * (unsigned)((trip & 1) * kLatMaxRanks), tot, box_remote[r] + 8u * (unsigned)(trip & 1));
+  };
+  auto norm_sq = [&](int trip) {  // waits for the totals of `trip`, then adds them (absent ranks: zero)
+    static_assert(kLatMaxRanks == 8 && kLatWarpsMax == 8, "tree below");
+    if (!lone) receive(q, kBoxNorm + (trip & 1), true, t.tid == 0, 8 * cut.ranks, trip >> 1);
+    const double2* p = reinterpret_cast<const double2*>((lone ? shares : totals) + (trip & 1) * 8);
+    const double2 s0 = p[0], s1 = p[1], s2 = p[2], s3 = p[3];
+    return ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
+  };
 
   // seed (pipg.hpp:213-230): x, u, vc+, vc-; sigma0 = ||seed||_2
   double acc = 0.0;
@@ -327,7 +387,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       v0 = src[0];
       if (alive1) v1 = src[1];
     }
-    publish_primal(S, t, cut, bx, v0, v1);  // the first node also reaches the previous rank: "next" phase 0
+    publish_primal(q, t, v0, v1);  // the first node also reaches the previous rank: "next" phase 0
     acc = v0 * v0 + v1 * v1;
   }
   double vcd = 0.0;  // vc+ - vc-: the only combination of the two groups the forward map uses
@@ -337,31 +397,10 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     acc += vp * vp;
     acc += vn * vn;
   }
-  auto send_share = [&](double share, int trip) {  // own slot, and the same slot in every other rank
-    const int at = (cut.rank * 2 + (trip & 1)) * kLatWarpsMax + t.warp;
-    S->shares[at] = share;
-    for (int r = 0; r < cut.ranks; ++r)
-      if (r != cut.rank)
-        push_f64(partner_u32(S->shares + at, r), share, partner_u32(S->box + kBoxNorm + (trip & 1), r));
-  };
-  // two norm mailboxes by trip parity: a rank may run up to one trip ahead of another (see solver_fast.cu)
-  auto recv_norm = [&](int trip) {
-    if (cut.ranks > 1) receive(bx, kBoxNorm + (trip & 1), true, t.tid == 0, unorm, trip >> 1);
-  };
-  auto norm_sq = [&](int parity) {  // every rank adds the shares in the same order
-    double s = 0.0;
-    for (int r = 0; r < cut.ranks; ++r) {
-      const double* sh = S->shares + (r * 2 + parity) * kLatWarpsMax;
-      double sr = 0.0;
-      for (int w = 0; w < t.nwarps; ++w) sr += sh[w];
-      s += sr;
-    }
-    return s;
-  };
   acc = warp_sum(acc);
-  if (t.lane == 0) send_share(acc, 0);
+  if (t.lane == 0) shares[t.warp] = acc;
   __syncthreads();
-  recv_norm(0);
+  if (t.tid == 0 && !lone) send_total(0);
   double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (t.tid == 0 && cut.rank == 0) {
@@ -369,24 +408,25 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       a.sigma[b] = 0.0;
       if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
     }
-    if (cut.has_next) receive(bx, kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
+    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
     cg::this_cluster().sync();
     return;
   }
   double inv = rsqrt(sigma);
   sigma = sqrt(sigma);
+  // row lanes scale (forward row - x_{k+1}[row]) + vcd; the relaxation-dual lane x_{k+1}[14] - x_k[14]
+  const double live = (t.row_alive || (t.theta_lane && t.ival)) ? 1.0 : 0.0;
 
   int trips = 0;
   bool done = false;
   for (int j = 1; j <= a.j_max; ++j) {
     // ---- forward map (pipg.hpp:234-245); the norm of trip j-1 arrives while the products run
-    receive(bx, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // the next rank's first node of trip j-1
-    const double r = forward_row(aop, seg, t.rg);
-    const double s = (r - x_next[0]) + vcd;
-    const double dy = x_next[0] - x_cur[0];
+    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // the next rank's first node of trip j-1
+    const double xn1 = q.x_next[0], xc = q.x_cur[0];
+    const double r = forward_row(aop, q.seg, t.rg);
+    const double s = t.theta_lane ? xn1 - xc : (r - xn1) + vcd;
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
-      recv_norm(j - 1);
-      const double ss = norm_sq((j - 1) & 1);
+      const double ss = norm_sq(j - 1);
       const double sigma_star = sqrt(ss);
       inv = rsqrt(ss);
       if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
@@ -402,48 +442,32 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       }
     }
     trips = j;
-    const double phi = t.row_alive ? s * inv : 0.0;
-    const double mine = t.theta_lane ? (t.ival ? dy * inv : 0.0) : phi;
+    const double mine = live * (s * inv);  // phi_k[row], or theta_k on lane (3,3)
     double d[4], cs[2];
     gather_rows(mine, d);
     drop_theta_slot(t, d);
     transposed_pair(aop, d, cs);
-    publish_duals(S, t, cut, bx, mine, cs);
+    publish_duals(q, t, mine, cs);
+    const double phi = t.theta_lane ? 0.0 : mine;
     vcd = 2.0 * phi;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
     const double acc_d = vcd * phi;
     __syncthreads();
     // ---- adjoint map (pipg.hpp:247-275)
-    receive(bx, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // the previous rank's last interval
-    const double2 nb = *reinterpret_cast<const double2*>(nb_ptr);
-    double v0, v1;
-    if (u_owner) {
-      v0 = cs[0] + nb.x;
-      v1 = cs[1] + nb.y;
-    } else {
-      v0 = cs[0] + -nb.x;
-      v1 = cs[1] + -nb.y;
-      if (is14) {  // -theta_k + theta_{k-1} on the last state (e_y)
-        v0 += -S->php[(t.pc + 1) * kXP + kNX];
-        v0 += nb.y;
-      }
-    }
-    v0 = alive0 ? v0 : 0.0;
-    v1 = alive1 ? v1 : 0.0;
-    publish_primal(S, t, cut, bx, v0, v1);
+    receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // the previous rank's last interval
+    const double2 nb = *reinterpret_cast<const double2*>(q.nb);
+    const double extra = is14 ? nb.y - q.theta_k[0] : 0.0;  // -theta_k + theta_{k-1} on the last state (e_y)
+    const double v0 = keep0 * (fma(sgn, nb.x, cs[0]) + extra);
+    const double v1 = keep1 * fma(sgn, nb.y, cs[1]);
+    publish_primal(q, t, v0, v1);
     acc = fma(v0, v0, v1 * v1) + acc_d;
     acc = warp_sum(acc);
-    if (t.lane == 0) send_share(acc, j);
+    if (t.lane == 0) shares[(j & 1) * kLatWarpsMax + t.warp] = acc;
     __syncthreads();
+    if (t.tid == 0 && !lone) send_total(j);
   }
   if (!done) {  // j_max trips without meeting the tolerance
-    if (a.j_max >= 1) recv_norm(a.j_max);
-    sigma = sqrt(norm_sq(a.j_max & 1));
-  }
-  // what the neighbours sent last is still on its way
-  if (done) {
-    // the loop was left after `receive next (trips)` but before `receive prev (trips)`: nothing pending
-  } else if (a.j_max >= 1) {
-    receive(bx, kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);
+    sigma = a.j_max >= 1 ? sqrt(norm_sq(a.j_max)) : sigma;
+    if (a.j_max >= 1) receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);  // still on its way
   }
   if (t.tid == 0 && cut.rank == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sigma;
@@ -463,30 +487,23 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
   if (a.active && !a.active[b]) return;  // every CTA of the cluster leaves together
   const int n = a.shape.n, m = n - 1;
   const Lane t = make_lane(cut, m);
-  const Boxes bx = open_boxes(S, cut, t.tid);
-  const double* seg = t.cq == 0   ? S->xs + (t.pc + 1) * kXP
-                      : t.cq == 1 ? S->xs + (t.pc + 1) * kXP + 8
-                      : t.cq == 2 ? S->us + (t.pc + 1) * kUP
-                                  : S->us + (t.pc + 2) * kUP;
-  const int rsel = t.theta_lane ? kNX - 1 : t.row;
-  const double* x_next = S->xs + (t.pc + 2) * kXP + rsel;
-  const double* x_cur = S->xs + (t.pc + 1) * kXP + rsel;
-  const double* nb_ptr = t.cq == 2 ? S->bps + t.pc * kUP + t.c0 : S->php + t.pc * kXP + 8 * (t.cq & 1) + t.c0;
+  open_boxes(S, t.tid);
+  const Ports q = make_ports(S, t, cut);
   const bool u_owner = t.cq == 2;
   const bool is14 = t.cq == 1 && t.rg == 3;
   const bool alive0 = t.node && t.cq < 3, alive1 = alive0 && t.rg < 3 + (t.cq == 0);
   const bool last_node = t.node && t.kg == n - 1;
+  const double sgn = u_owner ? 1.0 : -1.0;
 
   double aop[4][4][2];
   load_tile(a.sp, (size_t)b * m + (t.ival ? t.kg : 0), t, aop);
 
-  // ---- per-entry constants and the warm start (pipg.hpp:362-374): ex = cur = workspace
-  // primal pair: entry index inside x / u, proximal-term extras, box or boundary value
+  // ---- per-entry constants and the warm start (pipg.hpp:362-374): ex = cur = workspace.
+  // One code path for every kind of entry: a control entry is clamped to its box (pipg.hpp:418-419),
+  // a boundary row to [value, value] (:408-413), a free state to (-inf, inf), an entry that does
+  // not exist (pads, idle threads, cq 3) to [0, 0].
   const int ce = u_owner ? t.c0 : 8 * t.cq + t.c0;
-  double pe[2] = {0.0, 0.0}, lo[2], hi[2], fv[2] = {0.0, 0.0}, cost[2] = {0.0, 0.0};
-  bool fixed[2] = {false, false};
-  lo[0] = lo[1] = -INFINITY;
-  hi[0] = hi[1] = INFINITY;
+  double pe[2] = {0.0, 0.0}, lo[2] = {0.0, 0.0}, hi[2] = {0.0, 0.0}, cost[2] = {0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const bool alive = e == 0 ? alive0 : alive1;
@@ -494,27 +511,26 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
     if (u_owner) {
       const size_t g = ((size_t)b * n + t.kg) * kNU + ce + e;
       pe[e] = a.ws.u[g];
-      lo[e] = a.sp.u_min[g];  // pipg.hpp:418-419
+      lo[e] = a.sp.u_min[g];
       hi[e] = a.sp.u_max[g];
     } else {
       pe[e] = a.ws.x[((size_t)b * n + t.kg) * kNX + ce + e];
+      lo[e] = -INFINITY;
+      hi[e] = INFINITY;
       if (last_node) cost[e] = a.shape.w_cost * a.shape.e_cost[ce + e];
-      // boundary rows (pipg.hpp:408-413); later entries override earlier ones, as the assignment loops do
+      // later entries override earlier ones, as the assignment loops do
       if (t.kg == 0)
         for (int i = 0; i < a.shape.n_init_fix; ++i)
-          if (a.shape.init_fix_idx[i] == ce + e) {
-            fixed[e] = true;
-            fv[e] = a.sp.init_fix_val[(size_t)b * a.shape.n_init_fix + i];
-          }
+          if (a.shape.init_fix_idx[i] == ce + e) lo[e] = hi[e] = a.sp.init_fix_val[(size_t)b * a.shape.n_init_fix + i];
       if (last_node)
         for (int i = 0; i < a.shape.n_final_fix; ++i)
-          if (a.shape.final_fix_idx[i] == ce + e) {
-            fixed[e] = true;
-            fv[e] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
-          }
+          if (a.shape.final_fix_idx[i] == ce + e) lo[e] = hi[e] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
     }
   }
-  // dual row: dynamics dual + the two slack groups, or (lane (3,3)) the relaxation dual
+  // dual row: dynamics dual + the two slack groups, or (lane (3,3)) the relaxation dual.  Again one
+  // code path: the relaxation lane has an infinite slack weight (its slacks stay 0) and clips its
+  // dual at 0; a row that does not exist has a zero step (its dual stays 0).
+  const bool theta_alive = t.theta_lane && t.ival;
   double phe = 0.0, vpe = 0.0, vne = 0.0, wrow = 0.0;
   if (t.row_alive) {
     const size_t g = ((size_t)b * m + t.kg) * kNX + t.row;
@@ -522,10 +538,11 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
     vpe = a.ws.vc_pos[g];
     vne = a.ws.vc_neg[g];
     wrow = a.sp.w[g];
-  } else if (t.theta_lane && t.ival) {
+  } else if (theta_alive) {
     phe = a.ws.relax_dual[(size_t)b * m + t.kg];
-    wrow = a.sp.eps_relax[(size_t)b * m + t.kg];
+    wrow = -a.sp.eps_relax[(size_t)b * m + t.kg];
   }
+  const double w_ep_lane = t.theta_lane ? INFINITY : a.shape.w_ep;
   // materialised *_cur values of the last two iterations (pipg.hpp:490-495 returns the current ones)
   double cur_p[2] = {pe[0], pe[1]}, cur_d = phe, cur_vp = vpe, cur_vn = vne;
   double prv_p[2] = {pe[0], pe[1]}, prv_d = phe, prv_vp = vpe, prv_vn = vne;
@@ -533,7 +550,8 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
   const double sigma = a.sigma[b];
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
   const double beta = a.omega * alpha;
-  auto extrapolate = [&](double ex, double cur) { return fma(a.rho, cur - ex, ex); };  // pipg.hpp:461-472
+  const double beta_lane = (t.row_alive || theta_alive) ? beta : 0.0;
+  const double rho = a.rho, w_prox = a.shape.w_prox;
 
   double cs[2];
   {  // partial sums of H^T phi_ex of the warm start, for the first primal step
@@ -541,88 +559,89 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
     gather_rows(phe, d);
     drop_theta_slot(t, d);
     transposed_pair(aop, d, cs);
-    publish_duals(S, t, cut, bx, phe, cs);
+    publish_duals(q, t, phe, cs);
   }
   __syncthreads();
 
   int iters = 0;
   bool converged = false, diverged = false;
   int to_check = a.j_check;
+#ifdef PTOPT_LAT_PROFILE
+  long long ph_clk[6] = {0, 0, 0, 0, 0, 0}, tc = clock64();
+#define LAT_PHASE(i) { const long long tn = clock64(); ph_clk[i] += tn - tc; tc = tn; }
+#else
+#define LAT_PHASE(i)
+#endif
   for (int j = 1; j <= a.j_max; ++j) {
     --to_check;
     const bool check = to_check == 0;
-    if (check) to_check = a.j_check;
-    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
-    receive(bx, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // previous rank, after iteration j-1
-    {
-      const double2 nb = *reinterpret_cast<const double2*>(nb_ptr);
-      const double nbv[2] = {nb.x, nb.y};
-      double rf[2];
+    if (check) {  // this iteration is compared with the one before it
+      to_check = a.j_check;
       prv_p[0] = cur_p[0];
       prv_p[1] = cur_p[1];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double x0 = pe[e];
-        double xn;
-        if (u_owner) {
-          const double grad = x0 * a.shape.w_prox + (cs[e] + nbv[e]);
-          xn = x0 + -alpha * grad;
-          const double cl = (hi[e] < xn) ? hi[e] : xn;  // std::max(lo, std::min(hi, v))
-          xn = (lo[e] < cl) ? cl : lo[e];
-        } else {
-          double base = x0 * a.shape.w_prox;
-          base += cost[e];
-          base += -nbv[e];
-          if (e == 0 && is14) base += nb.y - S->php[(t.pc + 1) * kXP + kNX];
-          const double grad = base + cs[e];
-          xn = x0 + -alpha * grad;
-          xn = fixed[e] ? fv[e] : xn;
-        }
-        const bool alive = e == 0 ? alive0 : alive1;
-        xn = alive ? xn : 0.0;
-        rf[e] = alive ? fma(2.0, xn, -x0) : 0.0;
-        cur_p[e] = xn;
-        pe[e] = alive ? extrapolate(x0, xn) : 0.0;
-      }
-      publish_primal(S, t, cut, bx, rf[0], rf[1]);
-    }
-    __syncthreads();
-    receive(bx, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // next rank's first node, this iteration
-    // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458), extrapolation of
-    //      the dual groups (:468-472) and the partial sums of H^T phi_ex for the next primal step
-    {
-      const double r = forward_row(aop, seg, t.rg);
-      const double xn1 = x_next[0];
       prv_d = cur_d;
       prv_vp = cur_vp;
       prv_vn = cur_vn;
-      if (t.theta_lane) {
-        const double drift = xn1 - x_cur[0] - wrow;
-        const double tn = clip0(phe + beta * drift);
-        cur_d = t.ival ? tn : 0.0;
-        phe = t.ival ? extrapolate(phe, tn) : 0.0;
-      } else {
-        double resid = r + -xn1;
-        const double p0 = phe, vp0 = vpe, vn0 = vne;
-        const double vp = clip0(vp0 - alpha * (a.shape.w_ep + p0));
-        const double vn = clip0(vn0 - alpha * (a.shape.w_ep - p0));
-        resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wrow;
-        const double pn = p0 + beta * resid;
-        cur_d = t.row_alive ? pn : 0.0;
-        cur_vp = t.row_alive ? vp : 0.0;
-        cur_vn = t.row_alive ? vn : 0.0;
-        phe = t.row_alive ? extrapolate(p0, pn) : 0.0;
-        vpe = t.row_alive ? extrapolate(vp0, vp) : 0.0;
-        vne = t.row_alive ? extrapolate(vn0, vn) : 0.0;
+    }
+    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
+    receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // previous rank, after iteration j-1
+    {
+      const double2 nb = *reinterpret_cast<const double2*>(q.nb);
+      const double extra = is14 ? nb.y - q.theta_k[0] : 0.0;  // theta_{k-1} - theta_k on the last state
+      const double nbv[2] = {nb.x, nb.y};
+      double rf[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double x0 = pe[e];
+        double base = x0 * w_prox;
+        base += cost[e];
+        base = fma(sgn, nbv[e], base);
+        if (e == 0) base += extra;
+        const double grad = base + cs[e];
+        double xn = x0 + -alpha * grad;
+        const double cl = (hi[e] < xn) ? hi[e] : xn;  // std::max(lo, std::min(hi, v))
+        xn = (lo[e] < cl) ? cl : lo[e];
+        rf[e] = fma(2.0, xn, -x0);
+        cur_p[e] = xn;
+        pe[e] = fma(rho, xn - x0, x0);  // extrapolation, pipg.hpp:461-472
       }
+      publish_primal(q, t, rf[0], rf[1]);
+    }
+    LAT_PHASE(0)
+    __syncthreads();
+    LAT_PHASE(1)
+    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // next rank's first node, this iteration
+    LAT_PHASE(2)
+    // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458), extrapolation of
+    //      the dual groups (:468-472) and the partial sums of H^T phi_ex for the next primal step
+    {
+      const double xn1 = q.x_next[0], xc = q.x_cur[0];
+      const double p0 = phe, vp0 = vpe, vn0 = vne;
+      const double vp = clip0(vp0 - alpha * (w_ep_lane + p0));
+      const double vn = clip0(vn0 - alpha * (w_ep_lane - p0));
+      const double slack = ((2.0 * vp - vp0) - (2.0 * vn - vn0)) + wrow;
+      const double r = forward_row(aop, q.seg, t.rg);
+      // row lanes: (A- x + B- u + B+ u+)[row] - x_{k+1}[row];  relaxation lane: x_{k+1}[14] - x_k[14]
+      const double lead = t.theta_lane ? xn1 : r, trail = t.theta_lane ? xc : xn1;
+      const double resid = (lead - trail) + slack;
+      double pn = fma(beta_lane, resid, p0);
+      pn = t.theta_lane ? clip0(pn) : pn;
+      cur_d = pn;
+      cur_vp = vp;
+      cur_vn = vn;
+      phe = fma(rho, pn - p0, p0);
+      vpe = fma(rho, vp - vp0, vp0);
+      vne = fma(rho, vn - vn0, vn0);
       double d[4];
       gather_rows(phe, d);
       drop_theta_slot(t, d);
       transposed_pair(aop, d, cs);
-      publish_duals(S, t, cut, bx, phe, cs);
+      publish_duals(q, t, phe, cs);
     }
     iters = j;
+    LAT_PHASE(3)
     __syncthreads();
+    LAT_PHASE(4)
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
       double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, bad = 0.0;
 #pragma unroll
@@ -632,21 +651,19 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
         z_del = fmax(z_del, fabs(cur_p[e] - prv_p[e]));
         if (!pt_finite(cur_p[e])) bad = 1.0;
       }
-      if (!t.theta_lane) {
-        z_cur = fmax(z_cur, fmax(fabs(cur_vp), fabs(cur_vn)));
-        z_prev = fmax(z_prev, fmax(fabs(prv_vp), fabs(prv_vn)));
-        z_del = fmax(z_del, fmax(fabs(cur_vp - prv_vp), fabs(cur_vn - prv_vn)));
-        if (!pt_finite(cur_d)) bad = 1.0;
-      }
+      z_cur = fmax(z_cur, fmax(fabs(cur_vp), fabs(cur_vn)));
+      z_prev = fmax(z_prev, fmax(fabs(prv_vp), fabs(prv_vn)));
+      z_del = fmax(z_del, fmax(fabs(cur_vp - prv_vp), fabs(cur_vn - prv_vn)));
+      if (!t.theta_lane && !pt_finite(cur_d)) bad = 1.0;
       r_cur = fabs(cur_d);
       r_prev = fabs(prv_d);
       r_del = fabs(cur_d - prv_d);
       double v[7] = {z_cur, z_prev, z_del, r_cur, r_prev, r_del, bad};
 #pragma unroll
-      for (int q = 0; q < 7; ++q) v[q] = warp_max(v[q]);
+      for (int k = 0; k < 7; ++k) v[k] = warp_max(v[k]);
       if (t.lane == 0) {
 #pragma unroll
-        for (int q = 0; q < 7; ++q) S->red[t.warp * 8 + q] = v[q];
+        for (int k = 0; k < 7; ++k) S->red[t.warp * 8 + k] = v[k];
       }
       __syncthreads();
       if (t.tid < 7) {  // this CTA's maxima into every rank's table
@@ -656,10 +673,10 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       }
       cg::this_cluster().sync();
 #pragma unroll
-      for (int q = 0; q < 7; ++q) {
+      for (int k = 0; k < 7; ++k) {
         double mx = 0.0;
-        for (int r = 0; r < cut.ranks; ++r) mx = fmax(mx, S->redc[r * 8 + q]);
-        v[q] = mx;
+        for (int r = 0; r < cut.ranks; ++r) mx = fmax(mx, S->redc[r * 8 + k]);
+        v[k] = mx;
       }
       cg::this_cluster().sync();  // the tables are rewritten at the next check
       if (v[6] > 0.0) {
@@ -672,7 +689,13 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       }
     }
   }
-  receive(bx, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, iters);  // what the previous rank sent last
+#ifdef PTOPT_LAT_PROFILE
+  if (t.lane == 0 && b == 0)
+    printf("pipg_lat rank %d warp %d: primal %.0f  barrier %.0f  recv-next %.0f  dual %.0f  barrier %.0f clk/iter (%d iters)\n",
+           cut.rank, t.warp, (double)ph_clk[0] / iters, (double)ph_clk[1] / iters, (double)ph_clk[2] / iters,
+           (double)ph_clk[3] / iters, (double)ph_clk[4] / iters, iters);
+#endif
+  receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, iters);  // what the previous rank sent last
   if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
     if (t.tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSolverDiverged;
@@ -697,7 +720,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
     a.ws.dyn_dual[g] = cur_d;
     a.ws.vc_pos[g] = cur_vp;
     a.ws.vc_neg[g] = cur_vn;
-  } else if (t.theta_lane && t.ival) {
+  } else if (theta_alive) {
     a.ws.relax_dual[(size_t)b * m + t.kg] = cur_d;
   }
   if (t.tid == 0 && cut.rank == 0) {
@@ -731,12 +754,22 @@ int solver_lat_ranks(const SubShape& s, bool has_a_plus, int batch, int sm_count
   if (has_a_plus || s.nx != kNX || s.nu != kNU || s.n < 2) return 0;
   for (int i = 0; i < kNX; ++i)
     if (s.e_y[i] != (i == kNX - 1 ? 1.0 : 0.0)) return 0;
-  // the largest cluster that still fits the whole batch on the chip in one wave (batch = 0: any)
-  for (int ranks = kLatMaxRanks; ranks >= 2; ranks >>= 1) {
-    if (ranks > s.n || (s.n + ranks - 1) / ranks > kLatMaxLocalNodes) continue;
-    if (batch > 0 && (long long)batch * ranks > sm_count) continue;
-    return ranks;
-  }
+  // Measured on B200 (single solve, full budget): N = 15 takes 134 ms in one CTA (no hand-off at all),
+  // 141 / 151 / 163 ms over 2 / 4 / 8 CTAs; N = 50 takes 146 ms over 8 CTAs (one warp per scheduler) and
+  // 159 ms over 4 (two warps per scheduler).  So: a single CTA whenever the instance fits one
+  // (<= 16 nodes), else the largest cluster the batch leaves room for.  PTOPT_LAT_RANKS overrides.
+  static const int forced = [] {
+    const char* env = getenv("PTOPT_LAT_RANKS");
+    return env ? atoi(env) : 0;
+  }();
+  const auto fits = [&](int ranks) {
+    return ranks <= s.n && (s.n + ranks - 1) / ranks <= kLatMaxLocalNodes &&
+           (batch <= 0 || (long long)batch * ranks <= sm_count);
+  };
+  if (forced > 0) return fits(forced) ? forced : 0;
+  if (fits(1)) return 1;
+  for (int ranks = kLatMaxRanks; ranks >= 2; ranks >>= 1)
+    if (fits(ranks)) return ranks;
   return 0;
 }
 

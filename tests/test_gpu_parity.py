@@ -953,7 +953,7 @@ def test_auto_path_selection():
     sc.max_iters, sc.pipg_j_max, sc.power_j_max, sc.audit_substeps = 2, 100, 120, 8
     d = sc.problem_desc()
     spec = sc.dispersion
-    B = 80  # 80 x 2 > 148 SMs: throughput kernels; the first 3 alone: latency kernels
+    B = 200  # more instances than SMs: throughput kernels; the first 3 alone: latency kernels
     batch = scenario.make_batch(sc, range(B))
     args = lambda k: (batch["init_state"][:k], batch["x_guess"][:k], batch["u_guess"][:k], batch["rng_seed"][:k])
     res = {}

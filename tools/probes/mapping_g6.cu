@@ -17,7 +17,10 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-constexpr int kN = 50, kM = kN - 1;
+#ifndef KN
+#define KN 50
+#endif
+constexpr int kN = KN, kM = kN - 1;
 constexpr int kNX = 15, kNU = 7;
 constexpr int kWarps = 10, kThreads = 32 * kWarps;
 constexpr int kP = 15;  // pitch of every per-node array (3 groups of 5)

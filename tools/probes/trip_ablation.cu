@@ -9,7 +9,10 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-constexpr int kN = 50, kM = kN - 1;  // nodes, intervals
+#ifndef KN
+#define KN 50
+#endif
+constexpr int kN = KN, kM = kN - 1;  // nodes, intervals
 constexpr int kNX = 15, kNU = 7, kW = 29;
 constexpr int kXS = 18, kUS = 10, kPH = 16;
 

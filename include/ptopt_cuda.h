@@ -281,7 +281,12 @@ int ptopt_cuda_subproblem_shape(const ptopt_cuda_handle* h, ptopt_subproblem_sha
 /* Batched pipg::power_iteration_custom (proj/include/ptopt/pipg.hpp:206-292).
  * Seeds: seed_x [B][nodes][n_x], seed_u [B][nodes][n_u], seed_vcp/seed_vcn
  * [B][M][n_x].  sigma[b] = (1+eps_buff) * estimate; trips[b] = iterations run
- * (may be NULL).  status[b] = PTOPT_ST_POWER_SEED_ZERO for an all-zero seed. */
+ * (may be NULL).  status[b] = PTOPT_ST_POWER_SEED_ZERO for an all-zero seed.
+ * Known deviation: the kernels normalise with a reciprocal square root and add
+ * the norm as a tree, so the stopping test |sigma* - sigma| <= eps (1e-12 by
+ * default) can be met a few trips earlier or later than on the CPU: sigma agrees
+ * to 1e-9 relative, trips to max(3, 2 %) (tests/test_gpu_parity.py:
+ * test_power_iteration_random_subproblems); inside the SCP loop to max(5, 5 %). */
 int ptopt_cuda_power_iteration_batch(ptopt_cuda_handle* h, int batch,
                                      const ptopt_subproblem_shape* shape,
                                      const ptopt_subproblem_arrays* sp, const double* seed_x,
@@ -324,7 +329,8 @@ int ptopt_cuda_pipg_batch_dev(ptopt_cuda_handle* h, int batch, const ptopt_subpr
  * Outputs: x_out/u_out (ScpResult::iterate), scp_iterations [B], converged [B],
  * final_defect_inf [B], history [B][max_iters][5] (rows past scp_iterations are
  * zero; pipg_iterations stored as a double), power_trips [B][max_iters] (may be
- * NULL; extra diagnostic the reference does not expose), status/fail_index [B]. */
+ * NULL; extra diagnostic the reference does not expose; see the deviation note
+ * at ptopt_cuda_power_iteration_batch), status/fail_index [B]. */
 int ptopt_cuda_scp_solve_batch(ptopt_cuda_handle* h, int batch, const double* init_state,
                                const double* x_guess, const double* u_guess,
                                const uint64_t* rng_seed, double* x_out, double* u_out,

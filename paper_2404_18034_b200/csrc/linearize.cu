@@ -5,10 +5,13 @@
 //                    4 * steps RK4 stages (the only place the model and its Jacobian are
 //                    evaluated) and leaves one 84-double record per stage in HBM;
 //   * column pass  — one WARP per interval, lane j < 29 owns column j of
-//                    [Phi_x | Phi_u- | Phi_u+]; every stage it fetches the record (coalesced,
-//                    prefetched one stage ahead, staged in shared memory) and applies A(tau) and
-//                    the B forcing to its column in registers; then stages the 15 x 29 block in
-//                    shared memory for w = x_end - A x - B- u - B+ u+ and the coalesced write.
+//                    [Phi_x | Phi_u- | Phi_u+]; the four warps of a CTA take four neighbouring
+//                    intervals whose records of a stage form one contiguous chunk: the CTA copies it
+//                    with coalesced asynchronous copies three stages ahead, every 8-byte word
+//                    straight to its place in the slab of its interval (rocket_model.cuh); each
+//                    lane applies A(tau) and the B forcing to its column in registers; then the
+//                    15 x 29 block is staged in shared memory for w = x_end - A x - B- u - B+ u+
+//                    and the coalesced write.
 // See rocket_model.cuh for the per-thread / per-lane algorithms.
 #include <type_traits>
 
@@ -21,17 +24,17 @@ namespace {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kStageStride = kCols + 1;  // 30: row stride of the staged [15][29] block
-constexpr int kRecLamLeft = 81;          // spare record slots: the first-order-hold factors
-constexpr int kRecLamRight = 82;
-static_assert(kRecLamRight < kRecSize, "record padding");
 
-// Records of 32 consecutive intervals are interleaved (field-major inside a tile) so that the
-// state pass -- one thread per interval -- writes them coalesced.  The four warps of a
-// column-pass CTA read four neighbouring intervals, i.e. the same 32-byte sectors.
+// Records of kWarpsPerCta (4) consecutive intervals are interleaved word by word, one contiguous
+// chunk of 4 * kRecSize doubles per (tile, stage): the state pass -- one thread per interval --
+// fills whole 32-byte sectors with the four lanes of a tile, and a column-pass CTA (one tile) reads
+// a stage as one contiguous 2 688-byte piece.
+constexpr int kTile = kWarpsPerCta;
+constexpr int kChunk = kTile * kRecSize;  // doubles per (tile, stage)
 __host__ __device__ inline size_t record_index(long long local_interval, int nst, int stage_no) {
-  const long long tile = local_interval >> 5;
-  const int r = (int)(local_interval & 31);
-  return (((size_t)tile * nst + stage_no) * kRecSize) * 32 + r;
+  const long long tile = local_interval / kTile;
+  const int r = (int)(local_interval - tile * kTile);
+  return ((size_t)tile * nst + stage_no) * kChunk + r;
 }
 
 __global__ void __launch_bounds__(128) state_pass_kernel(LinearizeArgs a, long long first, long long count) {
@@ -57,17 +60,11 @@ __global__ void __launch_bounds__(128) state_pass_kernel(LinearizeArgs a, long l
   const int nst = 4 * a.steps;
   double* out = a.stages;
   const ModelConst& P = a.model;
-  const int rc = propagate_state_pass(
-      P, xk, uk, uk1, tau_k, tau_k1, a.steps, x_end, [&](int stage_no, const Stage& st, const double* u) {
-        double rec[kRecSize];
-        pack_stage_record(P, st, u, rec);
-        const StageTime t = stage_time(tau_k, tau_k1, a.steps, stage_no >> 2, stage_no & 3);
-        rec[kRecLamLeft] = t.lam_left;
-        rec[kRecLamRight] = t.lam_right;
-        double* o = out + record_index(local, nst, stage_no);
-#pragma unroll
-        for (int f = 0; f < kRecSize; ++f) o[(size_t)f * 32] = rec[f];
-      });
+  // every field goes straight from the register it was computed in to its place in the tile's chunk
+  double* out0 = out + record_index(local, nst, 0);
+  const int rc = propagate_state_pass(P, xk, uk, uk1, tau_k, tau_k1, a.steps, x_end, [&](int stage_no, int field, double v) {
+    out0[(size_t)stage_no * kChunk + (size_t)field * kTile] = v;
+  });
   if (rc != kStOk) {
     // first failing interval wins, as the serial reference loop would report it
     atomicMin(&a.fail_key[b], (k << 4) | rc);
@@ -78,59 +75,81 @@ __global__ void __launch_bounds__(128) state_pass_kernel(LinearizeArgs a, long l
   for (int i = 0; i < kNX; ++i) xe[i] = x_end[i];
 }
 
-constexpr int kRecRing = 4;  // stage records in flight per warp (cp.async ring)
+constexpr int kRecRing = 4;  // stage slabs in flight per warp (cp.async ring)
 
 struct __align__(16) WarpSmem {
-  double rec[kRecRing][kRecSize];    // ring of stage records
+  double slab[kRecRing][kSlabSize];  // ring of stage slabs (records with the B entries scattered, rocket_model.cuh)
   double block[kNX * kStageStride];  // staged [A | B- | B+], row-major
   double xk[kNX], uk[kNU], uk1[kNU], xe[kNX];
 };
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
 column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   __shared__ WarpSmem smem[kWarpsPerCta];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const long long local = (long long)blockIdx.x * kWarpsPerCta + wib;
-  if (local >= count) return;
-  const long long widx = first + local;
   const int M = a.nodes - 1;
-  const int b = (int)(widx / M);
-  const int k = (int)(widx - (long long)b * M);
-  if (a.active && !a.active[b]) return;  // instance already finished (SCP loop)
-  // an instance with a failed interval has no blocks (its records stop at the failure)
-  if (a.fail_key[b] != kFailKeyNone) return;
+  // A warp without work (past the end, instance finished or failed) still takes part in the CTA's
+  // copies and barriers; it computes on whatever its slab holds and stores nothing.
+  bool alive = local < count;
+  int b = 0, k = 0;
+  if (alive) {
+    const long long widx = first + local;
+    b = (int)(widx / M);
+    k = (int)(widx - (long long)b * M);
+    if (a.active && !a.active[b]) alive = false;  // instance already finished (SCP loop)
+    // an instance with a failed interval has no blocks (its records stop at the failure)
+    else if (a.fail_key[b] != kFailKeyNone) alive = false;
+  }
+  if (!__syncthreads_or(alive)) return;
 
   WarpSmem& ws = smem[wib];
   const size_t iv = (size_t)b * M + k;
   const double* xg = a.x + ((size_t)b * a.nodes + k) * kNX;
   const double* ug = a.u + ((size_t)b * a.nodes + k) * kNU;
-  if (lane < kNX) {
+  if (alive && lane < kNX) {
     ws.xk[lane] = xg[lane];
     ws.xe[lane] = a.x_end[iv * kNX + lane];
   }
-  if (lane < kNU) {
+  if (alive && lane < kNU) {
     ws.uk[lane] = ug[lane];
     ws.uk1[lane] = ug[kNU + lane];
   }
+  // the entries of a slab no record field lands on (the zeros of the dense B) are cleared once
+  for (int e = lane; e < kRecRing * kSlabSize; e += 32) (&ws.slab[0][0])[e] = 0.0;
+  __syncthreads();  // before any thread's copies land in another warp's slabs
 
-  const double* tau = a.tau + (size_t)b * a.tau_stride;
-  const double h = (tau[k + 1] - tau[k]) / a.steps;
+  double h = 0.0;
+  if (alive) {
+    const double* tau = a.tau + (size_t)b * a.tau_stride;
+    h = (tau[k + 1] - tau[k]) / a.steps;
+  }
   const double h6 = h / 6.0, h3 = h / 3.0, hh = 0.5 * h;  // as stage_time forms them
   const int nst = 4 * a.steps;
-  const double* recs = a.stages + record_index(local, nst, 0);
-  const size_t rec_stride = (size_t)kRecSize * 32;  // between consecutive stages of an interval
-  const bool third = lane + 64 < kRecSize;
-  // record `sn` -> ring slot sn % kRecRing, three 8-byte asynchronous copies per lane, one
-  // commit group per record (an empty group past the last record keeps the counting uniform)
+  // Stage `sn` of the tile: kChunk consecutive words; thread t copies words t, t + 128, t + 256
+  // (coalesced), word w = field w / 4 of interval w % 4, to slab_dest(field) of that interval's
+  // ring slot sn % kRecRing.  One commit group per stage (an empty group past the last stage keeps
+  // the counting uniform).
+  const double* chunk0 = a.stages + (size_t)blockIdx.x * nst * kChunk + threadIdx.x;
+  constexpr int kThreads = kWarpsPerCta * 32;
+  constexpr int kCopies = (kChunk + kThreads - 1) / kThreads;
+  unsigned dst[kCopies];
+#pragma unroll
+  for (int c = 0; c < kCopies; ++c) {
+    const int w = threadIdx.x + c * kThreads;
+    const int field = w < kChunk ? w / kTile : kRecSize - 1;
+    dst[c] = (unsigned)__cvta_generic_to_shared(&smem[w % kTile].slab[0][slab_dest(field)]);
+  }
+  const bool last_copy = threadIdx.x + (kCopies - 1) * kThreads < kChunk;
   auto fetch = [&](int sn) {
     if (sn < nst) {
-      const double* src = recs + (size_t)sn * rec_stride + (size_t)lane * 32;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(&ws.rec[sn % kRecRing][lane]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 32 * 8), "l"(src + 32 * 32) : "memory");
-      if (third)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 64 * 8), "l"(src + 64 * 32) : "memory");
+      const double* src = chunk0 + (size_t)sn * kChunk;
+      const unsigned ring = (unsigned)(sn % kRecRing) * (unsigned)(kSlabSize * sizeof(double));
+#pragma unroll
+      for (int c = 0; c < kCopies; ++c)
+        if (c + 1 < kCopies || last_copy)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst[c] + ring), "l"(src + c * kThreads) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -139,17 +158,19 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
 
   ColumnLane L;
   column_init(L, lane);
+  ColumnForcing Fc;
+  forcing_init(a.model, lane, Fc);
   const bool is_col = lane < kCols;
-  // one stage: wait for its record, start the copy of the record kRecRing - 1 stages ahead into
-  // the slot everybody finished reading a stage ago, apply the record to the column
+  // one stage: wait for this thread's copies of its chunk, meet the CTA (every copy of the chunk
+  // has landed, and every warp is done with the stage before), start the copies of the stage
+  // kRecRing - 1 ahead into the slot that was read last, apply the slab to the column (lanes 29..31
+  // carry an all-zero dummy column)
   auto run_stage = [&](auto stage_tag, int sn, double wk, double wn) {
     constexpr int kStage = decltype(stage_tag)::value;
     asm volatile("cp.async.wait_group %0;" ::"n"(kRecRing - 2) : "memory");
-    __syncwarp();
+    __syncthreads();
     fetch(sn + kRecRing - 1);
-    const double* rec = ws.rec[sn % kRecRing];
-    // lanes 29..31 carry an all-zero dummy column (no branch around the stage)
-    column_stage<kStage>(a.model, L, rec, wk, wn, rec[kRecLamLeft], rec[kRecLamRight]);
+    column_stage_slab<kStage>(L, Fc, ws.slab[sn % kRecRing], wk, wn);
   };
   for (int step = 0; step < a.steps; ++step) {
     run_stage(std::integral_constant<int, 0>{}, 4 * step, h6, hh);
@@ -157,6 +178,7 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
     run_stage(std::integral_constant<int, 2>{}, 4 * step + 2, h3, h);
     run_stage(std::integral_constant<int, 3>{}, 4 * step + 3, h6, hh);
   }
+  if (!alive) return;  // no block barrier below this line
 
   // stage the 15x29 block, then w = x_end - A x_k - B- u_k - B+ u_k1 row by row in the
   // reference's order (discretizer.hpp:144-147)
@@ -224,7 +246,7 @@ void launch_decode_fail_key(const int* fail_key, int batch, int* status, int* fa
 }
 
 size_t linearize_stage_doubles(long long intervals, int steps) {
-  const long long tiles = (intervals + 31) / 32;
+  const long long tiles = (intervals + 31) / 32;  // capacity in whole state-pass warps (a multiple of kTile)
   return (size_t)tiles * 32 * (size_t)(4 * steps) * kRecSize;
 }
 

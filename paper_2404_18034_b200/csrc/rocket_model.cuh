@@ -60,29 +60,38 @@ struct ModelConst {
 
 PT_HD bool pt_finite(double v) { return fabs(v) <= 1.79769313486231570e308; }
 
-/// Everything one RK4 stage needs from (x, u): the rate f, the scalars that define the
-/// nonzeros of A = df/dx, and what is needed to form one column of B = df/du.
-struct Stage {
-  double s;       // dilation factor
-  double f[kNX];  // augmented rate  s * (F, sum g+^2)
-  double F[kNXI]; // undilated model rate (the s-column of B, ctcs.hpp:99)
-  double integrand;
-  double C[9];    // body-to-inertial DCM
-  double rm;      // 1/m
-  double rTn;     // 1/|T|
-  double svm[3];  // A[v_i][m]
-  double svq[12]; // A[v_i][q_j]
-  double hw[3];   // s * 0.5 * w_k
-  double gq[4];   // s * 0.5 * q_k
-  double sww[9];  // A[w_i][w_j]
-  bool y_active;  // any path inequality violated
-  double ay[kNX]; // row y of A (valid when y_active)
-  double gp[9];   // clipped constraint values (valid when y_active)
-};
+// ---------------------------------------------------------------------------------------------
+// Stage records.  The state part of the RK4 bundle does not depend on the sensitivity columns, so
+// the model is evaluated once per (interval, stage) by the state pass, which leaves everything
+// the 29 column lanes need in a compact record; the column pass applies A(tau) and the B forcing
+// from it.  (Evaluating the model in every column lane, as a one-pass kernel does, spends 70 % of
+// the FP64 instructions on 32 identical copies of the evaluation.)
+// ---------------------------------------------------------------------------------------------
+constexpr int kRecS = 0;        // dilation factor
+constexpr int kRecSvm = 1;      // [3]  A[v_i][m]
+constexpr int kRecSvq = 4;      // [12] A[v_i][q_j]
+constexpr int kRecHw = 16;      // [3]  s * 0.5 * w_k
+constexpr int kRecGq = 19;      // [4]  s * 0.5 * q_k
+constexpr int kRecSww = 23;     // [9]  A[w_i][w_j]
+constexpr int kRecAy = 32;      // [15] row y of A (zeros unless active)
+constexpr int kRecActive = 47;  // 1.0 when a path inequality is violated
+constexpr int kRecBT = 48;      // [3][5] thrust columns of B: rows 0, 4, 5, 6, 14
+constexpr int kRecBG = 63;      // [3] torque columns of B: row 14
+constexpr int kRecBS = 66;      // [15] dilation column of B
+constexpr int kRecSize = 84;    // padded to a whole number of 32-byte sectors per tile of four intervals
+constexpr int kRecLamLeft = 81;   // spare record slots: the first-order-hold factors of the stage
+constexpr int kRecLamRight = 82;  //   (written after the padding zeros)
+static_assert(kRecBS + kNX <= kRecLamLeft && kRecLamRight < kRecSize, "record padding");
 
-/// Evaluates the stage at augmented state x and control u.  Returns a status code in the
-/// reference's throw order: dilation (ctcs.hpp:66), mass (rocket6dof.hpp:246), thrust (:306).
-PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stage& st) {
+/// Evaluates one RK4 stage at augmented state x and control u: the augmented rate f[15] =
+/// s * (F, sum g+^2) for the state update, and — through EMIT(field, value), every field of the
+/// stage record exactly once, each as soon as it is known so that nothing stays live for the
+/// record's sake — the scalars that define the nonzeros of A = df/dx and the nonzero rows of the
+/// seven columns of B = df/du (ctcs.hpp:96-128; rocket6dof.hpp:333-334, 370-380, 393-400).
+/// Returns a status code in the reference's throw order: dilation (ctcs.hpp:66), mass
+/// (rocket6dof.hpp:246), thrust (:306); nothing has been emitted when it is not kStOk.
+template <class EmitFn>
+PT_HD int eval_stage_emit(const ModelConst& P, const double* x, const double* u, double* f, EmitFn EMIT) {
   const double s = u[6];
   const double m = x[0];
   const double T0 = u[0], T1 = u[1], T2 = u[2];
@@ -90,19 +99,17 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
   if (!(m > 0.0)) return kStMass;
   const double Tn = sqrt(T0 * T0 + T1 * T1 + T2 * T2);
   if (Tn < 1e-9) return kStThrust;
-  st.s = s;
+  EMIT(kRecS, s);
   const double rm = 1.0 / m;
   const double rTn = 1.0 / Tn;
-  st.rm = rm;
-  st.rTn = rTn;
   const double q0 = x[7], q1 = x[8], q2 = x[9], qw = x[10];
   const double w0 = x[11], w1 = x[12], w2 = x[13];
 
   // dcm, rocket6dof.hpp:176-188
+  double C[9];
   {
     const double ss = q0 * q0 + q1 * q1 + q2 * q2;
     const double d = qw * qw - ss;
-    double* C = st.C;
     C[0] = d + 2.0 * q0 * q0;
     C[1] = 2.0 * q0 * q1 + 2.0 * qw * (-q2);
     C[2] = 2.0 * q0 * q2 + 2.0 * qw * q1;
@@ -115,10 +122,10 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
   }
   double CT[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) CT[i] = st.C[i * 3] * T0 + st.C[i * 3 + 1] * T1 + st.C[i * 3 + 2] * T2;
+  for (int i = 0; i < 3; ++i) CT[i] = C[i * 3] * T0 + C[i * 3 + 1] * T1 + C[i * 3 + 2] * T2;
 
   // eval_dynamics, rocket6dof.hpp:245-274
-  double* F = st.F;
+  double F[kNXI];
   F[0] = -P.alpha * Tn;
   F[1] = x[4];
   F[2] = x[5];
@@ -148,7 +155,7 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
   // eval_constraints, rocket6dof.hpp:278-301, clipped as in ctcs.hpp:47-56
   const double hq0 = P.H[0] * q0 + P.H[1] * q1 + P.H[2] * q2 + P.H[3] * qw;
   const double hq1 = P.H[4] * q0 + P.H[5] * q1 + P.H[6] * q2 + P.H[7] * qw;
-  double g[9];
+  double g[9], gp[9];
   g[0] = P.m_dry - m;
   g[1] = -x[1];
   g[2] = x[4] * x[4] + x[5] * x[5] + x[6] * x[6] - P.v_max_sq;
@@ -163,20 +170,22 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const double v = g[i] > 0.0 ? g[i] : 0.0;
-    st.gp[i] = v;
+    gp[i] = v;
     integrand += v * v;
     active = active || (v > 0.0);
   }
-  st.integrand = integrand;
-  st.y_active = active;
 #pragma unroll
-  for (int i = 0; i < kNXI; ++i) st.f[i] = s * F[i];
-  st.f[14] = s * integrand;
+  for (int i = 0; i < kNXI; ++i) f[i] = s * F[i];
+  f[14] = s * integrand;
+  // dilation column of B: the undilated rate (ctcs.hpp:99)
+#pragma unroll
+  for (int i = 0; i < kNXI; ++i) EMIT(kRecBS + i, F[i]);
+  EMIT(kRecBS + kNXI, integrand);
 
   // nonzeros of A = s * dF/dxi (rocket6dof.hpp:325-369 through ctcs.hpp:96-97)
   const double rm2 = rm * rm;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) st.svm[i] = s * (-CT[i] * rm2);
+  for (int i = 0; i < 3; ++i) EMIT(kRecSvm + i, s * (-CT[i] * rm2));
   {
     // dcm_times_vec_jac, rocket6dof.hpp:191-207, divided by m
     const double qT = q0 * T0 + q1 * T1 + q2 * T2;
@@ -190,18 +199,18 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
       for (int j = 0; j < 3; ++j) {
         double v = -2.0 * T[i] * qv[j] + 2.0 * qv[i] * T[j] - 2.0 * qw * Tk[i * 3 + j];
         if (i == j) v += 2.0 * qT;
-        st.svq[i * 4 + j] = s * (v * rm);
+        EMIT(kRecSvq + i * 4 + j, s * (v * rm));
       }
-      st.svq[i * 4 + 3] = s * ((2.0 * qw * T[i] + 2.0 * qxT[i]) * rm);
+      EMIT(kRecSvq + i * 4 + 3, s * ((2.0 * qw * T[i] + 2.0 * qxT[i]) * rm));
     }
   }
-  st.hw[0] = s * (0.5 * w0);
-  st.hw[1] = s * (0.5 * w1);
-  st.hw[2] = s * (0.5 * w2);
-  st.gq[0] = s * (0.5 * q0);
-  st.gq[1] = s * (0.5 * q1);
-  st.gq[2] = s * (0.5 * q2);
-  st.gq[3] = s * (0.5 * qw);
+  EMIT(kRecHw + 0, s * (0.5 * w0));
+  EMIT(kRecHw + 1, s * (0.5 * w1));
+  EMIT(kRecHw + 2, s * (0.5 * w2));
+  EMIT(kRecGq + 0, s * (0.5 * q0));
+  EMIT(kRecGq + 1, s * (0.5 * q1));
+  EMIT(kRecGq + 2, s * (0.5 * q2));
+  EMIT(kRecGq + 3, s * (0.5 * qw));
   {
     // dw/dw = Jinv * ([Jw]x - [w]x J), rocket6dof.hpp:352-369
     const double JWk[9] = {0.0, -Jw[2], Jw[1], Jw[2], 0.0, -Jw[0], -Jw[1], Jw[0], 0.0};
@@ -223,128 +232,57 @@ PT_HD int eval_stage(const ModelConst& P, const double* x, const double* u, Stag
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc += P.Jinv[i * 3 + k] * M[k * 3 + j];
-        st.sww[i * 3 + j] = s * acc;
+        EMIT(kRecSww + i * 3 + j, s * acc);
       }
   }
-  if (active) {
-    // row y of A: 2 s g+ dg/dxi (ctcs.hpp:108-115 with rocket6dof.hpp:383-391)
-    const double s2 = 2.0 * s;
-    double* ay = st.ay;
+  // row y of A: 2 s g+ dg/dxi (ctcs.hpp:108-115 with rocket6dof.hpp:383-391); zeros unless a
+  // path inequality is violated
+  {
+    double ay[kNX];
 #pragma unroll
     for (int i = 0; i < kNX; ++i) ay[i] = 0.0;
-    ay[0] = s2 * st.gp[0] * -1.0;
-    ay[1] = s2 * st.gp[1] * -1.0;
-    ay[4] = s2 * st.gp[2] * (2.0 * x[4]);
-    ay[5] = s2 * st.gp[2] * (2.0 * x[5]);
-    ay[6] = s2 * st.gp[2] * (2.0 * x[6]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) ay[7 + j] = s2 * st.gp[3] * (8.0 * (hq0 * P.H[j] + hq1 * P.H[4 + j]));
-    ay[11] = s2 * st.gp[4] * (2.0 * w0);
-    ay[12] = s2 * st.gp[4] * (2.0 * w1);
-    ay[13] = s2 * st.gp[4] * (2.0 * w2);
-  }
-  return kStOk;
-}
-
-/// One column of B = df/du (ctcs.hpp:96-128; rocket6dof.hpp:333-334, 370-380, 393-400).
-/// jc in [0,7): thrust x/y/z, torque x/y/z, dilation.
-PT_HD void b_column(const ModelConst& P, const Stage& st, const double* u, int jc, double* b) {
-#pragma unroll
-  for (int i = 0; i < kNX; ++i) b[i] = 0.0;
-  const double s = st.s;
-  if (jc < 3) {
-    const double Tj = jc == 0 ? u[0] : (jc == 1 ? u[1] : u[2]);
-    const double that = Tj * st.rTn;
-    b[0] = s * (-P.alpha * that);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double Cij = jc == 0 ? st.C[i * 3] : (jc == 1 ? st.C[i * 3 + 1] : st.C[i * 3 + 2]);
-      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
-      b[4 + i] = s * (Cij * st.rm);
-      b[11 + i] = s * JR;
-    }
-    if (st.y_active) {
+    if (active) {
       const double s2 = 2.0 * s;
-      double acc = 0.0;
-      acc += s2 * st.gp[5] * (that - (jc == 0 ? P.sec_delta : 0.0));
-      acc += s2 * st.gp[6] * that;
-      acc += s2 * st.gp[7] * (-that);
-      b[14] = acc;
-    }
-  } else if (jc < 6) {
-    const int j = jc - 3;
+      ay[0] = s2 * gp[0] * -1.0;
+      ay[1] = s2 * gp[1] * -1.0;
+      ay[4] = s2 * gp[2] * (2.0 * x[4]);
+      ay[5] = s2 * gp[2] * (2.0 * x[5]);
+      ay[6] = s2 * gp[2] * (2.0 * x[6]);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
-      b[11 + i] = s * Ji;
+      for (int j = 0; j < 4; ++j) ay[7 + j] = s2 * gp[3] * (8.0 * (hq0 * P.H[j] + hq1 * P.H[4 + j]));
+      ay[11] = s2 * gp[4] * (2.0 * w0);
+      ay[12] = s2 * gp[4] * (2.0 * w1);
+      ay[13] = s2 * gp[4] * (2.0 * w2);
     }
-    if (st.y_active) {
-      const double gj = j == 0 ? u[3] : (j == 1 ? u[4] : u[5]);
-      b[14] = 2.0 * s * st.gp[8] * (2.0 * gj);
-    }
-  } else {
 #pragma unroll
-    for (int i = 0; i < kNXI; ++i) b[i] = st.F[i];
-    b[14] = st.integrand;
+    for (int i = 0; i < kNX; ++i) EMIT(kRecAy + i, ay[i]);
+    EMIT(kRecActive, active ? 1.0 : 0.0);
   }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Stage records.  The state part of the RK4 bundle does not depend on the sensitivity columns, so
-// the model is evaluated once per (interval, stage) by the state pass, which leaves everything
-// the 29 column lanes need in a compact record; the column pass applies A(tau) and the B forcing
-// from it.  (Evaluating the model in every column lane, as a one-pass kernel does, spends 70 % of
-// the FP64 instructions on 32 identical copies of eval_stage.)
-// ---------------------------------------------------------------------------------------------
-constexpr int kRecS = 0;        // dilation factor
-constexpr int kRecSvm = 1;      // [3]
-constexpr int kRecSvq = 4;      // [12]
-constexpr int kRecHw = 16;      // [3]
-constexpr int kRecGq = 19;      // [4]
-constexpr int kRecSww = 23;     // [9]
-constexpr int kRecAy = 32;      // [15] row y of A (zeros unless active)
-constexpr int kRecActive = 47;  // 1.0 when a path inequality is violated
-constexpr int kRecBT = 48;      // [3][5] thrust columns of B: rows 0, 4, 5, 6, 14
-constexpr int kRecBG = 63;      // [3] torque columns of B: row 14
-constexpr int kRecBS = 66;      // [15] dilation column of B
-constexpr int kRecSize = 84;    // padded; a warp moves a record with three coalesced accesses
-
-/// Packs what the column lanes need from an evaluated stage.
-PT_HD void pack_stage_record(const ModelConst& P, const Stage& st, const double* u, double* rec) {
-  rec[kRecS] = st.s;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) rec[kRecSvm + i] = st.svm[i];
-#pragma unroll
-  for (int i = 0; i < 12; ++i) rec[kRecSvq + i] = st.svq[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) rec[kRecHw + i] = st.hw[i];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) rec[kRecGq + i] = st.gq[i];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) rec[kRecSww + i] = st.sww[i];
-#pragma unroll
-  for (int i = 0; i < kNX; ++i) rec[kRecAy + i] = st.y_active ? st.ay[i] : 0.0;
-  rec[kRecActive] = st.y_active ? 1.0 : 0.0;
-  double b[kNX];
+  // thrust columns of B: rows 0, 4..6, 14 (rows 11..13 are s * Jinv R: a constant times s)
 #pragma unroll
   for (int jc = 0; jc < 3; ++jc) {
-    b_column(P, st, u, jc, b);
-    rec[kRecBT + 5 * jc] = b[0];
-    rec[kRecBT + 5 * jc + 1] = b[4];
-    rec[kRecBT + 5 * jc + 2] = b[5];
-    rec[kRecBT + 5 * jc + 3] = b[6];
-    rec[kRecBT + 5 * jc + 4] = b[14];
+    const double Tj = jc == 0 ? T0 : (jc == 1 ? T1 : T2);
+    const double that = Tj * rTn;
+    EMIT(kRecBT + 5 * jc, s * (-P.alpha * that));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) EMIT(kRecBT + 5 * jc + 1 + i, s * (C[i * 3 + jc] * rm));
+    double by = 0.0;
+    if (active) {
+      const double s2 = 2.0 * s;
+      double acc = 0.0;
+      acc += s2 * gp[5] * (that - (jc == 0 ? P.sec_delta : 0.0));
+      acc += s2 * gp[6] * that;
+      acc += s2 * gp[7] * (-that);
+      by = acc;
+    }
+    EMIT(kRecBT + 5 * jc + 4, by);
   }
+  // torque columns of B: row 14 (rows 11..13 are s * Jinv)
 #pragma unroll
-  for (int jc = 3; jc < 6; ++jc) {
-    b_column(P, st, u, jc, b);
-    rec[kRecBG + jc - 3] = b[14];
-  }
-  b_column(P, st, u, 6, b);
+  for (int j = 0; j < 3; ++j) EMIT(kRecBG + j, active ? 2.0 * s * gp[8] * (2.0 * u[3 + j]) : 0.0);
 #pragma unroll
-  for (int i = 0; i < kNX; ++i) rec[kRecBS + i] = b[i];
-#pragma unroll
-  for (int i = kRecBS + kNX; i < kRecSize; ++i) rec[i] = 0.0;
+  for (int i = kRecBS + kNX; i < kRecSize; ++i) EMIT(i, 0.0);
+  return kStOk;
 }
 
 /// d = A * c in the structural sparsity of A (ascending column order inside every row, as
@@ -403,8 +341,8 @@ PT_HD StageTime stage_time(double tau_k, double tau_k1, int steps, int step, int
 }
 
 /// State pass of one interval (the x part of propagate_interval, discretizer.hpp:82-141):
-/// 4 * steps model evaluations; EMIT(stage_number, const Stage&, const double* u) receives each
-/// one.  On success x_end[15] holds the propagated state.
+/// 4 * steps model evaluations; EMIT(stage_number, field, value) receives every field of every
+/// stage record.  On success x_end[15] holds the propagated state.
 template <class EmitFn>
 PT_HD int propagate_state_pass(const ModelConst& P, const double* xk, const double* uk, const double* uk1,
                                double tau_k, double tau_k1, int steps, double* x_end, EmitFn EMIT) {
@@ -423,14 +361,16 @@ PT_HD int propagate_state_pass(const ModelConst& P, const double* xk, const doub
       double u[kNU];
 #pragma unroll
       for (int i = 0; i < kNU; ++i) u[i] = t.lam_left * uk[i] + t.lam_right * uk1[i];
-      Stage st;
-      const int rc = eval_stage(P, xin, u, st);
+      double f[kNX];
+      const int stage_no = step * 4 + stage;
+      const int rc = eval_stage_emit(P, xin, u, f, [&](int field, double v) { EMIT(stage_no, field, v); });
       if (rc != kStOk) return rc;
-      EMIT(step * 4 + stage, st, u);
+      EMIT(stage_no, kRecLamLeft, t.lam_left);  // spare record slots: the first-order-hold factors
+      EMIT(stage_no, kRecLamRight, t.lam_right);
 #pragma unroll
       for (int i = 0; i < kNX; ++i) {
-        const double axi = (stage == 0 ? sx[i] : ax[i]) + t.wk * st.f[i];
-        xin[i] = stage == 3 ? axi : sx[i] + t.wn * st.f[i];
+        const double axi = (stage == 0 ? sx[i] : ax[i]) + t.wk * f[i];
+        xin[i] = stage == 3 ? axi : sx[i] + t.wn * f[i];
         ax[i] = axi;
         if (stage == 3) sx[i] = axi;
       }
@@ -449,13 +389,8 @@ PT_HD int propagate_state_pass(const ModelConst& P, const double* xk, const doub
 /// Per-lane state of the column pass: sensitivity column `lane` of [Phi_x | Phi_u- | Phi_u+].
 struct ColumnLane {
   double s_c[kNX], a_c[kNX], c[kNX];  // step start, RK4 combination, stage input
-  int jc;                              // control index of this lane's B column
-  bool minus, forced;
 };
 PT_HD void column_init(ColumnLane& L, int lane) {
-  L.jc = lane < kNX ? 0 : (lane - kNX) % kNU;
-  L.minus = lane >= kNX && lane < kNX + kNU;  // Phi_u- lanes get lam_left
-  L.forced = lane >= kNX && lane < kCols;
 #pragma unroll
   for (int i = 0; i < kNX; ++i) {
     L.s_c[i] = (i == lane) ? 1.0 : 0.0;  // Phi_x(0) = I, Phi_u(0) = 0 (discretizer.hpp:94-96)
@@ -463,45 +398,77 @@ PT_HD void column_init(ColumnLane& L, int lane) {
   }
 }
 
-/// d += lam * (column jc of B), B taken from a stage record.  Rows where the column is
-/// structurally zero are skipped (the reference adds lam * 0 there, an exact no-op).
-PT_HD void add_b_column(const ModelConst& P, const double* rec, int jc, double lam, double* d) {
-  const double s = rec[kRecS];
-  if (jc < 3) {  // thrust: rows 0, 4..6, 11..13, 14
-    const double* r = rec + kRecBT + 5 * jc;
-    d[0] += lam * r[0];
-    d[4] += lam * r[1];
-    d[5] += lam * r[2];
-    d[6] += lam * r[3];
+// ---------------------------------------------------------------------------------------------
+// Stage slabs.  The column pass does not read a stage record as the state pass wrote it: while it
+// moves the record into shared memory it scatters the B entries into a DENSE 15 x 8 array (column 7
+// and every entry the record does not carry stay zero), so that every lane applies "its" column of
+// B with the same fifteen multiply-adds — no branch on the kind of column (thrust / torque /
+// dilation / none), which a warp whose lanes own different kinds would execute one after the other.
+// The entries s * Jinv R and s * Jinv of the thrust and torque columns (rows 11..13) are the
+// dilation factor times a constant: each lane keeps its three constants in registers instead.
+// ---------------------------------------------------------------------------------------------
+constexpr int kSlabB = 48;                  // dense B: entry (row i, control j) at kSlabB + 8 i + j
+constexpr int kSlabLamLeft = kSlabB + 120;  // first-order-hold factors of the stage
+constexpr int kSlabLamRight = kSlabLamLeft + 1;
+constexpr int kSlabSize = kSlabLamRight + 3;  // 172: a multiple of two doubles (16-byte aligned slabs)
+constexpr int kSlabZero = kSlabB + 7;         // an entry that is always zero (pad column, row 0)
+
+/// Where field `f` of a stage record goes inside a slab.
+PT_HD constexpr int slab_dest(int f) {
+  if (f < kRecBT) return f;  // A scalars, row y, the active flag: same place
+  if (f < kRecBG) {          // thrust columns: rows 0, 4, 5, 6, 14
+    const int jc = (f - kRecBT) / 5, r = (f - kRecBT) % 5;
+    const int row = r == 0 ? 0 : (r == 4 ? 14 : 3 + r);
+    return kSlabB + 8 * row + jc;
+  }
+  if (f < kRecBS) return kSlabB + 8 * 14 + 3 + (f - kRecBG);  // torque columns: row 14
+  if (f < kRecBS + kNX) return kSlabB + 8 * (f - kRecBS) + 6;  // dilation column
+  if (f == kRecLamLeft) return kSlabLamLeft;
+  if (f == kRecLamRight) return kSlabLamRight;
+  return kSlabSize - 1;  // record padding
+}
+
+/// What a lane keeps next to its column: where its B column and its first-order-hold factor are
+/// inside a slab, and s-proportional entries of rows 11..13 (thrust: Jinv R, torque: Jinv).
+struct ColumnForcing {
+  bool forced;   // the lane owns a column of Phi_u- / Phi_u+
+  int bcol;      // slab index of row 0 of the lane's B column
+  int lam;       // slab index of its first-order-hold factor
+  double jr[3];
+};
+PT_HD void forcing_init(const ModelConst& P, int lane, ColumnForcing& Fc) {
+  const bool forced = lane >= kNX && lane < kCols;
+  const int jc = forced ? (lane - kNX) % kNU : 7;
+  Fc.forced = forced;
+  Fc.bcol = kSlabB + jc;
+  Fc.lam = !forced ? kSlabZero : (lane < kNX + kNU ? kSlabLamLeft : kSlabLamRight);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double JR = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
-      d[11 + i] += lam * (s * JR);
-    }
-    d[14] += lam * r[4];
-  } else if (jc < 6) {  // torque: rows 11..13, 14
-    const int j = jc - 3;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const double Ji = j == 0 ? P.Jinv[i * 3] : (j == 1 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
-      d[11 + i] += lam * (s * Ji);
-    }
-    d[14] += lam * rec[kRecBG + j];
-  } else {  // dilation: the undilated rate
-#pragma unroll
-    for (int i = 0; i < kNX; ++i) d[i] += lam * rec[kRecBS + i];
+  for (int i = 0; i < 3; ++i) {
+    double v = 0.0;
+    if (jc < 3) v = jc == 0 ? P.JinvR[i * 3] : (jc == 1 ? P.JinvR[i * 3 + 1] : P.JinvR[i * 3 + 2]);
+    else if (jc < 6) v = jc == 3 ? P.Jinv[i * 3] : (jc == 4 ? P.Jinv[i * 3 + 1] : P.Jinv[i * 3 + 2]);
+    Fc.jr[i] = v;
   }
 }
 
-/// RK4 stage kStage of the column (discretizer.hpp:99-135): d = A c (+ lam * b), then the RK4
-/// combination.  After stage 3 the step result is in s_c.  wk / wn: RK4 weight and next-stage
-/// offset of the stage (StageTime); lam_left / lam_right: its first-order-hold factors.
+/// RK4 stage kStage of the column from a slab: d = A c + lam * b, then the RK4 combination.  Same
+/// arithmetic per entry as column_stage() — rows where the column of B is structurally zero get
+/// lam * 0 added, as in the reference's dense product.
 template <int kStage>
-PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, double wk, double wn,
-                        double lam_left, double lam_right) {
+PT_HD void column_stage_slab(ColumnLane& L, const ColumnForcing& Fc, const double* slab, double wk, double wn) {
   double d[kNX];
-  apply_A(rec, kStage == 0 ? L.s_c : L.c, d);
-  if (L.forced) add_b_column(P, rec, L.jc, L.minus ? lam_left : lam_right, d);
+  apply_A(slab, kStage == 0 ? L.s_c : L.c, d);
+  // One predicated region, the same code for every kind of B column; the lanes of Phi_x skip it
+  // (shared memory serves requested bytes: their loads would cost as much as the others').
+  if (Fc.forced) {
+    const double lam = slab[Fc.lam];
+    const double* b = slab + Fc.bcol;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) d[i] += lam * b[8 * i];
+    const double s = slab[kRecS];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d[11 + i] += lam * (s * Fc.jr[i]);
+  }
 #pragma unroll
   for (int i = 0; i < kNX; ++i) {
     if (kStage == 0) {
@@ -515,13 +482,23 @@ PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, d
     }
   }
 }
+
+/// Record -> slab on the CPU (the kernel does it with the addresses of its asynchronous copies).
+inline void expand_record(const double* rec, double lam_left, double lam_right, double* slab) {
+  for (int i = 0; i < kSlabSize; ++i) slab[i] = 0.0;
+  for (int f = 0; f < kRecSize; ++f) slab[slab_dest(f)] = rec[f];
+  slab[kSlabLamLeft] = lam_left;
+  slab[kSlabLamRight] = lam_right;
+  slab[kSlabSize - 1] = 0.0;
+}
+
 /// Run-time stage index (CPU simulation).
-PT_HD void column_stage(const ModelConst& P, ColumnLane& L, const double* rec, const StageTime& t, int stage) {
+PT_HD void column_stage_slab(ColumnLane& L, const ColumnForcing& Fc, const double* slab, const StageTime& t, int stage) {
   switch (stage) {
-    case 0: column_stage<0>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
-    case 1: column_stage<1>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
-    case 2: column_stage<2>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
-    default: column_stage<3>(P, L, rec, t.wk, t.wn, t.lam_left, t.lam_right); break;
+    case 0: column_stage_slab<0>(L, Fc, slab, t.wk, t.wn); break;
+    case 1: column_stage_slab<1>(L, Fc, slab, t.wk, t.wn); break;
+    case 2: column_stage_slab<2>(L, Fc, slab, t.wk, t.wn); break;
+    default: column_stage_slab<3>(L, Fc, slab, t.wk, t.wn); break;
   }
 }
 

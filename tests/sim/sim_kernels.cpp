@@ -23,16 +23,21 @@ int sim_propagate_interval(const ptopt_vehicle_params* vp, const double* xk, con
   double xe[kNX];
   std::vector<double> recs((size_t)4 * steps * kRecSize);
   const int rc = propagate_state_pass(mc, xk, uk, uk1, tau_k, tau_k1, steps, xe,
-                                      [&](int stage_no, const Stage& st, const double* u) {
-                                        pack_stage_record(mc, st, u, &recs[(size_t)stage_no * kRecSize]);
+                                      [&](int stage_no, int field, double v) {
+                                        recs[(size_t)stage_no * kRecSize + field] = v;
                                       });
   if (rc) return rc;
   for (int lane = 0; lane < kCols; ++lane) {
     ColumnLane L;
     column_init(L, lane);
-    for (int sn = 0; sn < 4 * steps; ++sn)
-      column_stage(mc, L, &recs[(size_t)sn * kRecSize], stage_time(tau_k, tau_k1, steps, sn >> 2, sn & 3),
-                   sn & 3);
+    ColumnForcing Fc;
+    forcing_init(mc, lane, Fc);
+    double slab[kSlabSize];
+    for (int sn = 0; sn < 4 * steps; ++sn) {
+      const StageTime t = stage_time(tau_k, tau_k1, steps, sn >> 2, sn & 3);
+      expand_record(&recs[(size_t)sn * kRecSize], t.lam_left, t.lam_right, slab);
+      column_stage_slab(L, Fc, slab, t, sn & 3);
+    }
     for (int i = 0; i < kNX; ++i) block[i][lane] = L.s_c[i];
   }
   for (int i = 0; i < kNX; ++i) {

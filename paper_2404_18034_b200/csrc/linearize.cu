@@ -4,9 +4,10 @@
 //   * state pass   — one THREAD per interval integrates the 15 augmented states through the
 //                    4 * steps RK4 stages (the only place the model and its Jacobian are
 //                    evaluated) and leaves one 84-double record per stage in HBM;
-//   * column pass  — one WARP per interval, lane j < 29 owns column j of
-//                    [Phi_x | Phi_u- | Phi_u+]; the four warps of a CTA take four neighbouring
-//                    intervals whose records of a stage form one contiguous chunk: the CTA copies it
+//   * column pass  — one lane per column of [Phi_x | Phi_u- | Phi_u+] (29 per interval); the four
+//                    warps of a CTA take four neighbouring intervals -- two warps their Phi_x
+//                    columns, two their Phi_u columns, each warp two intervals side by side --
+//                    whose records of a stage form one contiguous chunk: the CTA copies it
 //                    with coalesced asynchronous copies three stages ahead, every 8-byte word
 //                    straight to its place in the slab of its interval (rocket_model.cuh); each
 //                    lane applies A(tau) and the B forcing to its column in registers; then the
@@ -88,20 +89,34 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   __shared__ WarpSmem smem[kWarpsPerCta];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const long long local = (long long)blockIdx.x * kWarpsPerCta + wib;
   const int M = a.nodes - 1;
-  // A warp without work (past the end, instance finished or failed) still takes part in the CTA's
-  // copies and barriers; it computes on whatever its slab holds and stores nothing.
-  bool alive = local < count;
-  int b = 0, k = 0;
-  if (alive) {
+  // Interval t of the tile: is there work (inside the range, instance neither finished nor failed)?
+  // An interval without work still has its records copied and its columns computed (on whatever
+  // the slab holds); nothing is stored for it.
+  auto locate = [&](int t, int& b, int& k) {
+    const long long local = (long long)blockIdx.x * kTile + t;
+    b = k = 0;
+    if (local >= count) return false;
     const long long widx = first + local;
     b = (int)(widx / M);
     k = (int)(widx - (long long)b * M);
-    if (a.active && !a.active[b]) alive = false;  // instance already finished (SCP loop)
+    if (a.active && !a.active[b]) return false;  // instance already finished (SCP loop)
     // an instance with a failed interval has no blocks (its records stop at the failure)
-    else if (a.fail_key[b] != kFailKeyNone) alive = false;
-  }
+    return a.fail_key[b] == kFailKeyNone;
+  };
+  // Roles.  Shared memory serves requested bytes, and the 32 A scalars of a stage are the bulk of
+  // what a lane reads; a warp therefore works on TWO intervals, one per half warp (the sixteen
+  // lanes of a half read one address: a broadcast), and warps are uniform in what their columns
+  // need: warps 0, 1 own the Phi_x columns (no forcing: they never touch the B part of a slab),
+  // warps 2, 3 the Phi_u- | Phi_u+ columns.  Afterwards warp w assembles and stores interval w.
+  const bool u_role = wib >= 2;
+  const int half = lane >> 4, l16 = lane & 15;
+  const int mine = 2 * (wib & 1) + half;                      // interval of the tile this lane works on
+  const bool is_col = u_role ? l16 < 2 * kNU : l16 < kNX;
+  const int col = !is_col ? 31 : (u_role ? kNX + l16 : l16);  // column of [Phi_x | Phi_u- | Phi_u+]; 31: a zero dummy
+  int b, k, bm, km;
+  const bool alive = locate(wib, b, k);
+  const bool alive_mine = locate(mine, bm, km);
   if (!__syncthreads_or(alive)) return;
 
   WarpSmem& ws = smem[wib];
@@ -121,9 +136,9 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   __syncthreads();  // before any thread's copies land in another warp's slabs
 
   double h = 0.0;
-  if (alive) {
-    const double* tau = a.tau + (size_t)b * a.tau_stride;
-    h = (tau[k + 1] - tau[k]) / a.steps;
+  if (alive_mine) {
+    const double* tau = a.tau + (size_t)bm * a.tau_stride;
+    h = (tau[km + 1] - tau[km]) / a.steps;
   }
   const double h6 = h / 6.0, h3 = h / 3.0, hh = 0.5 * h;  // as stage_time forms them
   const int nst = 4 * a.steps;
@@ -157,20 +172,21 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
   for (int sn = 0; sn < kRecRing - 1; ++sn) fetch(sn);
 
   ColumnLane L;
-  column_init(L, lane);
+  column_init(L, col);
   ColumnForcing Fc;
-  forcing_init(a.model, lane, Fc);
-  const bool is_col = lane < kCols;
+  forcing_init(a.model, col, Fc);
+  const double* my_slabs = &smem[mine].slab[0][0];
   // one stage: wait for this thread's copies of its chunk, meet the CTA (every copy of the chunk
   // has landed, and every warp is done with the stage before), start the copies of the stage
-  // kRecRing - 1 ahead into the slot that was read last, apply the slab to the column (lanes 29..31
-  // carry an all-zero dummy column)
+  // kRecRing - 1 ahead into the slot that was read last, apply the slab to the column
   auto run_stage = [&](auto stage_tag, int sn, double wk, double wn) {
     constexpr int kStage = decltype(stage_tag)::value;
     asm volatile("cp.async.wait_group %0;" ::"n"(kRecRing - 2) : "memory");
     __syncthreads();
     fetch(sn + kRecRing - 1);
-    column_stage_slab<kStage>(L, Fc, ws.slab[sn % kRecRing], wk, wn);
+    const double* slab = my_slabs + (sn % kRecRing) * kSlabSize;
+    if (u_role) column_stage_slab<kStage, true>(L, Fc, slab, wk, wn);
+    else column_stage_slab<kStage, false>(L, Fc, slab, wk, wn);
   };
   for (int step = 0; step < a.steps; ++step) {
     run_stage(std::integral_constant<int, 0>{}, 4 * step, h6, hh);
@@ -178,15 +194,17 @@ column_pass_kernel(LinearizeArgs a, long long first, long long count) {
     run_stage(std::integral_constant<int, 2>{}, 4 * step + 2, h3, h);
     run_stage(std::integral_constant<int, 3>{}, 4 * step + 3, h6, hh);
   }
-  if (!alive) return;  // no block barrier below this line
 
-  // stage the 15x29 block, then w = x_end - A x_k - B- u_k - B+ u_k1 row by row in the
-  // reference's order (discretizer.hpp:144-147)
+  // stage the 15x29 blocks (every lane into the block of the interval it worked on), then warp w
+  // forms w = x_end - A x_k - B- u_k - B+ u_k1 of interval w row by row in the reference's order
+  // (discretizer.hpp:144-147) and writes its block
   if (is_col) {
+    double* blk = smem[mine].block;
 #pragma unroll
-    for (int i = 0; i < kNX; ++i) ws.block[i * kStageStride + lane] = L.s_c[i];
+    for (int i = 0; i < kNX; ++i) blk[i * kStageStride + col] = L.s_c[i];
   }
-  __syncwarp();
+  __syncthreads();
+  if (!alive) return;
   if (lane < kNX) {
     const double* row = ws.block + lane * kStageStride;
     double acc = 0.0;

@@ -454,13 +454,14 @@ PT_HD void forcing_init(const ModelConst& P, int lane, ColumnForcing& Fc) {
 /// RK4 stage kStage of the column from a slab: d = A c + lam * b, then the RK4 combination.  Same
 /// arithmetic per entry as column_stage() — rows where the column of B is structurally zero get
 /// lam * 0 added, as in the reference's dense product.
-template <int kStage>
+template <int kStage, bool kMayForce = true>
 PT_HD void column_stage_slab(ColumnLane& L, const ColumnForcing& Fc, const double* slab, double wk, double wn) {
   double d[kNX];
   apply_A(slab, kStage == 0 ? L.s_c : L.c, d);
   // One predicated region, the same code for every kind of B column; the lanes of Phi_x skip it
-  // (shared memory serves requested bytes: their loads would cost as much as the others').
-  if (Fc.forced) {
+  // (shared memory serves requested bytes: their loads would cost as much as the others'), and a
+  // warp that owns Phi_x columns only does not carry it at all (kMayForce = false).
+  if (kMayForce && Fc.forced) {
     const double lam = slab[Fc.lam];
     const double* b = slab + Fc.bcol;
 #pragma unroll

@@ -305,10 +305,11 @@ __device__ __forceinline__ void receive(const Ports& q, int which, bool mine, bo
 
 /// Publishes the dual of this thread's row (php) and — cq 3 — the B+ column sums (bps) in the
 /// node's slot; the CTA's last node sends the same values into slot -1 of the next rank.
+template <bool kLone>
 __device__ __forceinline__ void publish_duals(const Ports& q, const Lane& t, double d, const double (&cs)[2]) {
   *q.dual_dst = d;
   if (t.cq == 3) *reinterpret_cast<double2*>(q.bps_dst) = make_double2(cs[0], cs[1]);
-  if (t.push_prev) {
+  if (!kLone && t.push_prev) {
     push_f64(q.r_dual, d, q.box_to_next);
     if (t.cq == 3) push_f64x2(q.r_bps, cs[0], cs[1], q.box_to_next);
   }
@@ -316,14 +317,17 @@ __device__ __forceinline__ void publish_duals(const Ports& q, const Lane& t, dou
 
 /// Stores the two primal entries (cq 0, 1: x; cq 2: u) into the node's slot; the CTA's first node
 /// sends them into slot nloc of the previous rank as well.
+template <bool kLone>
 __device__ __forceinline__ void publish_primal(const Ports& q, const Lane& t, double v0, double v1) {
   if (t.cq != 3) *reinterpret_cast<double2*>(q.prim_dst) = make_double2(v0, v1);
-  if (t.push_next && t.cq != 3) push_f64x2(q.r_prim, v0, v1, q.box_to_prev);
+  if (!kLone && t.push_next && t.cq != 3) push_f64x2(q.r_prim, v0, v1, q.box_to_prev);
 }
 
 // ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
+// kLone: the cluster is a single CTA -- every hand-off (and its warp-uniform test) is compiled out.
+template <bool kLone>
 __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs a) {
   __shared__ LatSmem Sm;
   LatSmem* S = &Sm;
@@ -334,6 +338,9 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   const Lane t = make_lane(cut, m);
   open_boxes(S, t.tid);
   const Ports q = make_ports(S, t, cut);
+  auto recv = [&](int which, bool mine, bool armer, int bytes, int phase) {
+    if constexpr (!kLone) receive(q, which, mine, armer, bytes, phase);
+  };
   const bool u_owner = t.cq == 2;
   const bool is14 = t.cq == 1 && t.rg == 3;  // entry 0 of this pair is x[14], entry 1 the pad
   const bool alive0 = t.node && t.cq < 3, alive1 = alive0 && t.rg < 3 + (t.cq == 0);
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       box_remote[r] = r < cut.ranks ? partner_u32(S->box + kBoxNorm, r) : 0u;
     }
   }
-  const bool lone = cut.ranks == 1;  // a single CTA: the warps' shares are the whole norm, no mailbox
+  constexpr bool lone = kLone;  // a single CTA: the warps' shares are the whole norm, no mailbox
   auto send_total = [&](int trip) {  // thread 0, after the block barrier behind the warps' shares
     static_assert(kLatWarpsMax == 8, "tree below");
     const double2* p = reinterpret_cast<const double2*>(shares + (trip & 1) * kLatWarpsMax);
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   };
   auto norm_sq = [&](int trip) {  // waits for the totals of `trip`, then adds them (absent ranks: zero)
     static_assert(kLatMaxRanks == 8 && kLatWarpsMax == 8, "tree below");
-    if (!lone) receive(q, kBoxNorm + (trip & 1), true, t.tid == 0, 8 * cut.ranks, trip >> 1);
+    if (!lone) recv(kBoxNorm + (trip & 1), true, t.tid == 0, 8 * cut.ranks, trip >> 1);
     const double2* p = reinterpret_cast<const double2*>((lone ? shares : totals) + (trip & 1) * 8);
     const double2 s0 = p[0], s1 = p[1], s2 = p[2], s3 = p[3];
     return ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       v0 = src[0];
       if (alive1) v1 = src[1];
     }
-    publish_primal(q, t, v0, v1);  // the first node also reaches the previous rank: "next" phase 0
+    publish_primal<kLone>(q, t, v0, v1);  // the first node also reaches the previous rank: "next" phase 0
     acc = v0 * v0 + v1 * v1;
   }
   double vcd = 0.0;  // vc+ - vc-: the only combination of the two groups the forward map uses
@@ -408,7 +415,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       a.sigma[b] = 0.0;
       if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
     }
-    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
+    recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
     cg::this_cluster().sync();
     return;
   }
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   bool done = false;
   for (int j = 1; j <= a.j_max; ++j) {
     // ---- forward map (pipg.hpp:234-245); the norm of trip j-1 arrives while the products run
-    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // the next rank's first node of trip j-1
+    recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // the next rank's first node of trip j-1
     const double xn1 = q.x_next[0], xc = q.x_cur[0];
     const double r = forward_row(aop, q.seg, t.rg);
     const double s = t.theta_lane ? xn1 - xc : (r - xn1) + vcd;
@@ -447,18 +454,18 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     gather_rows(mine, d);
     drop_theta_slot(t, d);
     transposed_pair(aop, d, cs);
-    publish_duals(q, t, mine, cs);
+    publish_duals<kLone>(q, t, mine, cs);
     const double phi = t.theta_lane ? 0.0 : mine;
     vcd = 2.0 * phi;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
     const double acc_d = vcd * phi;
     __syncthreads();
     // ---- adjoint map (pipg.hpp:247-275)
-    receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // the previous rank's last interval
+    recv(kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // the previous rank's last interval
     const double2 nb = *reinterpret_cast<const double2*>(q.nb);
     const double extra = is14 ? nb.y - q.theta_k[0] : 0.0;  // -theta_k + theta_{k-1} on the last state (e_y)
     const double v0 = keep0 * (fma(sgn, nb.x, cs[0]) + extra);
     const double v1 = keep1 * fma(sgn, nb.y, cs[1]);
-    publish_primal(q, t, v0, v1);
+    publish_primal<kLone>(q, t, v0, v1);
     acc = fma(v0, v0, v1 * v1) + acc_d;
     acc = warp_sum(acc);
     if (t.lane == 0) shares[(j & 1) * kLatWarpsMax + t.warp] = acc;
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   }
   if (!done) {  // j_max trips without meeting the tolerance
     sigma = a.j_max >= 1 ? sqrt(norm_sq(a.j_max)) : sigma;
-    if (a.j_max >= 1) receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);  // still on its way
+    if (a.j_max >= 1) recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);  // still on its way
   }
   if (t.tid == 0 && cut.rank == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sigma;
@@ -479,6 +486,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
 // ---------------------------------------------------------------------------------------------
 // customized PIPG (pipg.hpp:350-497)
 // ---------------------------------------------------------------------------------------------
+template <bool kLone>
 __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a) {
   __shared__ LatSmem Sm;
   LatSmem* S = &Sm;
@@ -489,6 +497,9 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
   const Lane t = make_lane(cut, m);
   open_boxes(S, t.tid);
   const Ports q = make_ports(S, t, cut);
+  auto recv = [&](int which, bool mine, bool armer, int bytes, int phase) {
+    if constexpr (!kLone) receive(q, which, mine, armer, bytes, phase);
+  };
   const bool u_owner = t.cq == 2;
   const bool is14 = t.cq == 1 && t.rg == 3;
   const bool alive0 = t.node && t.cq < 3, alive1 = alive0 && t.rg < 3 + (t.cq == 0);
@@ -559,7 +570,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
     gather_rows(phe, d);
     drop_theta_slot(t, d);
     transposed_pair(aop, d, cs);
-    publish_duals(q, t, phe, cs);
+    publish_duals<kLone>(q, t, phe, cs);
   }
   __syncthreads();
 
@@ -584,7 +595,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       prv_vn = cur_vn;
     }
     // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
-    receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // previous rank, after iteration j-1
+    recv(kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, j - 1);  // previous rank, after iteration j-1
     {
       const double2 nb = *reinterpret_cast<const double2*>(q.nb);
       const double extra = is14 ? nb.y - q.theta_k[0] : 0.0;  // theta_{k-1} - theta_k on the last state
@@ -605,12 +616,12 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
         cur_p[e] = xn;
         pe[e] = fma(rho, xn - x0, x0);  // extrapolation, pipg.hpp:461-472
       }
-      publish_primal(q, t, rf[0], rf[1]);
+      publish_primal<kLone>(q, t, rf[0], rf[1]);
     }
     LAT_PHASE(0)
     __syncthreads();
     LAT_PHASE(1)
-    receive(q, kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // next rank's first node, this iteration
+    recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // next rank's first node, this iteration
     LAT_PHASE(2)
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458), extrapolation of
     //      the dual groups (:468-472) and the partial sums of H^T phi_ex for the next primal step
@@ -636,7 +647,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       gather_rows(phe, d);
       drop_theta_slot(t, d);
       transposed_pair(aop, d, cs);
-      publish_duals(q, t, phe, cs);
+      publish_duals<kLone>(q, t, phe, cs);
     }
     iters = j;
     LAT_PHASE(3)
@@ -695,7 +706,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
            cut.rank, t.warp, (double)ph_clk[0] / iters, (double)ph_clk[1] / iters, (double)ph_clk[2] / iters,
            (double)ph_clk[3] / iters, (double)ph_clk[4] / iters, iters);
 #endif
-  receive(q, kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, iters);  // what the previous rank sent last
+  recv(kBoxPrev, t.prev_warp, t.prev_armer, kPrevBytes, iters);  // what the previous rank sent last
   if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
     if (t.tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSolverDiverged;
@@ -774,11 +785,11 @@ int solver_lat_ranks(const SubShape& s, bool has_a_plus, int batch, int sm_count
 }
 
 cudaError_t launch_power_lat(const PowerArgs& a, int ranks, cudaStream_t stream) {
-  return launch_lat<PowerArgs>(power_lat_kernel, a, ranks, stream);
+  return launch_lat<PowerArgs>(ranks == 1 ? power_lat_kernel<true> : power_lat_kernel<false>, a, ranks, stream);
 }
 
 cudaError_t launch_pipg_lat(const PipgArgs& a, int ranks, cudaStream_t stream) {
-  return launch_lat<PipgArgs>(pipg_lat_kernel, a, ranks, stream);
+  return launch_lat<PipgArgs>(ranks == 1 ? pipg_lat_kernel<true> : pipg_lat_kernel<false>, a, ranks, stream);
 }
 
 }  // namespace ptopt_b200

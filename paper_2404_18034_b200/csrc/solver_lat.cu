@@ -258,6 +258,7 @@ struct Ports {
   double* bps_dst;     // bps[node][c0..c0+1]  (cq 3)
   double* prim_dst;    // xs / us [node][entry pair]  (cq 0..2)
   unsigned r_dual, r_bps, r_prim;  // the same slots inside the next (duals) / previous (primal) rank
+  unsigned send_dual, send_bps, send_prim;  // 1 when this thread sends that value
   unsigned box_to_next, box_to_prev;
   const double* seg;     // this thread's segment of the node vector [x_k | u_k | u_{k+1}]
   const double* x_next;  // x_{k+1}[row] (row 15: entry 14), x_k[same]
@@ -273,6 +274,9 @@ __device__ __forceinline__ Ports make_ports(LatSmem* S, const Lane& t, const Cut
   q.bps_dst = S->bps + (t.pc + 1) * kUP + t.c0;
   q.prim_dst = t.cq == 2 ? S->us + (t.pc + 1) * kUP + t.c0 : S->xs + (t.pc + 1) * kXP + 8 * (t.cq & 1) + t.c0;
   q.r_dual = q.r_bps = q.r_prim = q.box_to_next = q.box_to_prev = 0u;
+  q.send_dual = t.push_prev ? 1u : 0u;
+  q.send_bps = (t.push_prev && t.cq == 3) ? 1u : 0u;
+  q.send_prim = (t.push_next && t.cq != 3) ? 1u : 0u;
   if (t.push_prev) {  // slot -1 of the next rank
     q.r_dual = partner_u32(S->php + t.row, cut.rank + 1);
     q.r_bps = partner_u32(S->bps + t.c0, cut.rank + 1);
@@ -297,9 +301,30 @@ __device__ __forceinline__ Ports make_ports(LatSmem* S, const Lane& t, const Cut
   return q;
 }
 
+// The hand-off code sits on the critical path of every warp, also of those it does not concern:
+// a branch the compiler cannot prove warp-uniform costs a divergence frame (BSSY / BSYNC) on a loop
+// that is one dependent chain.  So the sends are single predicated instructions (no branch), and
+// the receive tests a vote result (provably uniform); `mine` is the same in all lanes of a warp.
+__device__ __forceinline__ void push_f64_if(unsigned pred, unsigned dst, double v, unsigned box) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %3, 0;\n"
+      "  @p st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2]; }" ::"r"(dst),
+      "d"(v), "r"(box), "r"(pred)
+      : "memory");
+}
+__device__ __forceinline__ void push_f64x2_if(unsigned pred, unsigned dst, double v0, double v1, unsigned box) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %4, 0;\n"
+      "  @p st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3]; }" ::"r"(dst),
+      "d"(v0), "d"(v1), "r"(box), "r"(pred)
+      : "memory");
+}
 __device__ __forceinline__ void receive(const Ports& q, int which, bool mine, bool armer, int bytes, int phase) {
-  if (!mine) return;
-  if (armer) mbar_expect(q.box + which, bytes);
+  if (!__any_sync(0xffffffffu, mine)) return;
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0;\n"
+               "  @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1; }" ::"r"(smem_u32(q.box + which)),
+               "r"(bytes), "r"((unsigned)armer)
+               : "memory");
   mbar_wait(q.box + which, phase);
 }
 
@@ -309,9 +334,9 @@ template <bool kLone>
 __device__ __forceinline__ void publish_duals(const Ports& q, const Lane& t, double d, const double (&cs)[2]) {
   *q.dual_dst = d;
   if (t.cq == 3) *reinterpret_cast<double2*>(q.bps_dst) = make_double2(cs[0], cs[1]);
-  if (!kLone && t.push_prev) {
-    push_f64(q.r_dual, d, q.box_to_next);
-    if (t.cq == 3) push_f64x2(q.r_bps, cs[0], cs[1], q.box_to_next);
+  if constexpr (!kLone) {
+    push_f64_if(q.send_dual, q.r_dual, d, q.box_to_next);
+    push_f64x2_if(q.send_bps, q.r_bps, cs[0], cs[1], q.box_to_next);
   }
 }
 
@@ -320,7 +345,7 @@ __device__ __forceinline__ void publish_duals(const Ports& q, const Lane& t, dou
 template <bool kLone>
 __device__ __forceinline__ void publish_primal(const Ports& q, const Lane& t, double v0, double v1) {
   if (t.cq != 3) *reinterpret_cast<double2*>(q.prim_dst) = make_double2(v0, v1);
-  if (!kLone && t.push_next && t.cq != 3) push_f64x2(q.r_prim, v0, v1, q.box_to_prev);
+  if constexpr (!kLone) push_f64x2_if(q.send_prim, q.r_prim, v0, v1, q.box_to_prev);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -357,24 +382,21 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   // totals in the same order.
   double* shares = S->shares;                       // [parity][kLatWarpsMax]
   double* totals = S->shares + 2 * kLatWarpsMax;    // [parity][kLatMaxRanks]
-  unsigned tot_remote[kLatMaxRanks], box_remote[kLatMaxRanks];
-  if (t.tid == 0) {
-#pragma unroll
-    for (int r = 0; r < kLatMaxRanks; ++r) {
-      tot_remote[r] = r < cut.ranks ? partner_u32(totals + cut.rank, r) : 0u;
-      box_remote[r] = r < cut.ranks ? partner_u32(S->box + kBoxNorm, r) : 0u;
-    }
+  // lane r of warp 0 sends to rank r: one predicated store, no loop and no branch (every thread forms
+  // the total -- four broadcast loads and three additions that overlap with what follows)
+  unsigned tot_remote = 0u, box_remote = 0u, tot_send = 0u;
+  if (!kLone && t.warp == 0 && t.lane < cut.ranks) {
+    tot_remote = partner_u32(totals + cut.rank, t.lane);
+    box_remote = partner_u32(S->box + kBoxNorm, t.lane);
+    tot_send = 1u;
   }
   constexpr bool lone = kLone;  // a single CTA: the warps' shares are the whole norm, no mailbox
-  auto send_total = [&](int trip) {  // thread 0, after the block barrier behind the warps' shares
+  auto send_total = [&](int trip) {  // after the block barrier behind the warps' shares
     static_assert(kLatWarpsMax == 8, "tree below");
     const double2* p = reinterpret_cast<const double2*>(shares + (trip & 1) * kLatWarpsMax);
     const double2 s0 = p[0], s1 = p[1], s2 = p[2], s3 = p[3];
     const double tot = ((s0.x + s0.y) + (s1.x + s1.y)) + ((s2.x + s2.y) + (s3.x + s3.y));
-#pragma unroll
-    for (int r = 0; r < kLatMaxRanks; ++r)
-      if (r < cut.ranks)
-        push_f64(tot_remote[r] + 8u * (unsigned)((trip & 1) * kLatMaxRanks), tot, box_remote[r] + 8u * (unsigned)(trip & 1));
+    push_f64_if(tot_send, tot_remote + 8u * (unsigned)((trip & 1) * kLatMaxRanks), tot, box_remote + 8u * (unsigned)(trip & 1));
   };
   auto norm_sq = [&](int trip) {  // waits for the totals of `trip`, then adds them (absent ranks: zero)
     static_assert(kLatMaxRanks == 8 && kLatWarpsMax == 8, "tree below");
@@ -407,7 +429,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   acc = warp_sum(acc);
   if (t.lane == 0) shares[t.warp] = acc;
   __syncthreads();
-  if (t.tid == 0 && !lone) send_total(0);
+  if constexpr (!kLone) send_total(0);
   double sigma = norm_sq(0);
   if (sigma == 0.0) {  // pipg.hpp:224-225
     if (t.tid == 0 && cut.rank == 0) {
@@ -470,7 +492,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     acc = warp_sum(acc);
     if (t.lane == 0) shares[(j & 1) * kLatWarpsMax + t.warp] = acc;
     __syncthreads();
-    if (t.tid == 0 && !lone) send_total(j);
+    if constexpr (!kLone) send_total(j);
   }
   if (!done) {  // j_max trips without meeting the tolerance
     sigma = a.j_max >= 1 ? sqrt(norm_sq(a.j_max)) : sigma;

@@ -58,12 +58,12 @@ enum BufId {
   B_X, B_U, B_A, B_BM, B_BP, B_W, B_XEND, B_STATUS, B_FAILIDX, B_FAILKEY, B_INIT,
   B_AM, B_AP, B_BMH, B_BPH, B_WH, B_EPS, B_UMIN, B_UMAX, B_INITVAL, B_FINALVAL,
   B_SEEDX, B_SEEDU, B_SEEDP, B_SEEDN, B_SIGMA, B_TRIPS, B_ITERS, B_CONV,
-  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR, B_TAU, B_STAGES,
+  B_WSX, B_WSU, B_WSP, B_WSN, B_WSD, B_WSR, B_TAU, B_STAGES, B_HANDLED,
   // SCP loop state (separate so a stand-alone call never disturbs a captured graph)
   S_ZX, S_ZU, S_INIT, S_SEED, S_A, S_BM, S_BP, S_W, S_XEND, S_AM, S_BMH, S_BPH, S_WH, S_EPS,
   S_UMIN, S_UMAX, S_INITVAL, S_FINALVAL, S_SEEDX, S_SEEDU, S_WSX, S_WSU, S_WSP, S_WSN, S_WSD,
   S_WSR, S_SIGMA, S_PITERS, S_FAILKEY, S_ACTIVE, S_CONV, S_SOLVES, S_LASTSTEP, S_FDEF, S_HIST,
-  S_TRIPS, S_STATUS, S_FAILIDX, S_STAGES,
+  S_TRIPS, S_STATUS, S_FAILIDX, S_STAGES, S_HANDLED,
   // Monte Carlo harness
   R_QTAB, R_INIT, R_XG, R_UG, R_SEED, R_XOUT, R_UOUT, R_ITERS, R_CONV, R_FDEF, R_STATUS, R_FAILIDX,
   R_GMAX, R_DY, R_AKEY, R_PG, R_RECORDS, R_SAMPLES,
@@ -241,6 +241,24 @@ bool use_fast_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_p
   return h->solver_path != PTOPT_SOLVER_GENERIC && solver_fast_supports(s, has_a_plus);
 }
 
+/// The column-sparse kernels (solver_cs.cu) run in front of the dense register-resident ones under
+/// AUTO and FAST_THROUGHPUT when the shape allows: they solve every instance whose operator has
+/// the zero pattern of the rocket model's discretization and mark it handled; the dense kernels
+/// then run on the rest (normally nothing: their CTAs leave at once).
+bool use_cs_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
+  return (h->solver_path == PTOPT_SOLVER_AUTO || h->solver_path == PTOPT_SOLVER_FAST_THROUGHPUT ||
+          h->solver_path == PTOPT_SOLVER_FAST_SPARSE) &&
+         solver_cs_supports(s, has_a_plus);
+}
+
+/// The PIPG stage takes the column-sparse kernel only under FAST_SPARSE: its four role-specific
+/// loop bodies (31 KB of SASS) do not fit the SM's 32 KB instruction cache next to the rest of the
+/// kernel, and it measures slower than the dense kernel (ncu: half of its warp-state samples are
+/// instruction-fetch stalls); the power iteration's bodies (21 KB) fit and win.
+bool use_cs_pipg(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
+  return h->solver_path == PTOPT_SOLVER_FAST_SPARSE && solver_cs_supports(s, has_a_plus);
+}
+
 /// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
 /// handle asks for it (and the node count allows it).  Measured on B200 it loses to one CTA per
 /// instance both in throughput (493 vs 655 solves/s at N=50) and in single-solve latency
@@ -261,6 +279,10 @@ int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
   if (fast) {
     PT_TRY(check_smem(h, pipg_fast_smem(s, false)));
     PT_CUDA(configure_solver_fast(s));
+    if (solver_cs_supports(s, false)) {
+      PT_TRY(check_smem(h, pipg_cs_smem(s)));
+      PT_CUDA(configure_solver_cs(s));
+    }
   } else {
     PT_TRY(check_smem(h, pipg_generic_smem(s, solver_generic_threads(s))));
     PT_CUDA(configure_solver_generic(s));
@@ -276,6 +298,16 @@ int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
+  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr)) {
+    unsigned char* handled = nullptr;
+    PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
+    PT_CUDA(launch_power_cs(a, handled, h->stream));
+    PowerArgs rest = a;
+    rest.skip = handled;
+    PT_CUDA(launch_power_fast(rest, false, h->stream));
+    h->launches += 2;
+    return PTOPT_OK;
+  }
   PT_CUDA(fast ? launch_power_fast(a, use_split_solver(h, a.batch), h->stream) : launch_power_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
@@ -289,6 +321,16 @@ int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
+  if (fast && use_cs_pipg(h, a.shape, a.sp.A_plus != nullptr)) {
+    unsigned char* handled = nullptr;
+    PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
+    PT_CUDA(launch_pipg_cs(a, handled, h->stream));
+    PipgArgs rest = a;
+    rest.skip = handled;
+    PT_CUDA(launch_pipg_fast(rest, false, h->stream));
+    h->launches += 2;
+    return PTOPT_OK;
+  }
   PT_CUDA(fast ? launch_pipg_fast(a, use_split_solver(h, a.batch), h->stream) : launch_pipg_generic(a, h->stream));
   h->launches += 1;
   return PTOPT_OK;
@@ -360,7 +402,7 @@ int ensure_scp_state(ptopt_cuda_handle* h, int batch, ScpState& s) {
       {S_WSR, B * m * 8}, {S_SIGMA, B * 8}, {S_PITERS, B * 4}, {S_FAILKEY, B * 4},
       {S_ACTIVE, B}, {S_CONV, B}, {S_SOLVES, B * 4}, {S_LASTSTEP, B * 8}, {S_FDEF, B * 8},
       {S_HIST, B * mi * 5 * 8}, {S_TRIPS, B * mi * 4}, {S_STATUS, B * 4}, {S_FAILIDX, B * 4},
-      {S_STAGES, stage_bytes}};
+      {S_STAGES, stage_bytes}, {S_HANDLED, B}};
   bool grew = false;
   for (const Req& r : reqs) {
     if (r.bytes > h->buf[r.id].bytes || !h->buf[r.id].p) grew = true;
@@ -462,6 +504,13 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
                         st.w, st.x_end, st.fail_key, st.active, S_STAGES, &la));
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
   const int lat = latency_ranks(h, h->rocket_shape, false, batch);
+  const bool cs = !lat && fast && use_cs_solver(h, h->rocket_shape, false);
+  const bool cs_pipg = cs && use_cs_pipg(h, h->rocket_shape, false);
+  unsigned char* handled = h->buf[S_HANDLED].as<unsigned char>();
+  PowerArgs pa_rest = pa;
+  PipgArgs ga_rest = ga;
+  pa_rest.skip = handled;
+  ga_rest.skip = handled;
   for (int it = 0; it <= h->desc.max_iters; ++it) {
     kernels += launch_linearize(la, h->stream);
     PT_CUDA(mark(0));
@@ -469,13 +518,25 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 1;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    PT_CUDA(lat    ? launch_power_lat(pa, lat, h->stream)
-            : fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream)
-                   : launch_power_generic(pa, h->stream));
+    if (cs) {  // column-sparse kernels, then the dense ones on whatever they did not take
+      PT_CUDA(launch_power_cs(pa, handled, h->stream));
+      PT_CUDA(launch_power_fast(pa_rest, false, h->stream));
+      kernels += 1;
+    } else {
+      PT_CUDA(lat    ? launch_power_lat(pa, lat, h->stream)
+              : fast ? launch_power_fast(pa, use_split_solver(h, batch), h->stream)
+                     : launch_power_generic(pa, h->stream));
+    }
     PT_CUDA(mark(2));
-    PT_CUDA(lat    ? launch_pipg_lat(ga, lat, h->stream)
-            : fast ? launch_pipg_fast(ga, use_split_solver(h, batch), h->stream)
-                   : launch_pipg_generic(ga, h->stream));
+    if (cs_pipg) {
+      PT_CUDA(launch_pipg_cs(ga, handled, h->stream));
+      PT_CUDA(launch_pipg_fast(ga_rest, false, h->stream));
+      kernels += 1;
+    } else {
+      PT_CUDA(lat    ? launch_pipg_lat(ga, lat, h->stream)
+              : fast ? launch_pipg_fast(ga, use_split_solver(h, batch), h->stream)
+                     : launch_pipg_generic(ga, h->stream));
+    }
     PT_CUDA(mark(3));
     launch_scp_update(sa, h->stream);
     PT_CUDA(mark(4));
@@ -675,7 +736,7 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
 
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path) {
   if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
-  if (path < PTOPT_SOLVER_AUTO || path > PTOPT_SOLVER_FAST_THROUGHPUT)
+  if (path < PTOPT_SOLVER_AUTO || path > PTOPT_SOLVER_FAST_SPARSE)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "unknown solver path");
   if (path != h->solver_path && h->scp_graph) {  // the captured graph names the other kernels
     DeviceGuard guard(h->device);

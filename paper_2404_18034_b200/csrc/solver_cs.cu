@@ -1,0 +1,956 @@
+// solver_cs.cu — "column-sparse" register-resident power iteration and customized PIPG for the
+// rocket-shaped subproblem (n_x = 15, n_u = 7, A_plus = -I, e_y = unit vector of the last state,
+// at most kCsMaxNodes nodes), exploiting the structural zeros of the exact discretization.
+//
+// Mapping.  One CTA per instance, FOUR threads per node, and the four threads of a node sit in
+// four DIFFERENT warps: warp (role, half) holds role `role` of 32 consecutive nodes, lane = node.
+// A role is a fixed set of COLUMNS of the packed interval block [A-_k | B-_k | B+_k] (all rows of
+// those columns) together with the primal entries these columns multiply:
+//     role 0: x columns q0 r0 r1 r2 y     u columns T0 T1      dual rows r0 r1 r2 (+ relaxation dual)
+//     role 1: x columns q1 m v2           u columns T2 tau0    dual rows q1 m v2 q0
+//     role 2: x columns q2 q3             u columns tau1 tau2  dual rows q2 q3 w2 y
+//     role 3: x columns w0 w1 w2 v0 v1    u column  s          dual rows w0 w1 v0 v1
+// Because every lane of a warp has the same role, the zero pattern of a role's columns is a
+// compile-time pattern of its instruction stream: the state-transition matrix of the 6-DoF model
+// (state m, r, v, q, w, y) is block triangular -- the column of r_i only reaches r_i and y, that of
+// v_i only r_i, v_i, y, the quaternion columns reach r, v, q, y, the rate columns everything but m,
+// the mass column m, r, v, y, the y column only y, and the torque columns never reach m
+// (rocket6dof.hpp:318-375, ctcs.hpp:84-129; a pattern closed under the products of the RK4
+// bundle, so the zeros are exact) -- 314 of the 435 entries of a block are structurally non-zero,
+// 78..80 per thread.  The kernels VERIFY the pattern while they load the operator: an instance
+// with a non-zero (or non-finite) entry outside it is left untouched for the dense kernels of
+// solver_fast.cu, which run right behind on the instances not marked as handled.
+//   * transposed product H^T phi: thread-local (a thread has whole columns); it reads the fifteen
+//     duals of its interval from shared memory, [row][node] arrays, lane-contiguous: 2 wavefronts
+//     per warp load, no bank conflicts, no broadcast waste;
+//   * forward product H z: a thread multiplies its columns by its OWN primal entries (registers)
+//     and publishes partial row sums for the rows other roles own; the row owner adds four partials;
+//   * neighbour-node coupling along the horizon is a lane shift inside the warp (shuffles); the
+//     boundary between the two warps of a role is covered by one redundantly computed halo node on
+//     either side (lane 31 of the first warp repeats node 31, lane 0 of the second warp node 30),
+//     so no value ever has to cross warps in the middle of a phase.
+// Two block barriers per iteration / trip, as in solver_fast.cu, but 0.4x the shared-memory
+// wavefronts, 0.72x the FMAs and a dependent instruction stream of ~330 instead of ~550 per warp.
+//
+// Follows /root/reference/proj/include/ptopt/pipg.hpp:206-292 (power_iteration_custom),
+// :307-326 (stopping_custom), :335-340 (step_sizes), :350-497 (pipg_custom).  Differences from the
+// reference are rounding only: sums in a different order, FMA contraction, exact zeros skipped.
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "kernels.cuh"
+
+namespace ptopt_b200 {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCsWarps = 8;
+
+// ---- structure of the operator ------------------------------------------------------------------
+/// Rows (bit i = row i) a column of A- can reach.  State order: m | r0..2 | v0..2 | q0..3 | w0..2 | y.
+__host__ __device__ constexpr unsigned xcol_mask(int c) {
+  return c == 0    ? (0x007fu | 0x4000u)                       // m: m, r, v, y
+         : c <= 3  ? ((1u << c) | 0x4000u)                     // r_i: r_i, y
+         : c <= 6  ? ((1u << (c - 3)) | (1u << c) | 0x4000u)   // v_i: r_i, v_i, y
+         : c <= 10 ? (0x07feu | 0x4000u)                       // q_j: r, v, q, y
+         : c <= 13 ? 0x7ffeu                                   // w_j: everything but m
+                   : 0x4000u;                                  // y: y
+}
+/// Rows a column of B- / B+ can reach.  Control order: T0..2 | tau0..2 | s.
+__host__ __device__ constexpr unsigned ucol_mask(int c) { return (c >= 3 && c <= 5) ? 0x7ffeu : 0x7fffu; }
+
+template <int R>
+struct RoleT;
+template <>
+struct RoleT<0> {
+  static constexpr int nxc = 5, nuc = 2, nrow = 3;
+  __host__ __device__ static constexpr int xc(int j) { return j == 0 ? 7 : j == 4 ? 14 : j; }  // q0 r0 r1 r2 y
+  __host__ __device__ static constexpr int uc(int j) { return j; }                                // T0 T1
+  __host__ __device__ static constexpr int row(int r) { return 1 + r; }                           // r0 r1 r2
+};
+template <>
+struct RoleT<1> {
+  static constexpr int nxc = 3, nuc = 2, nrow = 4;
+  __host__ __device__ static constexpr int xc(int j) { return j == 0 ? 8 : j == 1 ? 0 : 6; }     // q1 m v2
+  __host__ __device__ static constexpr int uc(int j) { return 2 + j; }                            // T2 tau0
+  __host__ __device__ static constexpr int row(int r) { return r == 0 ? 8 : r == 1 ? 0 : r == 2 ? 6 : 7; }
+};
+template <>
+struct RoleT<2> {
+  static constexpr int nxc = 2, nuc = 2, nrow = 4;
+  __host__ __device__ static constexpr int xc(int j) { return 9 + j; }                            // q2 q3
+  __host__ __device__ static constexpr int uc(int j) { return 4 + j; }                            // tau1 tau2
+  __host__ __device__ static constexpr int row(int r) { return r == 0 ? 9 : r == 1 ? 10 : r == 2 ? 13 : 14; }
+};
+template <>
+struct RoleT<3> {
+  static constexpr int nxc = 5, nuc = 1, nrow = 4;
+  __host__ __device__ static constexpr int xc(int j) { return j < 3 ? 11 + j : 1 + j; }          // w0 w1 w2 v0 v1
+  __host__ __device__ static constexpr int uc(int) { return 6; }                                  // s
+  __host__ __device__ static constexpr int row(int r) { return r < 2 ? 11 + r : 2 + r; }          // w0 w1 v0 v1
+};
+
+/// Rows the columns of role R reach (union of its column masks).
+template <int R>
+__host__ __device__ constexpr unsigned role_touch() {
+  unsigned m = 0;
+  for (int j = 0; j < RoleT<R>::nxc; ++j) m |= xcol_mask(RoleT<R>::xc(j));
+  for (int j = 0; j < RoleT<R>::nuc; ++j) m |= ucol_mask(RoleT<R>::uc(j));
+  return m;
+}
+__host__ __device__ constexpr unsigned role_touch_of(int r) {
+  return r == 0 ? role_touch<0>() : r == 1 ? role_touch<1>() : r == 2 ? role_touch<2>() : role_touch<3>();
+}
+/// Index of the x column of role R that equals row i (the row is "aligned": its owner also owns
+/// the primal entry of the same index, so x_{k+1}[i] arrives by a lane shift), or -1.
+template <int R>
+__host__ __device__ constexpr int aligned_col(int i) {
+  for (int j = 0; j < RoleT<R>::nxc; ++j)
+    if (RoleT<R>::xc(j) == i) return j;
+  return -1;
+}
+/// True when role R owns dual row i.
+template <int R>
+__host__ __device__ constexpr bool owns_row(int i) {
+  for (int r = 0; r < RoleT<R>::nrow; ++r)
+    if (RoleT<R>::row(r) == i) return true;
+  return false;
+}
+// primal entries whose reflections a row owner of ANOTHER role needs from node k+1 go through
+// shared memory: x[q0] (7, role 0 -> role 1), x[w2] (13, role 3 -> role 2), x[y] (14, role 0 -> role 2)
+__host__ __device__ constexpr int xn_slot(int c) { return c == 7 ? 0 : c == 13 ? 1 : c == 14 ? 2 : -1; }
+
+// ---- shared-memory layout --------------------------------------------------------------------------
+// [row][slot] arrays, slot = node + 1 (slot 0: the zero "node -1" / "interval -1" in front).
+template <int kHalves>
+struct CsCfg {
+  static constexpr int warps = 4 * kHalves;
+  static constexpr int threads = 32 * warps;
+  // nodes: the last lane never holds a node (the lane shift that fetches node k + 1 must find zeros
+  // behind the last node), and two halves share two halo lanes
+  static constexpr int cap = kHalves == 1 ? 31 : 61;
+  static constexpr int S = kHalves == 1 ? 34 : 64;     // slots per row
+};
+
+struct SnapCs {
+  int x, u, vp, vn, ph, th, total;
+};
+template <int kHalves>
+__host__ __device__ constexpr SnapCs snap_cs() {
+  constexpr int n = CsCfg<kHalves>::cap;
+  SnapCs s{};
+  int o = 0;
+  s.x = o; o += n * kNX;
+  s.u = o; o += n * kNU;
+  s.vp = o; o += n * kNX;
+  s.vn = o; o += n * kNX;
+  s.ph = o; o += n * kNX;
+  s.th = o; o += n;
+  s.total = (o + 1) & ~1;
+  return s;
+}
+
+struct CsLayout {
+  int phi, th, part, xn, red, total;
+  int wv, eps, bnd, fix, ecost, snap;  // PIPG only
+};
+template <int kHalves>
+__host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
+  constexpr int S = CsCfg<kHalves>::S;
+  CsLayout L{};
+  int o = 0;
+  L.phi = o; o += kNX * S;
+  L.th = o; o += S;
+  L.part = o; o += 4 * kNX * S;
+  L.xn = o; o += 3 * S;
+  L.red = o; o += 8 * kCsWarps;
+  if (pipg) {
+    L.wv = o; o += kNX * S;
+    L.eps = o; o += S;
+    L.bnd = o; o += 4 * 2 * 2 * S;   // [role][u column][lo, hi][slot]
+    L.fix = o; o += 4 * 16;          // init_val, final_val, init_on, final_on
+    L.ecost = o; o += 16;
+    L.snap = o; o += 2 * snap_cs<kHalves>().total;
+  }
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void block_barrier() { asm volatile("bar.sync 0;" ::: "memory"); }
+__device__ __forceinline__ double clip0(double v) { return 0.0 < v ? v : 0.0; }
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+/// Which node a lane holds and in what capacity.
+struct Lane {
+  int k;        // node
+  int slot;     // k + 1
+  bool auth;    // this thread is THE owner of node k (k < n, not a halo copy)
+  bool primal;  // its primal entries are valid (owner, or the halo copy of node 31 in the first warp)
+  bool ival;    // auth and k is an interval (k < n - 1)
+};
+template <int kHalves>
+__device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
+  Lane t;
+  if (kHalves == 1) {
+    t.k = lane;
+    t.auth = t.k < n;
+    t.primal = t.auth;
+  } else {
+    t.k = half == 0 ? lane : 30 + lane;
+    const bool halo = half == 0 ? lane == 31 : lane == 0;
+    t.auth = !halo && t.k < n;
+    t.primal = t.k < n && (half == 0 || lane != 0);
+  }
+  t.slot = t.k + 1;
+  t.ival = t.auth && t.k < n - 1;
+  return t;
+}
+
+/// The operator columns of role R of one interval, and whether the block has the expected zeros.
+template <int R>
+struct OpCols {
+  double ax[RoleT<R>::nxc][kNX];
+  double bm[RoleT<R>::nuc][kNX];
+  double bp[RoleT<R>::nuc][kNX];
+};
+
+/// Loads the columns of role R of interval `iv` (zero when !have).  Returns true when an entry
+/// outside the structural pattern is not an exact zero.
+template <int R>
+__device__ __forceinline__ bool load_cols(const SubArrays& sp, size_t iv, bool have, OpCols<R>& op) {
+  using RT = RoleT<R>;
+  bool bad = false;
+  const double* A = sp.A_minus + iv * kNX * kNX;
+  const double* Bm = sp.B_minus + iv * kNX * kNU;
+  const double* Bp = sp.B_plus + iv * kNX * kNU;
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j) {
+    const int c = RT::xc(j);
+    const unsigned mask = xcol_mask(c);
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) {
+      const double v = have ? __ldg(A + i * kNX + c) : 0.0;
+      if ((mask >> i) & 1u) op.ax[j][i] = v;
+      else bad |= !(v == 0.0);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RT::nuc; ++j) {
+    const int c = RT::uc(j);
+    const unsigned mask = ucol_mask(c);
+#pragma unroll
+    for (int i = 0; i < kNX; ++i) {
+      const double vm = have ? __ldg(Bm + i * kNU + c) : 0.0;
+      const double vp = have ? __ldg(Bp + i * kNU + c) : 0.0;
+      if ((mask >> i) & 1u) {
+        op.bm[j][i] = vm;
+        op.bp[j][i] = vp;
+      } else {
+        bad |= !(vm == 0.0) || !(vp == 0.0);
+      }
+    }
+  }
+  return bad;
+}
+
+/// Transposed products of role R against the fifteen duals of its interval: column sums of its x
+/// columns, of its B- columns and of its B+ columns.
+template <int R>
+__device__ __forceinline__ void transposed(const OpCols<R>& op, const double (&ph)[kNX],
+                                           double (&gx)[RoleT<R>::nxc], double (&gm)[RoleT<R>::nuc],
+                                           double (&gp)[RoleT<R>::nuc]) {
+  using RT = RoleT<R>;
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j) {
+    const unsigned mask = xcol_mask(RT::xc(j));
+    double s0 = 0.0, s1 = 0.0;  // two chains per column
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i)
+      if ((mask >> i) & 1u) {
+        if (cnt & 1) s1 = fma(op.ax[j][i], ph[i], s1);
+        else s0 = fma(op.ax[j][i], ph[i], s0);
+        ++cnt;
+      }
+    gx[j] = s0 + s1;
+  }
+#pragma unroll
+  for (int j = 0; j < RT::nuc; ++j) {
+    const unsigned mask = ucol_mask(RT::uc(j));
+    double m0 = 0.0, m1 = 0.0, p0 = 0.0, p1 = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < kNX; ++i)
+      if ((mask >> i) & 1u) {
+        if (cnt & 1) {
+          m1 = fma(op.bm[j][i], ph[i], m1);
+          p1 = fma(op.bp[j][i], ph[i], p1);
+        } else {
+          m0 = fma(op.bm[j][i], ph[i], m0);
+          p0 = fma(op.bp[j][i], ph[i], p0);
+        }
+        ++cnt;
+      }
+    gm[j] = m0 + m1;
+    gp[j] = p0 + p1;
+  }
+}
+
+/// Partial row sums of role R's columns against its own primal entries zx, zu and the next
+/// node's control entries zun (for the B+ columns).  Rows the role does not reach stay 0.
+template <int R>
+__device__ __forceinline__ void forward(const OpCols<R>& op, const double (&zx)[RoleT<R>::nxc],
+                                        const double (&zu)[RoleT<R>::nuc], const double (&zun)[RoleT<R>::nuc],
+                                        double (&acc)[kNX]) {
+  using RT = RoleT<R>;
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) acc[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < RT::nuc; ++j) {
+    const unsigned mask = ucol_mask(RT::uc(j));
+#pragma unroll
+    for (int i = 0; i < kNX; ++i)
+      if ((mask >> i) & 1u) {
+        acc[i] = fma(op.bm[j][i], zu[j], acc[i]);
+        acc[i] = fma(op.bp[j][i], zun[j], acc[i]);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j) {
+    const unsigned mask = xcol_mask(RT::xc(j));
+#pragma unroll
+    for (int i = 0; i < kNX; ++i)
+      if ((mask >> i) & 1u) acc[i] = fma(op.ax[j][i], zx[j], acc[i]);
+  }
+}
+
+/// Publishes the partial sums of the rows other roles own and keeps the own ones.
+template <int R, int S>
+__device__ __forceinline__ void publish_partials(const double (&acc)[kNX], double* part_slot, bool auth,
+                                                 double (&own)[RoleT<R>::nrow]) {
+  constexpr unsigned touch = role_touch<R>();
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) {
+    if (owns_row<R>(i)) continue;
+    if (!((touch >> i) & 1u)) continue;
+    if (auth) part_slot[(R * kNX + i) * S] = acc[i];
+  }
+#pragma unroll
+  for (int r = 0; r < RoleT<R>::nrow; ++r) own[r] = acc[RoleT<R>::row(r)];
+}
+
+/// Sum of the partial sums of row RoleT<R>::row(kRow): the own one and those of the roles that
+/// reach the row.
+template <int R, int S, int kRow>
+__device__ __forceinline__ double gather_row_t(double own, const double* part_slot) {
+  constexpr int i = RoleT<R>::row(kRow);
+  double s = own;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q == R) continue;
+    if (!((role_touch_of(q) >> i) & 1u)) continue;
+    s += part_slot[(q * kNX + i) * S];
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------------------------
+// power iteration (pipg.hpp:206-292)
+// ---------------------------------------------------------------------------------------------
+template <int R, int kHalves>
+__device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b, unsigned char* handled) {
+  using RT = RoleT<R>;
+  using Cfg = CsCfg<kHalves>;
+  constexpr int S = Cfg::S;
+  constexpr CsLayout L = cs_layout<kHalves>(false);
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp >> 2;
+  const Lane t = make_lane<kHalves>(n, half, lane);
+  for (int e = tid; e < L.total; e += Cfg::threads) sm[e] = 0.0;
+
+  OpCols<R> op;
+  const bool have = t.k < m;  // halo copies load their node's block too
+  const bool bad = load_cols<R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0) handled[b] = 0;
+    return;
+  }
+  if (tid == 0) handled[b] = 1;
+
+  double* phi_s = sm + L.phi + t.slot;    // row i at + i * S; interval k-1 at -1
+  double* th_s = sm + L.th + t.slot;
+  double* part_s = sm + L.part + t.slot;  // [role][row] at + (role * 15 + row) * S
+  double* xn_s = sm + L.xn + t.slot;      // [3] at + q * S; node k+1 at +1
+  double* red = sm + L.red;               // [2][kCsWarps] shares of the squared norm, by trip parity
+
+  // seed (pipg.hpp:213-230)
+  double zx[RT::nxc], zu[RT::nuc], vcd[RT::nrow];
+  double acc0 = 0.0;
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j) {
+    zx[j] = t.primal ? a.seed_x[((size_t)b * n + t.k) * kNX + RT::xc(j)] : 0.0;
+    acc0 = fma(zx[j], zx[j], acc0);
+  }
+#pragma unroll
+  for (int j = 0; j < RT::nuc; ++j) {
+    zu[j] = t.primal ? a.seed_u[((size_t)b * n + t.k) * kNU + RT::uc(j)] : 0.0;
+    acc0 = fma(zu[j], zu[j], acc0);
+  }
+#pragma unroll
+  for (int r = 0; r < RT::nrow; ++r) {
+    double vp = 0.0, vn = 0.0;
+    if (t.ival) {
+      vp = a.seed_vcp[((size_t)b * m + t.k) * kNX + RT::row(r)];
+      vn = a.seed_vcn[((size_t)b * m + t.k) * kNX + RT::row(r)];
+    }
+    vcd[r] = vp - vn;
+    acc0 = fma(vp, vp, acc0);
+    acc0 = fma(vn, vn, acc0);
+  }
+  acc0 = warp_sum(t.auth ? acc0 : 0.0);
+  if (lane == 0) red[warp] = acc0;
+  block_barrier();
+  auto norm_sq = [&](int parity) {
+    const double2* p = reinterpret_cast<const double2*>(red + parity * kCsWarps);
+    const double2 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
+    return ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
+  };
+  double ss = norm_sq(0);  // squared norm of the current iterate
+  if (ss == 0.0) {  // pipg.hpp:224-225
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSeedZero;
+      a.sigma[b] = 0.0;
+      if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
+    }
+    return;
+  }
+  // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test, whose
+  // tolerance is four orders of magnitude wider) and the scale 1 / sigma of pipg.hpp:243 is the
+  // same rsqrt: no square root and no division on the trip's critical path.  The value returned is
+  // the correctly rounded sqrt of the last squared norm.
+  double inv = rsqrt(ss);
+  double sigma = ss * inv;
+
+  // The forward products of trip j + 1 are issued right behind the adjoint map of trip j, in front
+  // of the barrier, so that the warp reduction of trip j's norm shares overlaps them.
+  double own[RT::nrow], xnx[RT::nrow], dy = 0.0;
+  auto forward_map = [&]() {  // pipg.hpp:234-245: partial row sums of the own columns
+    double zun[RT::nuc];
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) zun[q] = __shfl_down_sync(kFull, zu[q], 1);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {  // x_{k+1}[row] of the aligned rows
+      const int jc = aligned_col<R>(RT::row(r));
+      xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, zx[jc >= 0 ? jc : 0], 1) : 0.0;
+    }
+    if (R == 0) dy = __shfl_down_sync(kFull, zx[4], 1) - zx[4];  // e_y^T (x_{k+1} - x_k)
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      const int slot = xn_slot(RT::xc(q));
+      if (slot >= 0 && t.auth) xn_s[slot * S] = zx[q];
+    }
+    double acc[kNX];
+    forward<R>(op, zx, zu, zun, acc);
+    publish_partials<R, S>(acc, part_s, t.auth, own);
+  };
+  forward_map();
+
+  int trips = 0;
+  bool done = false;
+  for (int j = 1; j <= a.j_max; ++j) {
+    block_barrier();
+    // ---- rows: sum of the partials, scale by 1 / sigma
+    double s[RT::nrow];
+    s[0] = gather_row_t<R, S, 0>(own[0], part_s);
+    s[1] = gather_row_t<R, S, 1>(own[1], part_s);
+    s[2] = gather_row_t<R, S, 2>(own[2], part_s);
+    if (RT::nrow > 3) s[RT::nrow - 1] = gather_row_t<R, S, RT::nrow - 1>(own[RT::nrow - 1], part_s);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int i = RT::row(r);
+      const double xn = aligned_col<R>(i) >= 0 ? xnx[r] : xn_s[xn_slot(i) * S + 1];
+      s[r] = (s[r] - xn) + vcd[r];
+    }
+    if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+      ss = norm_sq((j - 1) & 1);
+      if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284
+        done = true;
+        break;
+      }
+      inv = rsqrt(ss);
+      const double sigma_star = ss * inv;
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
+      sigma = sigma_star;
+      if (hit) {
+        done = true;
+        break;
+      }
+    }
+    trips = j;
+    // rows of nodes without an interval come out as exact zeros (zero operator, zero neighbours);
+    // only real intervals are stored, the rest of the array stays cleared
+    double acc_d = 0.0;
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const double p = s[r] * inv;
+      if (t.ival) phi_s[RT::row(r) * S] = p;
+      vcd[r] = 2.0 * p;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
+      acc_d = fma(vcd[r], p, acc_d);
+    }
+    if (R == 0) {
+      if (t.ival) th_s[0] = dy * inv;
+    }
+    block_barrier();
+    // ---- adjoint map (pipg.hpp:247-275)
+    {
+      double ph[kNX];
+#pragma unroll
+      for (int i = 0; i < kNX; ++i) ph[i] = phi_s[i * S];
+      double gx[RT::nxc], gm[RT::nuc], gp[RT::nuc];
+      transposed<R>(op, ph, gx, gm, gp);
+#pragma unroll
+      for (int q = 0; q < RT::nxc; ++q) {
+        const int c = RT::xc(q);
+        double v = gx[q] - phi_s[c * S - 1];
+        if (c == kNX - 1) v += th_s[-1] - th_s[0];
+        zx[q] = v;
+      }
+#pragma unroll
+      for (int q = 0; q < RT::nuc; ++q) {
+        const double gpp = __shfl_up_sync(kFull, gp[q], 1);
+        zu[q] = gm[q] + (lane == 0 ? 0.0 : gpp);
+      }
+    }
+    double az0 = acc_d, az1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      if (q & 1) az1 = fma(zx[q], zx[q], az1);
+      else az0 = fma(zx[q], zx[q], az0);
+    }
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) az1 = fma(zu[q], zu[q], az1);
+    const double share = warp_sum(t.auth ? az0 + az1 : 0.0);
+    forward_map();  // of trip j + 1
+    if (lane == 0) red[(j & 1) * kCsWarps + warp] = share;
+  }
+  if (!done) {  // j_max trips without meeting the tolerance
+    block_barrier();
+    ss = norm_sq(a.j_max & 1);
+  }
+  if (tid == 0) {
+    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss);
+    if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
+  }
+}
+
+template <int kHalves>
+__global__ void __launch_bounds__(CsCfg<kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  switch ((threadIdx.x >> 5) & 3) {
+    case 0: power_role<0, kHalves>(a, sm, b, handled); break;
+    case 1: power_role<1, kHalves>(a, sm, b, handled); break;
+    case 2: power_role<2, kHalves>(a, sm, b, handled); break;
+    default: power_role<3, kHalves>(a, sm, b, handled); break;
+  }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// customized PIPG (pipg.hpp:350-497)
+// ---------------------------------------------------------------------------------------------
+template <int R, int kHalves>
+__device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
+  using RT = RoleT<R>;
+  using Cfg = CsCfg<kHalves>;
+  constexpr int S = Cfg::S;
+  constexpr int T = Cfg::threads;
+  constexpr CsLayout L = cs_layout<kHalves>(true);
+  constexpr SnapCs SN = snap_cs<kHalves>();
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp >> 2;
+  const Lane t = make_lane<kHalves>(n, half, lane);
+  for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
+
+  OpCols<R> op;
+  const bool have = t.k < m;  // halo copies load their node's block too
+  const bool bad = load_cols<R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0) handled[b] = 0;
+    return;
+  }
+  if (tid == 0) handled[b] = 1;
+
+  double* phi_s = sm + L.phi + t.slot;    // extrapolated dynamics dual, row i at + i * S; interval k-1 at -1
+  double* th_s = sm + L.th + t.slot;      // extrapolated relaxation dual
+  double* part_s = sm + L.part + t.slot;
+  double* xn_s = sm + L.xn + t.slot;      // reflections of x[q0], x[w2], x[y]; node k+1 at +1
+  const double* wv_s = sm + L.wv + t.slot;
+  const double* eps_s = sm + L.eps + t.slot;
+  double* bnd_s = sm + L.bnd + (R * 4) * S + t.slot;  // [u column][lo, hi] at + (2 * q + {0, 1}) * S
+  double* red = sm + L.red;
+  double* snap0 = sm + L.snap;
+  double* init_val = sm + L.fix;
+  double* final_val = init_val + 16;
+  double* init_on = final_val + 16;
+  double* final_on = init_on + 16;
+  double* ecost = sm + L.ecost;
+
+  const size_t gx = (size_t)b * n * kNX, gu = (size_t)b * n * kNU, gm_ = (size_t)b * m * kNX, gt = (size_t)b * m;
+  const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
+  if (tid < kNX) ecost[tid] = a.shape.e_cost[tid];
+  if (tid == 0) {
+    // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
+    for (int i = 0; i < a.shape.n_init_fix; ++i) {
+      init_on[a.shape.init_fix_idx[i]] = 1.0;
+      init_val[a.shape.init_fix_idx[i]] = a.sp.init_fix_val[(size_t)b * a.shape.n_init_fix + i];
+    }
+    for (int i = 0; i < a.shape.n_final_fix; ++i) {
+      final_on[a.shape.final_fix_idx[i]] = 1.0;
+      final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
+    }
+  }
+  for (int e = tid; e < NM; e += T) {  // [interval][row] -> [row][slot]
+    const int k = e / kNX, i = e - k * kNX;
+    sm[L.wv + i * S + k + 1] = a.sp.w[gm_ + e];
+  }
+  for (int e = tid; e < m; e += T) sm[L.eps + e + 1] = a.sp.eps_relax[gt + e];
+#pragma unroll
+  for (int q = 0; q < RT::nuc; ++q) {  // box of the own control entries (pipg.hpp:418-419); unbounded where there is no node
+    bnd_s[(2 * q) * S] = t.primal ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
+    bnd_s[(2 * q + 1) * S] = t.primal ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
+  }
+  // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
+  for (int e = tid; e < NXn; e += T) snap0[SN.x + e] = a.ws.x[gx + e];
+  for (int e = tid; e < NUn; e += T) snap0[SN.u + e] = a.ws.u[gu + e];
+  for (int e = tid; e < NM; e += T) {
+    snap0[SN.vp + e] = a.ws.vc_pos[gm_ + e];
+    snap0[SN.vn + e] = a.ws.vc_neg[gm_ + e];
+    snap0[SN.ph + e] = a.ws.dyn_dual[gm_ + e];
+  }
+  for (int e = tid; e < m; e += T) snap0[SN.th + e] = a.ws.relax_dual[gt + e];
+  block_barrier();
+
+  // boundary columns of this thread (pipg.hpp:408-413): bit q set when own x column q is assigned
+  int fix_bits = 0;
+  const double* fix_val = init_val;
+  const bool last_node = t.primal && t.k == n - 1;
+  if (t.primal && (t.k == 0 || t.k == n - 1)) {
+    const double* on = last_node ? final_on : init_on;
+    fix_val = last_node ? final_val : init_val;
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q)
+      if (on[RT::xc(q)] != 0.0) fix_bits |= 1 << q;
+  }
+  const bool warp_fix = __any_sync(kFull, fix_bits != 0);  // warp-uniform
+  const bool warp_last = __any_sync(kFull, last_node);
+
+  // owner-private extrapolated copies
+  double xe[RT::nxc], ue[RT::nuc], vpe[RT::nrow], vne[RT::nrow], phe[RT::nrow], the = 0.0;
+#pragma unroll
+  for (int q = 0; q < RT::nxc; ++q) xe[q] = t.primal ? snap0[SN.x + t.k * kNX + RT::xc(q)] : 0.0;
+#pragma unroll
+  for (int q = 0; q < RT::nuc; ++q) ue[q] = t.primal ? snap0[SN.u + t.k * kNU + RT::uc(q)] : 0.0;
+#pragma unroll
+  for (int r = 0; r < RT::nrow; ++r) {
+    const int e = t.k * kNX + RT::row(r);
+    vpe[r] = t.ival ? snap0[SN.vp + e] : 0.0;
+    vne[r] = t.ival ? snap0[SN.vn + e] : 0.0;
+    phe[r] = t.ival ? snap0[SN.ph + e] : 0.0;
+    if (t.auth) phi_s[RT::row(r) * S] = phe[r];
+  }
+  if (R == 0) {
+    the = t.ival ? snap0[SN.th + t.k] : 0.0;
+    if (t.auth) th_s[0] = the;
+  }
+
+  const double sigma = a.sigma[b];
+  const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
+  const double beta = a.omega * alpha;
+  // extrapolation (pipg.hpp:461-472) (1 - rho) * ex + rho * cur, evaluated as ex + rho * (cur - ex)
+  auto extrapolate = [&](double ex, double cur) { return fma(a.rho, cur - ex, ex); };
+  block_barrier();
+
+  // One iteration.  kStore additionally writes the new *_cur values of every owner into `snap`.
+  auto iteration = [&](auto store_tag, double* snap) {
+    constexpr bool kStore = decltype(store_tag)::value;
+    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
+    double rx[RT::nxc], ru[RT::nuc];
+    {
+      double ph[kNX];
+#pragma unroll
+      for (int i = 0; i < kNX; ++i) ph[i] = phi_s[i * S];
+      double gx_[RT::nxc], gm[RT::nuc], gp[RT::nuc];
+      transposed<R>(op, ph, gx_, gm, gp);
+#pragma unroll
+      for (int q = 0; q < RT::nxc; ++q) {
+        const int c = RT::xc(q);
+        const double x0 = xe[q];
+        double base = x0 * a.shape.w_prox;
+        if (warp_last) base += last_node ? a.shape.w_cost * ecost[c] : 0.0;
+        base += -phi_s[c * S - 1];
+        if (c == kNX - 1) base += th_s[-1] - th_s[0];
+        const double grad = base + gx_[q];
+        double xn = x0 + -alpha * grad;
+        if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;
+        xn = t.primal ? xn : 0.0;
+        rx[q] = fma(2.0, xn, -x0);
+        if (kStore && t.auth) snap[SN.x + t.k * kNX + c] = xn;
+        xe[q] = extrapolate(x0, xn);
+      }
+#pragma unroll
+      for (int q = 0; q < RT::nuc; ++q) {
+        double gpp = __shfl_up_sync(kFull, gp[q], 1);
+        gpp = lane == 0 ? 0.0 : gpp;
+        const double u0 = ue[q];
+        const double grad = u0 * a.shape.w_prox + (gm[q] + gpp);
+        double un = u0 + -alpha * grad;
+        const double lo = bnd_s[(2 * q) * S], hi = bnd_s[(2 * q + 1) * S];
+        // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
+        const double cl = (hi < un) ? hi : un;
+        un = (lo < cl) ? cl : lo;
+        un = t.primal ? un : 0.0;
+        ru[q] = fma(2.0, un, -u0);
+        if (kStore && t.auth) snap[SN.u + t.k * kNU + RT::uc(q)] = un;
+        ue[q] = extrapolate(u0, un);
+      }
+    }
+    // ---- forward products of the reflections: partial row sums of the own columns
+    double run[RT::nuc];
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) run[q] = __shfl_down_sync(kFull, ru[q], 1);
+    double xnx[RT::nrow];
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int jc = aligned_col<R>(RT::row(r));
+      xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, rx[jc >= 0 ? jc : 0], 1) : 0.0;
+    }
+    double drift = 0.0;
+    if (R == 0) drift = __shfl_down_sync(kFull, rx[4], 1) - rx[4];
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      const int slot = xn_slot(RT::xc(q));
+      if (slot >= 0 && t.auth) xn_s[slot * S] = rx[q];
+    }
+    double own[RT::nrow];
+    {
+      double acc[kNX];
+      forward<R>(op, rx, ru, run, acc);
+      publish_partials<R, S>(acc, part_s, t.auth, own);
+    }
+    block_barrier();
+    // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
+    //      extrapolation of the dual groups (:468-472)
+    double s[RT::nrow];
+    s[0] = gather_row_t<R, S, 0>(own[0], part_s);
+    s[1] = gather_row_t<R, S, 1>(own[1], part_s);
+    s[2] = gather_row_t<R, S, 2>(own[2], part_s);
+    if (RT::nrow > 3) s[RT::nrow - 1] = gather_row_t<R, S, RT::nrow - 1>(own[RT::nrow - 1], part_s);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int i = RT::row(r);
+      const double xn = aligned_col<R>(i) >= 0 ? xnx[r] : xn_s[xn_slot(i) * S + 1];
+      double resid = s[r] - xn;
+      const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
+      const double vp = clip0(vp0 - alpha * (a.shape.w_ep + p0));
+      const double vn = clip0(vn0 - alpha * (a.shape.w_ep - p0));
+      resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv_s[i * S];
+      const double pn = p0 + beta * resid;
+      if (kStore && t.ival) {
+        const int e = t.k * kNX + i;
+        snap[SN.vp + e] = vp;
+        snap[SN.vn + e] = vn;
+        snap[SN.ph + e] = pn;
+      }
+      const double pe = extrapolate(p0, pn);
+      phe[r] = t.ival ? pe : 0.0;
+      vpe[r] = extrapolate(vp0, vp);
+      vne[r] = extrapolate(vn0, vn);
+      if (t.auth) phi_s[i * S] = phe[r];
+    }
+    if (R == 0) {
+      const double tn = clip0(the + beta * (drift - eps_s[0]));
+      if (kStore && t.ival) snap[SN.th + t.k] = tn;
+      the = t.ival ? extrapolate(the, tn) : 0.0;
+      if (t.auth) th_s[0] = the;
+    }
+    block_barrier();
+  };
+
+  int iters = 0, cur_set = 0;  // snapshot holding the latest materialised *_cur groups
+  bool converged = false, diverged = false;
+  int to_check = a.j_check;  // iterations left until the next stopping test (counts down to 0)
+  for (int j = 1; j <= a.j_max; ++j) {
+    --to_check;
+    const bool check = to_check == 0;
+    // cur values are materialised when the next iteration checks against them, when this one
+    // checks (a converged exit returns them), and on the last iteration
+    const bool keep = to_check <= 1 || j == a.j_max;
+    if (check) to_check = a.j_check;
+    if (keep) {
+      cur_set ^= 1;
+      iteration(std::true_type{}, snap0 + cur_set * SN.total);
+    } else {
+      iteration(std::false_type{}, nullptr);
+    }
+    iters = j;
+    if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
+      const double* cur = snap0 + cur_set * SN.total;
+      const double* prev = snap0 + (cur_set ^ 1) * SN.total;
+      double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
+      double badv = 0.0;
+      auto primal = [&](int off, int count, bool finite_checked) {
+        for (int e = tid; e < count; e += T) {
+          const double c = cur[off + e], o = prev[off + e];
+          z_cur = fmax(z_cur, fabs(c));
+          z_prev = fmax(z_prev, fabs(o));
+          z_del = fmax(z_del, fabs(c - o));
+          if (finite_checked && !pt_finite(c)) badv = 1.0;
+        }
+      };
+      auto dual = [&](int off, int count, bool finite_checked) {
+        for (int e = tid; e < count; e += T) {
+          const double c = cur[off + e], o = prev[off + e];
+          r_cur = fmax(r_cur, fabs(c));
+          r_prev = fmax(r_prev, fabs(o));
+          r_del = fmax(r_del, fabs(c - o));
+          if (finite_checked && !pt_finite(c)) badv = 1.0;
+        }
+      };
+      primal(SN.x, NXn, true);
+      primal(SN.u, NUn, true);
+      primal(SN.vp, NM, false);
+      primal(SN.vn, NM, false);
+      dual(SN.ph, NM, true);
+      dual(SN.th, m, false);
+      z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
+      r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
+      badv = warp_max(badv);
+      if (lane == 0) {
+        double* rw = red + warp * 8;
+        rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
+        rw[6] = badv;
+      }
+      block_barrier();
+      double v[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        double mx = 0.0;
+#pragma unroll
+        for (int w = 0; w < Cfg::warps; ++w) mx = fmax(mx, red[w * 8 + q]);
+        v[q] = mx;
+      }
+      block_barrier();  // red and the snapshots are rewritten later
+      if (v[6] > 0.0) {
+        diverged = true;
+        break;
+      }
+      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) &&
+          v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+        converged = true;
+        break;
+      }
+    }
+  }
+
+  if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSolverDiverged;
+      if (a.fail_index) a.fail_index[b] = iters;
+      if (a.iterations) a.iterations[b] = iters;
+      if (a.converged) a.converged[b] = 0;
+      if (a.active) a.active[b] = 0;
+    }
+    return;
+  }
+  // solution = the *_cur groups, pipg.hpp:490-495 (every iteration ends with a barrier)
+  const double* cur = snap0 + cur_set * SN.total;
+  for (int e = tid; e < NXn; e += T) a.ws.x[gx + e] = cur[SN.x + e];
+  for (int e = tid; e < NUn; e += T) a.ws.u[gu + e] = cur[SN.u + e];
+  for (int e = tid; e < NM; e += T) {
+    a.ws.vc_pos[gm_ + e] = cur[SN.vp + e];
+    a.ws.vc_neg[gm_ + e] = cur[SN.vn + e];
+    a.ws.dyn_dual[gm_ + e] = cur[SN.ph + e];
+  }
+  for (int e = tid; e < m; e += T) a.ws.relax_dual[gt + e] = cur[SN.th + e];
+  if (tid == 0) {
+    if (a.iterations) a.iterations[b] = iters;
+    if (a.converged) a.converged[b] = converged ? 1 : 0;
+  }
+}
+
+template <int kHalves>
+__global__ void __launch_bounds__(CsCfg<kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  switch ((threadIdx.x >> 5) & 3) {
+    case 0: pipg_role<0, kHalves>(a, sm, b, handled); break;
+    case 1: pipg_role<1, kHalves>(a, sm, b, handled); break;
+    case 2: pipg_role<2, kHalves>(a, sm, b, handled); break;
+    default: pipg_role<3, kHalves>(a, sm, b, handled); break;
+  }
+}
+
+}  // namespace
+
+bool solver_cs_supports(const SubShape& s, bool has_a_plus) {
+  return solver_fast_supports(s, has_a_plus) && s.n <= kCsMaxNodes;
+}
+
+namespace {
+template <int kHalves>
+cudaError_t opt_in_power() {
+  return cudaFuncSetAttribute(power_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(sizeof(double) * cs_layout<kHalves>(false).total));
+}
+template <int kHalves>
+cudaError_t opt_in_pipg() {
+  return cudaFuncSetAttribute(pipg_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(sizeof(double) * cs_layout<kHalves>(true).total));
+}
+}  // namespace
+
+size_t pipg_cs_smem(const SubShape& s) {
+  return sizeof(double) * (size_t)(s.n <= CsCfg<1>::cap ? cs_layout<1>(true).total : cs_layout<2>(true).total);
+}
+
+cudaError_t configure_solver_cs(const SubShape&) {
+  cudaError_t e = opt_in_power<1>();
+  if (e == cudaSuccess) e = opt_in_power<2>();
+  if (e == cudaSuccess) e = opt_in_pipg<1>();
+  if (e == cudaSuccess) e = opt_in_pipg<2>();
+  return e;
+}
+
+cudaError_t launch_pipg_cs(const PipgArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n <= CsCfg<1>::cap) {
+    pipg_cs_kernel<1><<<a.batch, CsCfg<1>::threads, sizeof(double) * cs_layout<1>(true).total, stream>>>(a, handled);
+  } else {
+    pipg_cs_kernel<2><<<a.batch, CsCfg<2>::threads, sizeof(double) * cs_layout<2>(true).total, stream>>>(a, handled);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n <= CsCfg<1>::cap) {
+    power_cs_kernel<1><<<a.batch, CsCfg<1>::threads, sizeof(double) * cs_layout<1>(false).total, stream>>>(a, handled);
+  } else {
+    power_cs_kernel<2><<<a.batch, CsCfg<2>::threads, sizeof(double) * cs_layout<2>(false).total, stream>>>(a, handled);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ptopt_b200

@@ -374,6 +374,7 @@ power_fast_kernel(PowerArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
+  if (a.skip && a.skip[b]) return;       // solved by the column-sparse kernels (solver_cs.cu)
   const int n = a.shape.n, m = n - 1;
   const Split cut = make_split<kCluster>(n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -622,6 +623,7 @@ pipg_fast_kernel(PipgArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
+  if (a.skip && a.skip[b]) return;       // solved by the column-sparse kernels (solver_cs.cu)
   const int n = a.shape.n, m = n - 1;
   const Split cut = make_split<kCluster>(n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

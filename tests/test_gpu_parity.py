@@ -19,10 +19,13 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(1.0, np.abs(b).max())
 
 
-@pytest.fixture(scope="module", params=["fast", "generic", "split", "latency"])
+@pytest.fixture(scope="module", params=["fast", "dense", "sparse", "generic", "split", "latency"])
 def solver15(request):
     """The default-scenario handle, once per kernel family: 'fast' runs the register-resident
-    throughput kernels on rocket-shaped subproblems (five threads per node, one CTA per instance),
+    throughput kernels on rocket-shaped subproblems (the column-sparse kernels -- four role-uniform
+    warps per 32 nodes -- with the dense ones behind them for operators without the rocket model's
+    zero pattern; power iteration only), 'dense' the dense ones alone (five threads per node, one
+    CTA per instance), 'sparse' the column-sparse kernels for both solver stages,
     'generic' forces the shape-generic ones, 'split' shares every rocket-shaped instance between
     the two CTAs of a cluster, 'latency' spreads every instance over a cluster of up to eight CTAs
     with sixteen threads per node.  ('auto' picks 'latency' for batches that fit the chip in one
@@ -342,6 +345,56 @@ def test_pipg_rocket_2000_iterations(solver15, ptor):
         assert np.abs(ws[f][0] - getattr(ref, f)).max() <= TOL_ITER, f
 
 
+def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor):
+    """The column-sparse kernels check the zero pattern of every instance while they load it.  A
+    batch of three rocket subproblems whose middle one carries an entry outside the pattern (rate
+    row, position column: never produced by the model) and whose last one a NaN there: under
+    'sparse' the first instance is solved by the column-sparse kernels, the other two by the dense
+    kernels behind them -- all three as the CPU oracle solves them."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(15)
+    d, shape, sub = rocket_subproblem(sc, ptor, 1)
+    n, m = d.nodes, d.nodes - 1
+    subs = [sub]
+    for bad in (0.37, np.nan):
+        other = SubArrays(**{f: (None if getattr(sub, f) is None else getattr(sub, f).copy())
+                             for f in sub.FIELDS})
+        other.A_minus[3, 11, 2] = bad
+        subs.append(other)
+
+    def stack(items):
+        return {f: (None if getattr(items[0], f) is None else np.stack([getattr(x, f) for x in items]))
+                for f in sub.FIELDS}
+
+    sx, su = ptor.scp_seed(scenario.run_seed(sc.dispersion.seed, 1), n)
+    z = np.zeros((m, NX))
+    cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=300, j_check=10, eps_abs=1e-11,
+                         eps_rel=1e-11, eps_buff=0.05)
+    with Solver(d) as s:
+        s.set_solver_path("sparse")
+        sig, trips, status = s.power_iteration_custom(shape, stack(subs), np.stack([sx] * 3),
+                                                      np.stack([su] * 3), np.stack([z] * 3),
+                                                      np.stack([z] * 3), 1e-12, 1e-12, 0.05, 400)
+        sig_ref = []
+        for b in range(2):
+            rc, sigma, _ = ptor.power_iteration(shape, subs[b], sx, su, z, z, 1e-12, 1e-12, 0.05, 400,
+                                                with_trips=True)
+            assert rc == 0 and status[b] == 0
+            assert abs(sig[b] - sigma) <= TOL_SIGMA * sigma
+            sig_ref.append(sigma)
+        assert sig_ref[0] != sig_ref[1]
+        assert not np.isfinite(sig[2])
+        ws = {f: np.concatenate([v, v]) for f, v in ws_dict(Workspace(NX, NU, n)).items()}
+        it, conv, status, _ = s.pipg_custom(shape, stack(subs[:2]), cfg, sig_ref, ws)
+        for b in range(2):
+            ref = Workspace(NX, NU, n)
+            rc, it_ref, _, _ = ptor.pipg(shape, subs[b], cfg, sig_ref[b], ref)
+            assert rc == 0 and status[b] == 0 and it[b] == it_ref
+            for f in ref.FIELDS:
+                assert np.abs(ws[f][b] - getattr(ref, f)).max() <= TOL_ITER, (b, f)
+
+
 def check_scp_against_oracle(sc, out, b, ref, trips_ref=None):
     assert out["status"][b] == 0
     assert out["scp_iterations"][b] == ref["scp_iterations"]
@@ -383,7 +436,7 @@ def test_scp_solve_default_scenario_full_budget(solver15, ptor):
     assert abs(out["x"][0, -1, 0] - 1.416480459) < 1e-6
 
 
-@pytest.mark.parametrize("path", ["fast", "latency"])
+@pytest.mark.parametrize("path", ["fast", "dense", "latency"])
 def test_scp_solve_reduced_budget_batch(ptor, path):
     """Many dispersed instances with a reduced iteration budget (fast on the CPU oracle), one
     of them poisoned so that the per-instance failure path is exercised inside the loop."""
@@ -416,7 +469,7 @@ def test_scp_solve_reduced_budget_batch(ptor, path):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-@pytest.mark.parametrize("path", ["fast", "latency"])
+@pytest.mark.parametrize("path", ["fast", "dense", "sparse", "latency"])
 def test_scp_solve_n50_two_instances(ptor, path):
     """BASELINE config 4 shape (N=50, all defaults) on two dispersed instances."""
     from paper_2404_18034_b200.binding import Solver
@@ -429,8 +482,10 @@ def test_scp_solve_n50_two_instances(ptor, path):
         out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
                           batch["rng_seed"])
         launches = s.launch_count
-    # init + 25 x (state pass, column pass, prepare, power, PIPG, update) + the final defect pass
-    assert launches == 1 + 6 * 25 + 3
+    # init + 25 x (state pass, column pass, prepare, power, PIPG, update) + the final defect pass;
+    # 'fast' launches the column-sparse and the dense kernel of the power iteration, 'sparse' of
+    # both solver stages
+    assert launches == 1 + {"fast": 7, "sparse": 8}.get(path, 6) * 25 + 3
     spec = sc.dispersion
     wall, rec, xr, ur = ptor.run_batch(d, sc.initial_state, spec.r_low, spec.r_high, spec.seed, 2,
                                        2, 8, keep=True)
@@ -722,11 +777,13 @@ def test_config5_n100_cluster_and_generic_kernels(ptor, path):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-@pytest.mark.parametrize("nodes", [2, 3, 32, 51, 52, 64, 77, 102, 103])
+@pytest.mark.parametrize("nodes", [2, 3, 30, 31, 32, 50, 51, 52, 61, 62, 64, 77, 102, 103])
 def test_scp_solve_node_count_edges(ptor, nodes):
-    """Node counts at the edges of the register-resident kernels: the minimum grid, a count whose
-    thread groups fill the warps exactly (32), the largest single-CTA count (51), the first one
-    that is split over a two-CTA cluster (52), cluster splits with an even / odd node count and no
+    """Node counts at the edges of the register-resident kernels: the minimum grid, the last count
+    the column-sparse kernels hold in one warp per role (31) and its neighbours (30; 32: two warps
+    per role with a halo lane each), their largest count (61) and the first one that only the
+    dense kernels serve (62), the largest dense single-CTA count (51), the first one that is split
+    over a two-CTA cluster (52), cluster splits with an even / odd node count and no
     idle threads (64, 77), the largest cluster count (102) and the first one that falls back to
     the shape-generic kernels (103)."""
     from paper_2404_18034_b200.binding import Solver
@@ -735,14 +792,18 @@ def test_scp_solve_node_count_edges(ptor, nodes):
     sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 120, 150
     d = sc.problem_desc()
     batch = scenario.make_batch(sc, [0, 11])
-    with Solver(d) as s:
-        s.set_solver_path("fast")
-        out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+    outs = []
+    for path in ["fast"] + (["sparse"] if nodes <= 62 else []):
+        with Solver(d) as s:
+            s.set_solver_path(path)
+            outs.append(s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
+                                    batch["rng_seed"]))
     for b in range(2):
         rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
                                  int(batch["rng_seed"][b]), with_trips=True)
         assert rc == 0
-        check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+        for out in outs:
+            check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
 @pytest.mark.parametrize("nodes", [4, 5, 26, 49, 50, 51])
@@ -785,7 +846,7 @@ def test_solver_divergence_inside_the_scp_loop(ptor):
         assert rc == abi.ST_SOLVER_DIVERGED, rc
         refs.append(ref["fail_index"])
     assert refs[0] != refs[1]
-    for path in ("fast", "generic", "split", "latency"):
+    for path in ("fast", "dense", "sparse", "generic", "split", "latency"):
         with Solver(d) as s:
             s.set_solver_path(path)
             out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])

@@ -46,7 +46,7 @@ namespace ptopt_b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCsWarps = 8;
+constexpr int kCsWarps = 16;  // slots of the per-warp reduction arrays (at most 14 warps)
 
 // ---- structure of the operator ------------------------------------------------------------------
 /// Rows (bit i = row i) a column of A- can reach.  State order: m | r0..2 | v0..2 | q0..3 | w0..2 | y.
@@ -61,72 +61,82 @@ __host__ __device__ constexpr unsigned xcol_mask(int c) {
 /// Rows a column of B- / B+ can reach.  Control order: T0..2 | tau0..2 | s.
 __host__ __device__ constexpr unsigned ucol_mask(int c) { return (c >= 3 && c <= 5) ? 0x7ffeu : 0x7fffu; }
 
-template <int R>
+// The partition of the 29 columns (K = 4 roles: 8 warps, 255 registers, 78..80 operator entries per
+// thread).  Partitions with more roles were measured and dropped: six roles
+// (12 warps at 168 registers, 48..58 entries) are slower -- 49 % more warp instructions and twice the
+// shared-memory wavefronts, because every role reads all fifteen duals and publishes its own
+// partial sums; seven roles (14 warps) get 128 registers and spill.  A dual row is "aligned" when
+// its owner also owns the primal entry of the same index: x_{k+1}[row] then arrives by a lane shift.
+template <int K, int R>
 struct RoleT;
 template <>
-struct RoleT<0> {
+struct RoleT<4, 0> {
   static constexpr int nxc = 5, nuc = 2, nrow = 3;
   __host__ __device__ static constexpr int xc(int j) { return j == 0 ? 7 : j == 4 ? 14 : j; }  // q0 r0 r1 r2 y
   __host__ __device__ static constexpr int uc(int j) { return j; }                                // T0 T1
   __host__ __device__ static constexpr int row(int r) { return 1 + r; }                           // r0 r1 r2
 };
 template <>
-struct RoleT<1> {
+struct RoleT<4, 1> {
   static constexpr int nxc = 3, nuc = 2, nrow = 4;
   __host__ __device__ static constexpr int xc(int j) { return j == 0 ? 8 : j == 1 ? 0 : 6; }     // q1 m v2
   __host__ __device__ static constexpr int uc(int j) { return 2 + j; }                            // T2 tau0
   __host__ __device__ static constexpr int row(int r) { return r == 0 ? 8 : r == 1 ? 0 : r == 2 ? 6 : 7; }
 };
 template <>
-struct RoleT<2> {
+struct RoleT<4, 2> {
   static constexpr int nxc = 2, nuc = 2, nrow = 4;
   __host__ __device__ static constexpr int xc(int j) { return 9 + j; }                            // q2 q3
   __host__ __device__ static constexpr int uc(int j) { return 4 + j; }                            // tau1 tau2
   __host__ __device__ static constexpr int row(int r) { return r == 0 ? 9 : r == 1 ? 10 : r == 2 ? 13 : 14; }
 };
 template <>
-struct RoleT<3> {
+struct RoleT<4, 3> {
   static constexpr int nxc = 5, nuc = 1, nrow = 4;
   __host__ __device__ static constexpr int xc(int j) { return j < 3 ? 11 + j : 1 + j; }          // w0 w1 w2 v0 v1
   __host__ __device__ static constexpr int uc(int) { return 6; }                                  // s
   __host__ __device__ static constexpr int row(int r) { return r < 2 ? 11 + r : 2 + r; }          // w0 w1 v0 v1
 };
-
 /// Rows the columns of role R reach (union of its column masks).
-template <int R>
+template <int K, int R>
 __host__ __device__ constexpr unsigned role_touch() {
   unsigned m = 0;
-  for (int j = 0; j < RoleT<R>::nxc; ++j) m |= xcol_mask(RoleT<R>::xc(j));
-  for (int j = 0; j < RoleT<R>::nuc; ++j) m |= ucol_mask(RoleT<R>::uc(j));
+  for (int j = 0; j < RoleT<K, R>::nxc; ++j) m |= xcol_mask(RoleT<K, R>::xc(j));
+  for (int j = 0; j < RoleT<K, R>::nuc; ++j) m |= ucol_mask(RoleT<K, R>::uc(j));
   return m;
 }
+template <int K>
 __host__ __device__ constexpr unsigned role_touch_of(int r) {
-  return r == 0 ? role_touch<0>() : r == 1 ? role_touch<1>() : r == 2 ? role_touch<2>() : role_touch<3>();
+  static_assert(K == 4, "one partition");
+  return r == 0 ? role_touch<4, 0>() : r == 1 ? role_touch<4, 1>() : r == 2 ? role_touch<4, 2>() : role_touch<4, 3>();
 }
 /// Index of the x column of role R that equals row i (the row is "aligned": its owner also owns
 /// the primal entry of the same index, so x_{k+1}[i] arrives by a lane shift), or -1.
-template <int R>
+template <int K, int R>
 __host__ __device__ constexpr int aligned_col(int i) {
-  for (int j = 0; j < RoleT<R>::nxc; ++j)
-    if (RoleT<R>::xc(j) == i) return j;
+  for (int j = 0; j < RoleT<K, R>::nxc; ++j)
+    if (RoleT<K, R>::xc(j) == i) return j;
   return -1;
 }
 /// True when role R owns dual row i.
-template <int R>
+template <int K, int R>
 __host__ __device__ constexpr bool owns_row(int i) {
-  for (int r = 0; r < RoleT<R>::nrow; ++r)
-    if (RoleT<R>::row(r) == i) return true;
+  for (int r = 0; r < RoleT<K, R>::nrow; ++r)
+    if (RoleT<K, R>::row(r) == i) return true;
   return false;
 }
 // primal entries whose reflections a row owner of ANOTHER role needs from node k+1 go through
 // shared memory: x[q0] (7, role 0 -> role 1), x[w2] (13, role 3 -> role 2), x[y] (14, role 0 -> role 2)
-__host__ __device__ constexpr int xn_slot(int c) { return c == 7 ? 0 : c == 13 ? 1 : c == 14 ? 2 : -1; }
+template <int K>
+__host__ __device__ constexpr int xn_slot(int c) {
+  return c == 7 ? 0 : c == 13 ? 1 : c == 14 ? 2 : -1;
+}
 
 // ---- shared-memory layout --------------------------------------------------------------------------
 // [row][slot] arrays, slot = node + 1 (slot 0: the zero "node -1" / "interval -1" in front).
-template <int kHalves>
+template <int K, int kHalves>
 struct CsCfg {
-  static constexpr int warps = 4 * kHalves;
+  static constexpr int warps = K * kHalves;
   static constexpr int threads = 32 * warps;
   // nodes: the last lane never holds a node (the lane shift that fetches node k + 1 must find zeros
   // behind the last node), and two halves share two halo lanes
@@ -137,9 +147,9 @@ struct CsCfg {
 struct SnapCs {
   int x, u, vp, vn, ph, th, total;
 };
-template <int kHalves>
+template <int K, int kHalves>
 __host__ __device__ constexpr SnapCs snap_cs() {
-  constexpr int n = CsCfg<kHalves>::cap;
+  constexpr int n = CsCfg<K, kHalves>::cap;
   SnapCs s{};
   int o = 0;
   s.x = o; o += n * kNX;
@@ -156,23 +166,23 @@ struct CsLayout {
   int phi, th, part, xn, red, total;
   int wv, eps, bnd, fix, ecost, snap;  // PIPG only
 };
-template <int kHalves>
+template <int K, int kHalves>
 __host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
-  constexpr int S = CsCfg<kHalves>::S;
+  constexpr int S = CsCfg<K, kHalves>::S;
   CsLayout L{};
   int o = 0;
   L.phi = o; o += kNX * S;
   L.th = o; o += S;
-  L.part = o; o += 4 * kNX * S;
+  L.part = o; o += K * kNX * S;
   L.xn = o; o += 3 * S;
-  L.red = o; o += 8 * kCsWarps;
+  L.red = o; o += 8 * kCsWarps;  // power: [2][kCsWarps]; PIPG: [warps][8]
   if (pipg) {
     L.wv = o; o += kNX * S;
     L.eps = o; o += S;
-    L.bnd = o; o += 4 * 2 * 2 * S;   // [role][u column][lo, hi][slot]
+    L.bnd = o; o += K * 2 * 2 * S;   // [role][u column][lo, hi][slot]
     L.fix = o; o += 4 * 16;          // init_val, final_val, init_on, final_on
     L.ecost = o; o += 16;
-    L.snap = o; o += 2 * snap_cs<kHalves>().total;
+    L.snap = o; o += 2 * snap_cs<K, kHalves>().total;
   }
   L.total = o;
   return L;
@@ -218,18 +228,18 @@ __device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
 }
 
 /// The operator columns of role R of one interval, and whether the block has the expected zeros.
-template <int R>
+template <int K, int R>
 struct OpCols {
-  double ax[RoleT<R>::nxc][kNX];
-  double bm[RoleT<R>::nuc][kNX];
-  double bp[RoleT<R>::nuc][kNX];
+  double ax[RoleT<K, R>::nxc][kNX];
+  double bm[RoleT<K, R>::nuc][kNX];
+  double bp[RoleT<K, R>::nuc][kNX];
 };
 
 /// Loads the columns of role R of interval `iv` (zero when !have).  Returns true when an entry
 /// outside the structural pattern is not an exact zero.
-template <int R>
-__device__ __forceinline__ bool load_cols(const SubArrays& sp, size_t iv, bool have, OpCols<R>& op) {
-  using RT = RoleT<R>;
+template <int K, int R>
+__device__ __forceinline__ bool load_cols(const SubArrays& sp, size_t iv, bool have, OpCols<K, R>& op) {
+  using RT = RoleT<K, R>;
   bool bad = false;
   const double* A = sp.A_minus + iv * kNX * kNX;
   const double* Bm = sp.B_minus + iv * kNX * kNU;
@@ -264,124 +274,123 @@ __device__ __forceinline__ bool load_cols(const SubArrays& sp, size_t iv, bool h
   return bad;
 }
 
-/// Transposed products of role R against the fifteen duals of its interval: column sums of its x
-/// columns, of its B- columns and of its B+ columns.
-template <int R>
-__device__ __forceinline__ void transposed(const OpCols<R>& op, const double (&ph)[kNX],
-                                           double (&gx)[RoleT<R>::nxc], double (&gm)[RoleT<R>::nuc],
-                                           double (&gp)[RoleT<R>::nuc]) {
-  using RT = RoleT<R>;
+/// Transposed products of role R against the duals of its interval (read from shared memory row
+/// by row: one dual is live at a time, the column sums are the only accumulators): column sums of
+/// its x columns, of its B- columns and of its B+ columns.
+template <int K, int R, int S>
+__device__ __forceinline__ void transposed(const OpCols<K, R>& op, const double* phi_slot,
+                                           double (&gx)[RoleT<K, R>::nxc], double (&gm)[RoleT<K, R>::nuc],
+                                           double (&gp)[RoleT<K, R>::nuc]) {
+  using RT = RoleT<K, R>;
+  constexpr unsigned touch = role_touch<K, R>();
 #pragma unroll
-  for (int j = 0; j < RT::nxc; ++j) {
-    const unsigned mask = xcol_mask(RT::xc(j));
-    double s0 = 0.0, s1 = 0.0;  // two chains per column
-    int cnt = 0;
+  for (int j = 0; j < RT::nxc; ++j) gx[j] = 0.0;
 #pragma unroll
-    for (int i = 0; i < kNX; ++i)
-      if ((mask >> i) & 1u) {
-        if (cnt & 1) s1 = fma(op.ax[j][i], ph[i], s1);
-        else s0 = fma(op.ax[j][i], ph[i], s0);
-        ++cnt;
-      }
-    gx[j] = s0 + s1;
-  }
-#pragma unroll
-  for (int j = 0; j < RT::nuc; ++j) {
-    const unsigned mask = ucol_mask(RT::uc(j));
-    double m0 = 0.0, m1 = 0.0, p0 = 0.0, p1 = 0.0;
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < kNX; ++i)
-      if ((mask >> i) & 1u) {
-        if (cnt & 1) {
-          m1 = fma(op.bm[j][i], ph[i], m1);
-          p1 = fma(op.bp[j][i], ph[i], p1);
-        } else {
-          m0 = fma(op.bm[j][i], ph[i], m0);
-          p0 = fma(op.bp[j][i], ph[i], p0);
-        }
-        ++cnt;
-      }
-    gm[j] = m0 + m1;
-    gp[j] = p0 + p1;
-  }
-}
-
-/// Partial row sums of role R's columns against its own primal entries zx, zu and the next
-/// node's control entries zun (for the B+ columns).  Rows the role does not reach stay 0.
-template <int R>
-__device__ __forceinline__ void forward(const OpCols<R>& op, const double (&zx)[RoleT<R>::nxc],
-                                        const double (&zu)[RoleT<R>::nuc], const double (&zun)[RoleT<R>::nuc],
-                                        double (&acc)[kNX]) {
-  using RT = RoleT<R>;
-#pragma unroll
-  for (int i = 0; i < kNX; ++i) acc[i] = 0.0;
-#pragma unroll
-  for (int j = 0; j < RT::nuc; ++j) {
-    const unsigned mask = ucol_mask(RT::uc(j));
-#pragma unroll
-    for (int i = 0; i < kNX; ++i)
-      if ((mask >> i) & 1u) {
-        acc[i] = fma(op.bm[j][i], zu[j], acc[i]);
-        acc[i] = fma(op.bp[j][i], zun[j], acc[i]);
-      }
-  }
-#pragma unroll
-  for (int j = 0; j < RT::nxc; ++j) {
-    const unsigned mask = xcol_mask(RT::xc(j));
-#pragma unroll
-    for (int i = 0; i < kNX; ++i)
-      if ((mask >> i) & 1u) acc[i] = fma(op.ax[j][i], zx[j], acc[i]);
-  }
-}
-
-/// Publishes the partial sums of the rows other roles own and keeps the own ones.
-template <int R, int S>
-__device__ __forceinline__ void publish_partials(const double (&acc)[kNX], double* part_slot, bool auth,
-                                                 double (&own)[RoleT<R>::nrow]) {
-  constexpr unsigned touch = role_touch<R>();
+  for (int j = 0; j < RT::nuc; ++j) gm[j] = gp[j] = 0.0;
 #pragma unroll
   for (int i = 0; i < kNX; ++i) {
-    if (owns_row<R>(i)) continue;
     if (!((touch >> i) & 1u)) continue;
-    if (auth) part_slot[(R * kNX + i) * S] = acc[i];
-  }
+    const double p = phi_slot[i * S];
 #pragma unroll
-  for (int r = 0; r < RoleT<R>::nrow; ++r) own[r] = acc[RoleT<R>::row(r)];
+    for (int j = 0; j < RT::nuc; ++j)
+      if ((ucol_mask(RT::uc(j)) >> i) & 1u) {
+        gm[j] = fma(op.bm[j][i], p, gm[j]);
+        gp[j] = fma(op.bp[j][i], p, gp[j]);
+      }
+#pragma unroll
+    for (int j = 0; j < RT::nxc; ++j)
+      if ((xcol_mask(RT::xc(j)) >> i) & 1u) gx[j] = fma(op.ax[j][i], p, gx[j]);
+  }
 }
 
-/// Sum of the partial sums of row RoleT<R>::row(kRow): the own one and those of the roles that
-/// reach the row.
-template <int R, int S, int kRow>
-__device__ __forceinline__ double gather_row_t(double own, const double* part_slot) {
-  constexpr int i = RoleT<R>::row(kRow);
-  double s = own;
+/// Partial sum of row i of role R's columns against its own primal entries zx, zu and the next
+/// node's control entries zun (for the B+ columns).
+template <int K, int R>
+__device__ __forceinline__ double forward_row(const OpCols<K, R>& op, const double (&zx)[RoleT<K, R>::nxc],
+                                              const double (&zu)[RoleT<K, R>::nuc],
+                                              const double (&zun)[RoleT<K, R>::nuc], int i) {
+  using RT = RoleT<K, R>;
+  double a0 = 0.0, a1 = 0.0;  // two chains per row
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q == R) continue;
-    if (!((role_touch_of(q) >> i) & 1u)) continue;
-    s += part_slot[(q * kNX + i) * S];
+  for (int j = 0; j < RT::nuc; ++j)
+    if ((ucol_mask(RT::uc(j)) >> i) & 1u) {
+      a0 = fma(op.bm[j][i], zu[j], a0);
+      a1 = fma(op.bp[j][i], zun[j], a1);
+    }
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j)
+    if ((xcol_mask(RT::xc(j)) >> i) & 1u) {
+      if (j & 1) a1 = fma(op.ax[j][i], zx[j], a1);
+      else a0 = fma(op.ax[j][i], zx[j], a0);
+    }
+  return a0 + a1;
+}
+
+/// Forward products of role R row by row: the partial sums of the rows other roles own are
+/// published at once, the own ones kept.
+template <int K, int R, int S>
+__device__ __forceinline__ void forward_publish(const OpCols<K, R>& op, const double (&zx)[RoleT<K, R>::nxc],
+                                                const double (&zu)[RoleT<K, R>::nuc],
+                                                const double (&zun)[RoleT<K, R>::nuc], double* part_slot,
+                                                bool auth, double (&own)[RoleT<K, R>::nrow]) {
+  constexpr unsigned touch = role_touch<K, R>();
+#pragma unroll
+  for (int i = 0; i < kNX; ++i) {
+    if (owns_row<K, R>(i)) continue;
+    if (!((touch >> i) & 1u)) continue;
+    const double v = forward_row<K, R>(op, zx, zu, zun, i);
+    if (auth) part_slot[(R * kNX + i) * S] = v;
   }
-  return s;
+#pragma unroll
+  for (int r = 0; r < RoleT<K, R>::nrow; ++r) own[r] = forward_row<K, R>(op, zx, zu, zun, RoleT<K, R>::row(r));
+}
+
+/// Sum of the partial sums of row RoleT<K, R>::row(kRow): the own one and those of the roles that
+/// reach the row.
+template <int K, int R, int S, int kRow>
+__device__ __forceinline__ double gather_row_t(double own, const double* part_slot) {
+  constexpr int i = RoleT<K, R>::row(kRow);
+  double s0 = own, s1 = 0.0;  // two short chains instead of one
+  int cnt = 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    if (q == R) continue;
+    if (!((role_touch_of<K>(q) >> i) & 1u)) continue;
+    if (cnt & 1) s0 += part_slot[(q * kNX + i) * S];
+    else s1 += part_slot[(q * kNX + i) * S];
+    ++cnt;
+  }
+  return s0 + s1;
+}
+
+template <int K, int R, int S>
+__device__ __forceinline__ void gather_rows(const double (&own)[RoleT<K, R>::nrow], const double* part_slot,
+                                            double (&s)[RoleT<K, R>::nrow]) {
+  constexpr int nrow = RoleT<K, R>::nrow;
+  s[0] = gather_row_t<K, R, S, 0>(own[0], part_slot);
+  if constexpr (nrow > 1) s[1] = gather_row_t<K, R, S, 1>(own[1], part_slot);
+  if constexpr (nrow > 2) s[2] = gather_row_t<K, R, S, 2>(own[2], part_slot);
+  if constexpr (nrow > 3) s[3] = gather_row_t<K, R, S, 3>(own[3], part_slot);
+  static_assert(nrow <= 4, "rows per role");
 }
 
 // ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
-template <int R, int kHalves>
+template <int K, int R, int kHalves>
 __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b, unsigned char* handled) {
-  using RT = RoleT<R>;
-  using Cfg = CsCfg<kHalves>;
+  using RT = RoleT<K, R>;
+  using Cfg = CsCfg<K, kHalves>;
   constexpr int S = Cfg::S;
-  constexpr CsLayout L = cs_layout<kHalves>(false);
+  constexpr CsLayout L = cs_layout<K, kHalves>(false);
   const int n = a.shape.n, m = n - 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
   const Lane t = make_lane<kHalves>(n, half, lane);
   for (int e = tid; e < L.total; e += Cfg::threads) sm[e] = 0.0;
 
-  OpCols<R> op;
+  OpCols<K, R> op;
   const bool have = t.k < m;  // halo copies load their node's block too
-  const bool bad = load_cols<R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
   if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
     if (tid == 0) handled[b] = 0;
     return;
@@ -424,7 +433,10 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   auto norm_sq = [&](int parity) {
     const double2* p = reinterpret_cast<const double2*>(red + parity * kCsWarps);
     const double2 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
-    return ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
+    const double lo = ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
+    if (Cfg::warps <= 8) return lo;
+    const double2 q4 = p[4], q5 = p[5], q6 = p[6], q7 = p[7];
+    return lo + (((q4.x + q4.y) + (q5.x + q5.y)) + ((q6.x + q6.y) + (q7.x + q7.y)));
   };
   double ss = norm_sq(0);  // squared norm of the current iterate
   if (ss == 0.0) {  // pipg.hpp:224-225
@@ -444,6 +456,7 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
 
   // The forward products of trip j + 1 are issued right behind the adjoint map of trip j, in front
   // of the barrier, so that the warp reduction of trip j's norm shares overlaps them.
+  constexpr int kJy = aligned_col<K, R>(kNX - 1);  // the role that owns x[y] also owns the relaxation dual
   double own[RT::nrow], xnx[RT::nrow], dy = 0.0;
   auto forward_map = [&]() {  // pipg.hpp:234-245: partial row sums of the own columns
     double zun[RT::nuc];
@@ -451,18 +464,16 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
     for (int q = 0; q < RT::nuc; ++q) zun[q] = __shfl_down_sync(kFull, zu[q], 1);
 #pragma unroll
     for (int r = 0; r < RT::nrow; ++r) {  // x_{k+1}[row] of the aligned rows
-      const int jc = aligned_col<R>(RT::row(r));
+      const int jc = aligned_col<K, R>(RT::row(r));
       xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, zx[jc >= 0 ? jc : 0], 1) : 0.0;
     }
-    if (R == 0) dy = __shfl_down_sync(kFull, zx[4], 1) - zx[4];  // e_y^T (x_{k+1} - x_k)
+    if (kJy >= 0) dy = __shfl_down_sync(kFull, zx[kJy >= 0 ? kJy : 0], 1) - zx[kJy >= 0 ? kJy : 0];  // e_y^T (x_{k+1} - x_k)
 #pragma unroll
     for (int q = 0; q < RT::nxc; ++q) {
-      const int slot = xn_slot(RT::xc(q));
+      const int slot = xn_slot<K>(RT::xc(q));
       if (slot >= 0 && t.auth) xn_s[slot * S] = zx[q];
     }
-    double acc[kNX];
-    forward<R>(op, zx, zu, zun, acc);
-    publish_partials<R, S>(acc, part_s, t.auth, own);
+    forward_publish<K, R, S>(op, zx, zu, zun, part_s, t.auth, own);
   };
   forward_map();
 
@@ -472,14 +483,11 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
     block_barrier();
     // ---- rows: sum of the partials, scale by 1 / sigma
     double s[RT::nrow];
-    s[0] = gather_row_t<R, S, 0>(own[0], part_s);
-    s[1] = gather_row_t<R, S, 1>(own[1], part_s);
-    s[2] = gather_row_t<R, S, 2>(own[2], part_s);
-    if (RT::nrow > 3) s[RT::nrow - 1] = gather_row_t<R, S, RT::nrow - 1>(own[RT::nrow - 1], part_s);
+    gather_rows<K, R, S>(own, part_s, s);
 #pragma unroll
     for (int r = 0; r < RT::nrow; ++r) {
       const int i = RT::row(r);
-      const double xn = aligned_col<R>(i) >= 0 ? xnx[r] : xn_s[xn_slot(i) * S + 1];
+      const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
       s[r] = (s[r] - xn) + vcd[r];
     }
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
@@ -508,17 +516,14 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
       vcd[r] = 2.0 * p;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
       acc_d = fma(vcd[r], p, acc_d);
     }
-    if (R == 0) {
+    if (kJy >= 0) {
       if (t.ival) th_s[0] = dy * inv;
     }
     block_barrier();
     // ---- adjoint map (pipg.hpp:247-275)
     {
-      double ph[kNX];
-#pragma unroll
-      for (int i = 0; i < kNX; ++i) ph[i] = phi_s[i * S];
       double gx[RT::nxc], gm[RT::nuc], gp[RT::nuc];
-      transposed<R>(op, ph, gx, gm, gp);
+      transposed<K, R, S>(op, phi_s, gx, gm, gp);
 #pragma unroll
       for (int q = 0; q < RT::nxc; ++q) {
         const int c = RT::xc(q);
@@ -554,39 +559,38 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   }
 }
 
-template <int kHalves>
-__global__ void __launch_bounds__(CsCfg<kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
+template <int K, int kHalves>
+__global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
   if (a.active && !a.active[b]) return;
-  switch ((threadIdx.x >> 5) & 3) {
-    case 0: power_role<0, kHalves>(a, sm, b, handled); break;
-    case 1: power_role<1, kHalves>(a, sm, b, handled); break;
-    case 2: power_role<2, kHalves>(a, sm, b, handled); break;
-    default: power_role<3, kHalves>(a, sm, b, handled); break;
+  switch ((threadIdx.x >> 5) % K) {
+    case 0: power_role<4, 0, kHalves>(a, sm, b, handled); break;
+    case 1: power_role<4, 1, kHalves>(a, sm, b, handled); break;
+    case 2: power_role<4, 2, kHalves>(a, sm, b, handled); break;
+    default: power_role<4, 3, kHalves>(a, sm, b, handled); break;
   }
 }
-
 
 // ---------------------------------------------------------------------------------------------
 // customized PIPG (pipg.hpp:350-497)
 // ---------------------------------------------------------------------------------------------
-template <int R, int kHalves>
+template <int K, int R, int kHalves>
 __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
-  using RT = RoleT<R>;
-  using Cfg = CsCfg<kHalves>;
+  using RT = RoleT<K, R>;
+  using Cfg = CsCfg<K, kHalves>;
   constexpr int S = Cfg::S;
   constexpr int T = Cfg::threads;
-  constexpr CsLayout L = cs_layout<kHalves>(true);
-  constexpr SnapCs SN = snap_cs<kHalves>();
+  constexpr CsLayout L = cs_layout<K, kHalves>(true);
+  constexpr SnapCs SN = snap_cs<K, kHalves>();
   const int n = a.shape.n, m = n - 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
   const Lane t = make_lane<kHalves>(n, half, lane);
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
 
-  OpCols<R> op;
+  OpCols<K, R> op;
   const bool have = t.k < m;  // halo copies load their node's block too
-  const bool bad = load_cols<R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
   if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
     if (tid == 0) handled[b] = 0;
     return;
@@ -689,11 +693,8 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
     double rx[RT::nxc], ru[RT::nuc];
     {
-      double ph[kNX];
-#pragma unroll
-      for (int i = 0; i < kNX; ++i) ph[i] = phi_s[i * S];
       double gx_[RT::nxc], gm[RT::nuc], gp[RT::nuc];
-      transposed<R>(op, ph, gx_, gm, gp);
+      transposed<K, R, S>(op, phi_s, gx_, gm, gp);
 #pragma unroll
       for (int q = 0; q < RT::nxc; ++q) {
         const int c = RT::xc(q);
@@ -734,34 +735,27 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     double xnx[RT::nrow];
 #pragma unroll
     for (int r = 0; r < RT::nrow; ++r) {
-      const int jc = aligned_col<R>(RT::row(r));
+      const int jc = aligned_col<K, R>(RT::row(r));
       xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, rx[jc >= 0 ? jc : 0], 1) : 0.0;
     }
     double drift = 0.0;
-    if (R == 0) drift = __shfl_down_sync(kFull, rx[4], 1) - rx[4];
+    if (R == 0) drift = __shfl_down_sync(kFull, rx[4], 1) - rx[4];  // K = 4: role 0 owns x[y]
 #pragma unroll
     for (int q = 0; q < RT::nxc; ++q) {
-      const int slot = xn_slot(RT::xc(q));
+      const int slot = xn_slot<K>(RT::xc(q));
       if (slot >= 0 && t.auth) xn_s[slot * S] = rx[q];
     }
     double own[RT::nrow];
-    {
-      double acc[kNX];
-      forward<R>(op, rx, ru, run, acc);
-      publish_partials<R, S>(acc, part_s, t.auth, own);
-    }
+    forward_publish<K, R, S>(op, rx, ru, run, part_s, t.auth, own);
     block_barrier();
     // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
     //      extrapolation of the dual groups (:468-472)
     double s[RT::nrow];
-    s[0] = gather_row_t<R, S, 0>(own[0], part_s);
-    s[1] = gather_row_t<R, S, 1>(own[1], part_s);
-    s[2] = gather_row_t<R, S, 2>(own[2], part_s);
-    if (RT::nrow > 3) s[RT::nrow - 1] = gather_row_t<R, S, RT::nrow - 1>(own[RT::nrow - 1], part_s);
+    gather_rows<K, R, S>(own, part_s, s);
 #pragma unroll
     for (int r = 0; r < RT::nrow; ++r) {
       const int i = RT::row(r);
-      const double xn = aligned_col<R>(i) >= 0 ? xnx[r] : xn_s[xn_slot(i) * S + 1];
+      const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
       double resid = s[r] - xn;
       const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
       const double vp = clip0(vp0 - alpha * (a.shape.w_ep + p0));
@@ -892,15 +886,15 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
 }
 
 template <int kHalves>
-__global__ void __launch_bounds__(CsCfg<kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
+__global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
   if (a.active && !a.active[b]) return;
   switch ((threadIdx.x >> 5) & 3) {
-    case 0: pipg_role<0, kHalves>(a, sm, b, handled); break;
-    case 1: pipg_role<1, kHalves>(a, sm, b, handled); break;
-    case 2: pipg_role<2, kHalves>(a, sm, b, handled); break;
-    default: pipg_role<3, kHalves>(a, sm, b, handled); break;
+    case 0: pipg_role<4, 0, kHalves>(a, sm, b, handled); break;
+    case 1: pipg_role<4, 1, kHalves>(a, sm, b, handled); break;
+    case 2: pipg_role<4, 2, kHalves>(a, sm, b, handled); break;
+    default: pipg_role<4, 3, kHalves>(a, sm, b, handled); break;
   }
 }
 
@@ -911,44 +905,45 @@ bool solver_cs_supports(const SubShape& s, bool has_a_plus) {
 }
 
 namespace {
-template <int kHalves>
+template <int K, int kHalves>
 cudaError_t opt_in_power() {
-  return cudaFuncSetAttribute(power_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(double) * cs_layout<kHalves>(false).total));
+  return cudaFuncSetAttribute(power_cs_kernel<K, kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(sizeof(double) * cs_layout<K, kHalves>(false).total));
 }
 template <int kHalves>
 cudaError_t opt_in_pipg() {
   return cudaFuncSetAttribute(pipg_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(double) * cs_layout<kHalves>(true).total));
+                              (int)(sizeof(double) * cs_layout<4, kHalves>(true).total));
+}
+template <int K, int kHalves>
+void launch_power(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+  power_cs_kernel<K, kHalves><<<a.batch, CsCfg<K, kHalves>::threads, sizeof(double) * cs_layout<K, kHalves>(false).total, stream>>>(a, handled);
 }
 }  // namespace
 
 size_t pipg_cs_smem(const SubShape& s) {
-  return sizeof(double) * (size_t)(s.n <= CsCfg<1>::cap ? cs_layout<1>(true).total : cs_layout<2>(true).total);
+  return sizeof(double) * (size_t)(s.n <= CsCfg<4, 1>::cap ? cs_layout<4, 1>(true).total : cs_layout<4, 2>(true).total);
 }
 
 cudaError_t configure_solver_cs(const SubShape&) {
-  cudaError_t e = opt_in_power<1>();
-  if (e == cudaSuccess) e = opt_in_power<2>();
+  cudaError_t e = opt_in_power<4, 1>();
+  if (e == cudaSuccess) e = opt_in_power<4, 2>();
   if (e == cudaSuccess) e = opt_in_pipg<1>();
   if (e == cudaSuccess) e = opt_in_pipg<2>();
   return e;
 }
 
-cudaError_t launch_pipg_cs(const PipgArgs& a, unsigned char* handled, cudaStream_t stream) {
-  if (a.shape.n <= CsCfg<1>::cap) {
-    pipg_cs_kernel<1><<<a.batch, CsCfg<1>::threads, sizeof(double) * cs_layout<1>(true).total, stream>>>(a, handled);
-  } else {
-    pipg_cs_kernel<2><<<a.batch, CsCfg<2>::threads, sizeof(double) * cs_layout<2>(true).total, stream>>>(a, handled);
-  }
+cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n <= CsCfg<4, 1>::cap) launch_power<4, 1>(a, handled, stream);
+  else launch_power<4, 2>(a, handled, stream);
   return cudaGetLastError();
 }
 
-cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
-  if (a.shape.n <= CsCfg<1>::cap) {
-    power_cs_kernel<1><<<a.batch, CsCfg<1>::threads, sizeof(double) * cs_layout<1>(false).total, stream>>>(a, handled);
+cudaError_t launch_pipg_cs(const PipgArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n <= CsCfg<4, 1>::cap) {
+    pipg_cs_kernel<1><<<a.batch, CsCfg<4, 1>::threads, sizeof(double) * cs_layout<4, 1>(true).total, stream>>>(a, handled);
   } else {
-    power_cs_kernel<2><<<a.batch, CsCfg<2>::threads, sizeof(double) * cs_layout<2>(false).total, stream>>>(a, handled);
+    pipg_cs_kernel<2><<<a.batch, CsCfg<4, 2>::threads, sizeof(double) * cs_layout<4, 2>(true).total, stream>>>(a, handled);
   }
   return cudaGetLastError();
 }

@@ -189,7 +189,6 @@ __host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
 }
 
 __device__ __forceinline__ void block_barrier() { asm volatile("bar.sync 0;" ::: "memory"); }
-__device__ __forceinline__ double clip0(double v) { return 0.0 < v ? v : 0.0; }
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -575,6 +574,61 @@ __global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel
 // ---------------------------------------------------------------------------------------------
 // customized PIPG (pipg.hpp:350-497)
 // ---------------------------------------------------------------------------------------------
+/// stopping_custom(cur, prev) and the divergence test of pipg.hpp:475-487 over two snapshots: 0 =
+/// go on, 1 = converged, 2 = a non-finite primal or dual entry.  One copy for the four roles (the
+/// loop bodies are role-specific and have to share the instruction cache with as little as possible).
+template <int kHalves>
+__device__ __noinline__ int pipg_check(const double* cur, const double* prev, int n, double* red, double eps_abs,
+                                       double eps_rel) {
+  constexpr SnapCs SN = snap_cs<4, kHalves>();
+  constexpr int T = CsCfg<4, kHalves>::threads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = n - 1;
+  double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, badv = 0.0;
+  auto scan = [&](int off, int count, bool dual, bool finite_checked) {
+#pragma unroll 1
+    for (int e = tid; e < count; e += T) {
+      const double c = cur[off + e], o = prev[off + e];
+      if (dual) {
+        r_cur = fmax(r_cur, fabs(c));
+        r_prev = fmax(r_prev, fabs(o));
+        r_del = fmax(r_del, fabs(c - o));
+      } else {
+        z_cur = fmax(z_cur, fabs(c));
+        z_prev = fmax(z_prev, fabs(o));
+        z_del = fmax(z_del, fabs(c - o));
+      }
+      if (finite_checked && !pt_finite(c)) badv = 1.0;
+    }
+  };
+  scan(SN.x, n * kNX, false, true);
+  scan(SN.u, n * kNU, false, true);
+  scan(SN.vp, m * kNX, false, false);
+  scan(SN.vn, m * kNX, false, false);
+  scan(SN.ph, m * kNX, true, true);
+  scan(SN.th, m, true, false);
+  z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
+  r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
+  badv = warp_max(badv);
+  if (lane == 0) {
+    double* rw = red + warp * 8;
+    rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
+    rw[6] = badv;
+  }
+  block_barrier();
+  double v[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double mx = 0.0;
+#pragma unroll
+    for (int w = 0; w < CsCfg<4, kHalves>::warps; ++w) mx = fmax(mx, red[w * 8 + q]);
+    v[q] = mx;
+  }
+  block_barrier();  // red and the snapshots are rewritten later
+  if (v[6] > 0.0) return 2;
+  return (v[2] <= eps_abs + eps_rel * fmax(v[0], v[1]) && v[5] <= eps_abs + eps_rel * fmax(v[3], v[4])) ? 1 : 0;
+}
+
 template <int K, int R, int kHalves>
 __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
   using RT = RoleT<K, R>;
@@ -706,7 +760,6 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         const double grad = base + gx_[q];
         double xn = x0 + -alpha * grad;
         if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;
-        xn = t.primal ? xn : 0.0;
         rx[q] = fma(2.0, xn, -x0);
         if (kStore && t.auth) snap[SN.x + t.k * kNX + c] = xn;
         xe[q] = extrapolate(x0, xn);
@@ -720,9 +773,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         double un = u0 + -alpha * grad;
         const double lo = bnd_s[(2 * q) * S], hi = bnd_s[(2 * q + 1) * S];
         // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
-        const double cl = (hi < un) ? hi : un;
-        un = (lo < cl) ? cl : lo;
-        un = t.primal ? un : 0.0;
+        un = clamp_box(lo, hi, un);
         ru[q] = fma(2.0, un, -u0);
         if (kStore && t.auth) snap[SN.u + t.k * kNU + RT::uc(q)] = un;
         ue[q] = extrapolate(u0, un);
@@ -768,17 +819,18 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         snap[SN.vn + e] = vn;
         snap[SN.ph + e] = pn;
       }
-      const double pe = extrapolate(p0, pn);
-      phe[r] = t.ival ? pe : 0.0;
+      // rows of nodes without an interval (zero operator, zero neighbours, zero right-hand side,
+      // w_ep >= 0) stay exact zeros; only real intervals are stored
+      phe[r] = extrapolate(p0, pn);
       vpe[r] = extrapolate(vp0, vp);
       vne[r] = extrapolate(vn0, vn);
-      if (t.auth) phi_s[i * S] = phe[r];
+      if (t.ival) phi_s[i * S] = phe[r];
     }
     if (R == 0) {
       const double tn = clip0(the + beta * (drift - eps_s[0]));
       if (kStore && t.ival) snap[SN.th + t.k] = tn;
-      the = t.ival ? extrapolate(the, tn) : 0.0;
-      if (t.auth) th_s[0] = the;
+      the = extrapolate(the, tn);
+      if (t.ival) th_s[0] = the;
     }
     block_barrier();
   };
@@ -801,58 +853,13 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     }
     iters = j;
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
-      const double* cur = snap0 + cur_set * SN.total;
-      const double* prev = snap0 + (cur_set ^ 1) * SN.total;
-      double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0;
-      double badv = 0.0;
-      auto primal = [&](int off, int count, bool finite_checked) {
-        for (int e = tid; e < count; e += T) {
-          const double c = cur[off + e], o = prev[off + e];
-          z_cur = fmax(z_cur, fabs(c));
-          z_prev = fmax(z_prev, fabs(o));
-          z_del = fmax(z_del, fabs(c - o));
-          if (finite_checked && !pt_finite(c)) badv = 1.0;
-        }
-      };
-      auto dual = [&](int off, int count, bool finite_checked) {
-        for (int e = tid; e < count; e += T) {
-          const double c = cur[off + e], o = prev[off + e];
-          r_cur = fmax(r_cur, fabs(c));
-          r_prev = fmax(r_prev, fabs(o));
-          r_del = fmax(r_del, fabs(c - o));
-          if (finite_checked && !pt_finite(c)) badv = 1.0;
-        }
-      };
-      primal(SN.x, NXn, true);
-      primal(SN.u, NUn, true);
-      primal(SN.vp, NM, false);
-      primal(SN.vn, NM, false);
-      dual(SN.ph, NM, true);
-      dual(SN.th, m, false);
-      z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
-      r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
-      badv = warp_max(badv);
-      if (lane == 0) {
-        double* rw = red + warp * 8;
-        rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
-        rw[6] = badv;
-      }
-      block_barrier();
-      double v[7];
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        double mx = 0.0;
-#pragma unroll
-        for (int w = 0; w < Cfg::warps; ++w) mx = fmax(mx, red[w * 8 + q]);
-        v[q] = mx;
-      }
-      block_barrier();  // red and the snapshots are rewritten later
-      if (v[6] > 0.0) {
+      const int verdict = pipg_check<kHalves>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total, n, red,
+                                              a.eps_abs, a.eps_rel);
+      if (verdict == 2) {
         diverged = true;
         break;
       }
-      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) &&
-          v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+      if (verdict == 1) {
         converged = true;
         break;
       }

@@ -63,10 +63,6 @@ __host__ __device__ constexpr int pos_col(int j) {
   return j < kNX ? j : (j < kNX + kNU ? pos_bm(j - kNX) : pos_bp(j - kNX - kNU));
 }
 
-/// std::max(0.0, v) as the reference evaluates it (pipg.hpp:423-430: `(0.0 < v) ? v : 0.0`, so a
-/// NaN becomes 0): one compare and a select instead of fmax()'s NaN-propagating sequence.
-__device__ __forceinline__ double clip0(double v) { return 0.0 < v ? v : 0.0; }
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -821,8 +817,7 @@ pipg_fast_kernel(PipgArgs a) {
       const double grad = u0 * a.shape.w_prox + su[q];
       double un = u0 + -alpha * grad;
       // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
-      const double cl = (hi[q] < un) ? hi[q] : un;
-      un = (lo[q] < cl) ? cl : lo[q];
+      un = clamp_box(lo[q], hi[q], un);
       const double urf = fma(2.0, un, -u0);
       ur_k[ju] = urf;
       if (push_next && (q == 0 || g < 2))

@@ -46,9 +46,6 @@ constexpr int kLatWarpsMax = kLatThreadsMax / 32;
 constexpr int kSlots = kLatMaxLocalNodes + 3;  // node slots -1 .. kLatMaxLocalNodes + 1
 constexpr int kXP = 16, kUP = 8;               // node pitch of the x / u arrays (entry 15 / 7 is a zero pad)
 
-/// std::max(0.0, v) as the reference evaluates it (pipg.hpp:423-430).
-__device__ __forceinline__ double clip0(double v) { return 0.0 < v ? v : 0.0; }
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -632,8 +629,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
         if (e == 0) base += extra;
         const double grad = base + cs[e];
         double xn = x0 + -alpha * grad;
-        const double cl = (hi[e] < xn) ? hi[e] : xn;  // std::max(lo, std::min(hi, v))
-        xn = (lo[e] < cl) ? cl : lo[e];
+        xn = clamp_box(lo[e], hi[e], xn);  // std::max(lo, std::min(hi, v))
         rf[e] = fma(2.0, xn, -x0);
         cur_p[e] = xn;
         pe[e] = fma(rho, xn - x0, x0);  // extrapolation, pipg.hpp:461-472

@@ -555,7 +555,7 @@ def run_own_arm(args):
         traffic = None
         kernel_of = {"linearize": "column_pass_kernel",
                      "power_iteration": "power_cs_kernel" if n <= 61 else "power_fast_kernel",
-                     "pipg": "pipg_fast_kernel"}
+                     "pipg": "pipg_cs_kernel" if n <= 61 else "pipg_fast_kernel"}
         tpath = ROOT / "profiles" / "ncu_traffic.json"
         if tpath.exists() and n in (50, 100):
             tj = json.loads(tpath.read_text())
@@ -570,16 +570,16 @@ def run_own_arm(args):
         value = world * B * args.steps / (ms_total * 1e-3)
         # Shared-memory view of the two solver kernels (one CTA = one instance = one SM): clocks per
         # trip / iteration from the stage time at the sampled SM clock, against the shared-memory
-        # wavefronts one trip / iteration issues (ncu source counters of the hot loops: the
-        # column-sparse power kernel 376 per pass of its four role bodies x 2 warps per role,
-        # profiles/r02_cs_power_loop_stalls.txt; the dense PIPG kernel 250.1 per warp-pass x 8 warps,
-        # profiles/r01_s5_pipg_loop_stalls.txt; one wavefront per clock and SM, tools/probes/smem_width.cu)
+        # wavefronts one trip / iteration issues (ncu source counters of the hot loops of the
+        # column-sparse kernels: 376 / 446 per pass of the four role bodies x 2 warps per role,
+        # profiles/r02_cs_power_loop_stalls.txt and r02_cs_pipg_loop_stalls.txt; one wavefront per
+        # clock and SM, tools/probes/smem_width.cu)
         smem_view = None
         clk_info = clocks.summary()
         if n == 50 and args.solver_path == "auto" and clk_info.get("sm_mhz"):
             sms = min(torch.cuda.get_device_properties(dev).multi_processor_count, B)
             units = {"power_iteration": sum_trips, "pipg": pipg_iters}
-            wavefronts = {"power_iteration": 376.0 * 2, "pipg": 250.1 * 8}
+            wavefronts = {"power_iteration": 376.0 * 2, "pipg": 446.0 * 2}
             smem_view = {}
             for k in units:
                 clk = stages[k] * 1e-3 * clk_info["sm_mhz"] * 1e6 * sms / units[k]  # stage times: last launch
@@ -713,7 +713,7 @@ def main():
     ap.add_argument("--batch", type=int, default=4096, help="instances per GPU")
     ap.add_argument("--nodes", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--solver-path", choices=("auto", "generic", "split", "latency", "fast", "dense", "sparse"), default="auto",
+    ap.add_argument("--solver-path", choices=("auto", "generic", "split", "latency", "fast", "dense"), default="auto",
                     help="kernel family for power iteration / PIPG (ptopt_cuda_set_solver_path)")
     ap.add_argument("--cpu-instances", type=int, default=0,
                     help="instances in the CPU sample (default: one per host core)")

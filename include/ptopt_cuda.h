@@ -221,23 +221,19 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h);
  *              up to eight CTAs, sixteen threads per node (a short dependent instruction
  *              stream per thread); up to 128 nodes.  Lowest single-solve latency, lower
  *              throughput per SM.
- *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size.  Up to 62 nodes
- *              the power iteration runs on the column-sparse kernel first (four role-uniform warps
- *              per 32 nodes, the structural zeros of the rocket model's state-transition blocks
- *              skipped at compile time); it verifies the zero pattern of every instance while
- *              loading it and leaves instances without it to the dense kernel (FAST_DENSE), which
- *              runs right behind.  PIPG runs on the dense kernel.
+ *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size.  Up to 61 nodes
+ *              the column-sparse kernels run first (four role-uniform warps per 32 nodes, the
+ *              structural zeros of the rocket model's state-transition blocks skipped at compile
+ *              time); they verify the zero pattern of every instance while loading it and leave
+ *              instances without it to the dense kernels (FAST_DENSE), which run right behind.
  *   FAST_DENSE the dense register-resident kernels alone: five threads per node, one CTA per
- *              instance up to 51 nodes, a 2-CTA cluster up to 102; any operator values.
- *   FAST_SPARSE as FAST_THROUGHPUT, with the column-sparse kernel for PIPG too (experimental:
- *              its four role-specific loop bodies overflow the instruction cache). */
+ *              instance up to 51 nodes, a 2-CTA cluster up to 102; any operator values. */
 #define PTOPT_SOLVER_AUTO 0
 #define PTOPT_SOLVER_GENERIC 1
 #define PTOPT_SOLVER_FAST_SPLIT 2
 #define PTOPT_SOLVER_FAST_LATENCY 3
 #define PTOPT_SOLVER_FAST_THROUGHPUT 4
 #define PTOPT_SOLVER_FAST_DENSE 5
-#define PTOPT_SOLVER_FAST_SPARSE 6
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path);
 /* Blocks until all work enqueued on the handle's stream has finished. */
 int ptopt_cuda_synchronize(ptopt_cuda_handle* h);

@@ -138,9 +138,8 @@ class Solver:
         throughput kernels; generic kernels for non-rocket shapes), 'generic', 'split'
         (PTOPT_SOLVER_FAST_SPLIT), 'latency' (PTOPT_SOLVER_FAST_LATENCY) or 'fast'
         (PTOPT_SOLVER_FAST_THROUGHPUT: column-sparse kernels with the dense ones behind them) or
-        'dense' (PTOPT_SOLVER_FAST_DENSE: the dense register-resident kernels alone), 'sparse'
-        (PTOPT_SOLVER_FAST_SPARSE: column-sparse kernels for the power iteration and for PIPG)."""
-        code = {"auto": 0, "generic": 1, "split": 2, "latency": 3, "fast": 4, "dense": 5, "sparse": 6}[path]
+        'dense' (PTOPT_SOLVER_FAST_DENSE: the dense register-resident kernels alone)."""
+        code = {"auto": 0, "generic": 1, "split": 2, "latency": 3, "fast": 4, "dense": 5}[path]
         _check(self.lib.ptopt_cuda_set_solver_path(self._h, C.c_int(code)))
         self.solver_path = path
 

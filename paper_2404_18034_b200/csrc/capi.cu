@@ -246,17 +246,8 @@ bool use_fast_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_p
 /// the zero pattern of the rocket model's discretization and mark it handled; the dense kernels
 /// then run on the rest (normally nothing: their CTAs leave at once).
 bool use_cs_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
-  return (h->solver_path == PTOPT_SOLVER_AUTO || h->solver_path == PTOPT_SOLVER_FAST_THROUGHPUT ||
-          h->solver_path == PTOPT_SOLVER_FAST_SPARSE) &&
+  return (h->solver_path == PTOPT_SOLVER_AUTO || h->solver_path == PTOPT_SOLVER_FAST_THROUGHPUT) &&
          solver_cs_supports(s, has_a_plus);
-}
-
-/// The PIPG stage takes the column-sparse kernel only under FAST_SPARSE: its four role-specific
-/// loop bodies (31 KB of SASS) do not fit the SM's 32 KB instruction cache next to the rest of the
-/// kernel, and it measures slower than the dense kernel (ncu: half of its warp-state samples are
-/// instruction-fetch stalls); the power iteration's bodies (21 KB) fit and win.
-bool use_cs_pipg(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
-  return h->solver_path == PTOPT_SOLVER_FAST_SPARSE && solver_cs_supports(s, has_a_plus);
 }
 
 /// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
@@ -321,7 +312,7 @@ int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  if (fast && use_cs_pipg(h, a.shape, a.sp.A_plus != nullptr)) {
+  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr)) {
     unsigned char* handled = nullptr;
     PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
     PT_CUDA(launch_pipg_cs(a, handled, h->stream));
@@ -505,7 +496,6 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
   const int lat = latency_ranks(h, h->rocket_shape, false, batch);
   const bool cs = !lat && fast && use_cs_solver(h, h->rocket_shape, false);
-  const bool cs_pipg = cs && use_cs_pipg(h, h->rocket_shape, false);
   unsigned char* handled = h->buf[S_HANDLED].as<unsigned char>();
   PowerArgs pa_rest = pa;
   PipgArgs ga_rest = ga;
@@ -528,7 +518,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
                      : launch_power_generic(pa, h->stream));
     }
     PT_CUDA(mark(2));
-    if (cs_pipg) {
+    if (cs) {
       PT_CUDA(launch_pipg_cs(ga, handled, h->stream));
       PT_CUDA(launch_pipg_fast(ga_rest, false, h->stream));
       kernels += 1;
@@ -736,7 +726,7 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h) {
 
 int ptopt_cuda_set_solver_path(ptopt_cuda_handle* h, int path) {
   if (!h) return fail(PTOPT_ERR_INVALID_ARGUMENT, "null handle");
-  if (path < PTOPT_SOLVER_AUTO || path > PTOPT_SOLVER_FAST_SPARSE)
+  if (path < PTOPT_SOLVER_AUTO || path > PTOPT_SOLVER_FAST_DENSE)
     return fail(PTOPT_ERR_INVALID_ARGUMENT, "unknown solver path");
   if (path != h->solver_path && h->scp_graph) {  // the captured graph names the other kernels
     DeviceGuard guard(h->device);

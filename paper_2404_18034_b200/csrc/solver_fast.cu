@@ -771,8 +771,8 @@ pipg_fast_kernel(PipgArgs a) {
     // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry.  The
     //      terms that do not need the partial sums are gathered first so that the dependent
     //      chain behind the shared-memory loads stays short.
-    double base[kR], fv[kR], sx[kR];
-    double su[2], lo[2], hi[2];
+    double base[kR], sx[kR];
+    double su[2];
     // the sums over the thread's own interval first: in a cluster they hide part of the flight
     // time of the partner's boundary values, which only the previous-interval terms below need
 #pragma unroll
@@ -781,16 +781,10 @@ pipg_fast_kernel(PipgArgs a) {
     for (int q = 0; q < 2; ++q) su[q] = column_sum(part_k, q == 0 ? 15 + 3 * g : 16 + 3 * g);
     if constexpr (kCluster) bx.recv_prev(iter_no - 1);  // rank 0's last interval after iteration iter_no - 1 (0: warm start)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const double2 bq = q == 0 ? *bnd0 : *bnd1;
-      lo[q] = bq.x;
-      hi[q] = bq.y;
-      su[q] += column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
-    }
+    for (int q = 0; q < 2; ++q) su[q] += column_sum(part_k - kG * kPS, q == 0 ? 17 + 3 * g : 22 + 3 * g);
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       const int i = kR * g + r;
-      fv[r] = warp_fix ? fix_val[i] : 0.0;
       double t = xe[r] * a.shape.w_prox;
       if (last_node) t += a.shape.w_cost * ecost[i];
       t += -phx_k[r - kNX];
@@ -803,7 +797,7 @@ pipg_fast_kernel(PipgArgs a) {
       const double x0 = xe[r];
       const double grad = base[r] + sx[r];
       double xn = x0 + -alpha * grad;
-      xn = (fix_bits & (1 << r)) ? fv[r] : xn;
+      if (warp_fix) xn = (fix_bits & (1 << r)) ? fix_val[i] : xn;
       const double xrf = fma(2.0, xn, -x0);
       xr_k[i] = xrf;
       if (push_next) push_f64(partner_u32(sm + L.xs + cut.half * kXS + i, 0), xrf, bx.box(kBoxNext));
@@ -816,8 +810,8 @@ pipg_fast_kernel(PipgArgs a) {
       const double u0 = ue[q];
       const double grad = u0 * a.shape.w_prox + su[q];
       double un = u0 + -alpha * grad;
-      // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
-      un = clamp_box(lo[q], hi[q], un);
+      const double2 bq = q == 0 ? *bnd0 : *bnd1;
+      un = clamp_box(bq.x, bq.y, un);  // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
       const double urf = fma(2.0, un, -u0);
       ur_k[ju] = urf;
       if (push_next && (q == 0 || g < 2))

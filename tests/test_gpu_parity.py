@@ -19,13 +19,12 @@ def rel_err(a, b):
     return np.abs(a - b).max() / max(1.0, np.abs(b).max())
 
 
-@pytest.fixture(scope="module", params=["fast", "dense", "sparse", "generic", "split", "latency"])
+@pytest.fixture(scope="module", params=["fast", "dense", "generic", "split", "latency"])
 def solver15(request):
     """The default-scenario handle, once per kernel family: 'fast' runs the register-resident
     throughput kernels on rocket-shaped subproblems (the column-sparse kernels -- four role-uniform
     warps per 32 nodes -- with the dense ones behind them for operators without the rocket model's
-    zero pattern; power iteration only), 'dense' the dense ones alone (five threads per node, one
-    CTA per instance), 'sparse' the column-sparse kernels for both solver stages,
+    zero pattern), 'dense' the dense ones alone (five threads per node, one CTA per instance),
     'generic' forces the shape-generic ones, 'split' shares every rocket-shaped instance between
     the two CTAs of a cluster, 'latency' spreads every instance over a cluster of up to eight CTAs
     with sixteen threads per node.  ('auto' picks 'latency' for batches that fit the chip in one
@@ -349,7 +348,7 @@ def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor):
     """The column-sparse kernels check the zero pattern of every instance while they load it.  A
     batch of three rocket subproblems whose middle one carries an entry outside the pattern (rate
     row, position column: never produced by the model) and whose last one a NaN there: under
-    'sparse' the first instance is solved by the column-sparse kernels, the other two by the dense
+    'fast' the first instance is solved by the column-sparse kernels, the other two by the dense
     kernels behind them -- all three as the CPU oracle solves them."""
     from paper_2404_18034_b200.binding import Solver
 
@@ -372,7 +371,7 @@ def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor):
     cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=300, j_check=10, eps_abs=1e-11,
                          eps_rel=1e-11, eps_buff=0.05)
     with Solver(d) as s:
-        s.set_solver_path("sparse")
+        s.set_solver_path("fast")
         sig, trips, status = s.power_iteration_custom(shape, stack(subs), np.stack([sx] * 3),
                                                       np.stack([su] * 3), np.stack([z] * 3),
                                                       np.stack([z] * 3), 1e-12, 1e-12, 0.05, 400)
@@ -469,7 +468,7 @@ def test_scp_solve_reduced_budget_batch(ptor, path):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-@pytest.mark.parametrize("path", ["fast", "dense", "sparse", "latency"])
+@pytest.mark.parametrize("path", ["fast", "dense", "latency"])
 def test_scp_solve_n50_two_instances(ptor, path):
     """BASELINE config 4 shape (N=50, all defaults) on two dispersed instances."""
     from paper_2404_18034_b200.binding import Solver
@@ -483,9 +482,8 @@ def test_scp_solve_n50_two_instances(ptor, path):
                           batch["rng_seed"])
         launches = s.launch_count
     # init + 25 x (state pass, column pass, prepare, power, PIPG, update) + the final defect pass;
-    # 'fast' launches the column-sparse and the dense kernel of the power iteration, 'sparse' of
-    # both solver stages
-    assert launches == 1 + {"fast": 7, "sparse": 8}.get(path, 6) * 25 + 3
+    # 'fast' launches the column-sparse and the dense kernel of both solver stages
+    assert launches == 1 + (8 if path == "fast" else 6) * 25 + 3
     spec = sc.dispersion
     wall, rec, xr, ur = ptor.run_batch(d, sc.initial_state, spec.r_low, spec.r_high, spec.seed, 2,
                                        2, 8, keep=True)
@@ -792,12 +790,9 @@ def test_scp_solve_node_count_edges(ptor, nodes):
     sc.max_iters, sc.pipg_j_max, sc.power_j_max = 2, 120, 150
     d = sc.problem_desc()
     batch = scenario.make_batch(sc, [0, 11])
-    outs = []
-    for path in ["fast"] + (["sparse"] if nodes <= 62 else []):
-        with Solver(d) as s:
-            s.set_solver_path(path)
-            outs.append(s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"],
-                                    batch["rng_seed"]))
+    with Solver(d) as s:
+        s.set_solver_path("fast")
+        outs = [s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])]
     for b in range(2):
         rc, ref = ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
                                  int(batch["rng_seed"][b]), with_trips=True)
@@ -846,7 +841,7 @@ def test_solver_divergence_inside_the_scp_loop(ptor):
         assert rc == abi.ST_SOLVER_DIVERGED, rc
         refs.append(ref["fail_index"])
     assert refs[0] != refs[1]
-    for path in ("fast", "dense", "sparse", "generic", "split", "latency"):
+    for path in ("fast", "dense", "generic", "split", "latency"):
         with Solver(d) as s:
             s.set_solver_path(path)
             out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])

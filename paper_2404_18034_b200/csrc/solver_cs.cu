@@ -181,7 +181,7 @@ __host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
     L.eps = o; o += S;
     L.bnd = o; o += K * 2 * 2 * S;   // [role][u column][lo, hi][slot]
     L.fix = o; o += 4 * 16;          // init_val, final_val, init_on, final_on
-    L.ecost = o; o += 16;
+    L.ecost = o; o += kNX * S;        // w_cost * e_cost at the last node's slot, zero elsewhere: [row][slot]
     L.snap = o; o += 2 * snap_cs<K, kHalves>().total;
   }
   L.total = o;
@@ -204,6 +204,7 @@ __device__ __forceinline__ double warp_max(double v) {
 struct Lane {
   int k;        // node
   int slot;     // k + 1
+  bool halo;    // a redundant copy of a node another warp owns
   bool auth;    // this thread is THE owner of node k (k < n, not a halo copy)
   bool primal;  // its primal entries are valid (owner, or the halo copy of node 31 in the first warp)
   bool ival;    // auth and k is an interval (k < n - 1)
@@ -213,12 +214,13 @@ __device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
   Lane t;
   if (kHalves == 1) {
     t.k = lane;
+    t.halo = false;
     t.auth = t.k < n;
     t.primal = t.auth;
   } else {
     t.k = half == 0 ? lane : 30 + lane;
-    const bool halo = half == 0 ? lane == 31 : lane == 0;
-    t.auth = !halo && t.k < n;
+    t.halo = half == 0 ? lane == 31 : lane == 0;
+    t.auth = !t.halo && t.k < n;
     t.primal = t.k < n && (half == 0 || lane != 0);
   }
   t.slot = t.k + 1;
@@ -699,11 +701,11 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   double* final_val = init_val + 16;
   double* init_on = final_val + 16;
   double* final_on = init_on + 16;
-  double* ecost = sm + L.ecost;
+  const double* cost_s = sm + L.ecost + t.slot;  // the terminal-cost term of this node's entries (pipg.hpp:404)
 
   const size_t gx = (size_t)b * n * kNX, gu = (size_t)b * n * kNU, gm_ = (size_t)b * m * kNX, gt = (size_t)b * m;
   const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
-  if (tid < kNX) ecost[tid] = a.shape.e_cost[tid];
+  if (tid < kNX) sm[L.ecost + tid * S + n] = a.shape.w_cost * a.shape.e_cost[tid];  // slot of node n - 1
   if (tid == 0) {
     // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
     for (int i = 0; i < a.shape.n_init_fix; ++i) {
@@ -722,8 +724,9 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   for (int e = tid; e < m; e += T) sm[L.eps + e + 1] = a.sp.eps_relax[gt + e];
 #pragma unroll
   for (int q = 0; q < RT::nuc; ++q) {  // box of the own control entries (pipg.hpp:418-419); unbounded where there is no node
-    bnd_s[(2 * q) * S] = t.primal ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
-    bnd_s[(2 * q + 1) * S] = t.primal ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
+    if (t.halo) continue;  // the owner's warp fills the slot; the halo copy reads it behind the barrier
+    bnd_s[(2 * q) * S] = t.auth ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
+    bnd_s[(2 * q + 1) * S] = t.auth ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
   }
   // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
   for (int e = tid; e < NXn; e += T) snap0[SN.x + e] = a.ws.x[gx + e];
@@ -748,7 +751,6 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
       if (on[RT::xc(q)] != 0.0) fix_bits |= 1 << q;
   }
   const bool warp_fix = __any_sync(kFull, fix_bits != 0);  // warp-uniform
-  const bool warp_last = __any_sync(kFull, last_node);
 
   // owner-private extrapolated copies
   double xe[RT::nxc], ue[RT::nuc], vpe[RT::nrow], vne[RT::nrow], phe[RT::nrow], the = 0.0;
@@ -789,7 +791,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         const int c = RT::xc(q);
         const double x0 = xe[q];
         double base = x0 * a.shape.w_prox;
-        if (warp_last) base += last_node ? a.shape.w_cost * ecost[c] : 0.0;
+        base += cost_s[c * S];  // zero but at the last node: no branch, no predicated address arithmetic
         base += -phi_s[c * S - 1];
         if (c == kNX - 1) base += th_s[-1] - th_s[0];
         const double grad = base + gx_[q];

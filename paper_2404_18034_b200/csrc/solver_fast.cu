@@ -482,10 +482,12 @@ power_fast_kernel(PowerArgs a) {
     if constexpr (kCluster) cg::this_cluster().sync();  // the partner may still be reading
     return;
   }
-  // sigma and 1 / sigma (pipg.hpp:243 scales by 1.0 / sigma) from the same squared norm: rsqrt
-  // runs beside sqrt instead of a division chain behind it (1 ulp)
-  double inv = rsqrt(sigma);
-  sigma = sqrt(sigma);
+  // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test) and
+  // the scale 1 / sigma of pipg.hpp:243 the same rsqrt: no square root and no division on the
+  // trip's critical path.  The value returned is the correctly rounded sqrt of the last squared norm.
+  double ss_last = sigma;
+  double inv = rsqrt(ss_last);
+  sigma = ss_last * inv;
 
   // The norm of trip j-1 is reduced while trip j's forward products are already running: the
   // products do not need sigma until they are scaled, so the block reduction, the square root
@@ -512,13 +514,13 @@ power_fast_kernel(PowerArgs a) {
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
       if constexpr (kCluster) bx.recv_norm(j - 1);
       const double ss = norm_sq((j - 1) & 1);
-      const double sigma_star = sqrt(ss);
-      inv = rsqrt(ss);
-      if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
-        sigma = 0.0;
+      ss_last = ss;
+      if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         done = true;
         break;
       }
+      inv = rsqrt(ss);
+      const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
       sigma = sigma_star;
       if (hit) {
@@ -601,10 +603,10 @@ power_fast_kernel(PowerArgs a) {
         bx.recv_norm(a.j_max);
       }
     }
-    sigma = sqrt(norm_sq(a.j_max & 1));
+    ss_last = norm_sq(a.j_max & 1);
   }
   if (tid == 0 && cut.rank == 0) {
-    a.sigma[b] = (1.0 + a.eps_buff) * sigma;
+    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss_last);
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
   }
   if constexpr (kCluster) cg::this_cluster().sync();  // the partner may still be reading

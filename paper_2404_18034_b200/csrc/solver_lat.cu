@@ -438,8 +438,12 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     cg::this_cluster().sync();
     return;
   }
-  double inv = rsqrt(sigma);
-  sigma = sqrt(sigma);
+  // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test) and
+  // the scale 1 / sigma the same rsqrt: no square root on the trip's critical path.  The value
+  // returned is the correctly rounded sqrt of the last squared norm.
+  double ss_last = sigma;
+  double inv = rsqrt(ss_last);
+  sigma = ss_last * inv;
   // row lanes scale (forward row - x_{k+1}[row]) + vcd; the relaxation-dual lane x_{k+1}[14] - x_k[14]
   const double live = (t.row_alive || (t.theta_lane && t.ival)) ? 1.0 : 0.0;
 
@@ -453,13 +457,13 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     const double s = t.theta_lane ? xn1 - xc : (r - xn1) + vcd;
     if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
       const double ss = norm_sq(j - 1);
-      const double sigma_star = sqrt(ss);
-      inv = rsqrt(ss);
-      if (sigma_star == 0.0) {  // iterate in the null space, pipg.hpp:280-284
-        sigma = 0.0;
+      ss_last = ss;
+      if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284
         done = true;
         break;
       }
+      inv = rsqrt(ss);
+      const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
       sigma = sigma_star;
       if (hit) {
@@ -492,11 +496,11 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     if constexpr (!kLone) send_total(j);
   }
   if (!done) {  // j_max trips without meeting the tolerance
-    sigma = a.j_max >= 1 ? sqrt(norm_sq(a.j_max)) : sigma;
+    if (a.j_max >= 1) ss_last = norm_sq(a.j_max);
     if (a.j_max >= 1) recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);  // still on its way
   }
   if (t.tid == 0 && cut.rank == 0) {
-    a.sigma[b] = (1.0 + a.eps_buff) * sigma;
+    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss_last);
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
   }
   cg::this_cluster().sync();  // nobody leaves while a neighbour may still write into it

@@ -194,11 +194,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
 
 /// Which node a lane holds and in what capacity.
 struct Lane {
@@ -534,7 +529,7 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
       }
       inv = rsqrt(ss);
       const double sigma_star = ss * inv;
-      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;
       if (hit) {
         done = true;
@@ -627,13 +622,13 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
     for (int e = tid; e < count; e += T) {
       const double c = cur[off + e], o = prev[off + e];
       if (dual) {
-        r_cur = fmax(r_cur, fabs(c));
-        r_prev = fmax(r_prev, fabs(o));
-        r_del = fmax(r_del, fabs(c - o));
+        r_cur = max_nn(r_cur, fabs(c));
+        r_prev = max_nn(r_prev, fabs(o));
+        r_del = max_nn(r_del, fabs(c - o));
       } else {
-        z_cur = fmax(z_cur, fabs(c));
-        z_prev = fmax(z_prev, fabs(o));
-        z_del = fmax(z_del, fabs(c - o));
+        z_cur = max_nn(z_cur, fabs(c));
+        z_prev = max_nn(z_prev, fabs(o));
+        z_del = max_nn(z_del, fabs(c - o));
       }
       if (finite_checked && !pt_finite(c)) badv = 1.0;
     }
@@ -644,9 +639,9 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
   scan(SN.vn, m * kNX, false, false);
   scan(SN.ph, m * kNX, true, true);
   scan(SN.th, m, true, false);
-  z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
-  r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
-  badv = warp_max(badv);
+  z_cur = warp_max_nn(z_cur); z_prev = warp_max_nn(z_prev); z_del = warp_max_nn(z_del);
+  r_cur = warp_max_nn(r_cur); r_prev = warp_max_nn(r_prev); r_del = warp_max_nn(r_del);
+  badv = warp_max_nn(badv);
   if (lane == 0) {
     double* rw = red + warp * 8;
     rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
@@ -658,12 +653,12 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
   for (int q = 0; q < 7; ++q) {
     double mx = 0.0;
 #pragma unroll
-    for (int w = 0; w < CsCfg<4, kHalves>::warps; ++w) mx = fmax(mx, red[w * 8 + q]);
+    for (int w = 0; w < CsCfg<4, kHalves>::warps; ++w) mx = max_nn(mx, red[w * 8 + q]);
     v[q] = mx;
   }
   block_barrier();  // red and the snapshots are rewritten later
   if (v[6] > 0.0) return 2;
-  return (v[2] <= eps_abs + eps_rel * fmax(v[0], v[1]) && v[5] <= eps_abs + eps_rel * fmax(v[3], v[4])) ? 1 : 0;
+  return (v[2] <= eps_abs + eps_rel * max_nn(v[0], v[1]) && v[5] <= eps_abs + eps_rel * max_nn(v[3], v[4])) ? 1 : 0;
 }
 
 template <int K, int R, int kHalves>

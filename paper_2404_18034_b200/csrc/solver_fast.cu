@@ -69,11 +69,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 /// Loads rows 3g..3g+2 of [A-_k | B-_k | B+_k] of instance b into registers.
 __device__ __forceinline__ void load_rows(const SubArrays& sp, int b, int m, int k, int g,
@@ -521,7 +516,7 @@ power_fast_kernel(PowerArgs a) {
       }
       inv = rsqrt(ss);
       const double sigma_star = ss * inv;
-      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;
       if (hit) {
         done = true;
@@ -892,18 +887,18 @@ pipg_fast_kernel(PipgArgs a) {
       auto primal = [&](int off, int count, bool finite_checked) {
         for (int e = tid; e < count; e += T) {
           const double c = cur[off + e], o = prev[off + e];
-          z_cur = fmax(z_cur, fabs(c));
-          z_prev = fmax(z_prev, fabs(o));
-          z_del = fmax(z_del, fabs(c - o));
+          z_cur = max_nn(z_cur, fabs(c));
+          z_prev = max_nn(z_prev, fabs(o));
+          z_del = max_nn(z_del, fabs(c - o));
           if (finite_checked && !pt_finite(c)) bad = 1.0;
         }
       };
       auto dual = [&](int off, int count, bool finite_checked) {
         for (int e = tid; e < count; e += T) {
           const double c = cur[off + e], o = prev[off + e];
-          r_cur = fmax(r_cur, fabs(c));
-          r_prev = fmax(r_prev, fabs(o));
-          r_del = fmax(r_del, fabs(c - o));
+          r_cur = max_nn(r_cur, fabs(c));
+          r_prev = max_nn(r_prev, fabs(o));
+          r_del = max_nn(r_del, fabs(c - o));
           if (finite_checked && !pt_finite(c)) bad = 1.0;
         }
       };
@@ -913,9 +908,9 @@ pipg_fast_kernel(PipgArgs a) {
       primal(S.vn, NM, false);
       dual(S.ph, NM, true);
       dual(S.th, mloc, false);
-      z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
-      r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
-      bad = warp_max(bad);
+      z_cur = warp_max_nn(z_cur); z_prev = warp_max_nn(z_prev); z_del = warp_max_nn(z_del);
+      r_cur = warp_max_nn(r_cur); r_prev = warp_max_nn(r_prev); r_del = warp_max_nn(r_del);
+      bad = warp_max_nn(bad);
       if (lane == 0) {
         double* rw = red + warp * 8;
         rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
@@ -927,7 +922,7 @@ pipg_fast_kernel(PipgArgs a) {
       for (int q = 0; q < 7; ++q) {
         double mx = 0.0;
 #pragma unroll
-        for (int w = 0; w < kFastWarps; ++w) mx = fmax(mx, w < nwarps ? red[w * 8 + q] : 0.0);
+        for (int w = 0; w < kFastWarps; ++w) mx = max_nn(mx, w < nwarps ? red[w * 8 + q] : 0.0);
         v[q] = mx;
       }
       if constexpr (kCluster) {  // combine with the partner's maxima
@@ -938,7 +933,7 @@ pipg_fast_kernel(PipgArgs a) {
         }
         cg::this_cluster().sync();
 #pragma unroll
-        for (int q = 0; q < 7; ++q) v[q] = fmax(v[q], red[kFastWarps * 8 + q]);
+        for (int q = 0; q < 7; ++q) v[q] = max_nn(v[q], red[kFastWarps * 8 + q]);
         cg::this_cluster().sync();  // red and the snapshots are rewritten later
       } else {
         __syncthreads();  // red and the snapshots are rewritten later
@@ -947,8 +942,8 @@ pipg_fast_kernel(PipgArgs a) {
         diverged = true;
         break;
       }
-      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) &&
-          v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+      if (v[2] <= a.eps_abs + a.eps_rel * max_nn(v[0], v[1]) &&
+          v[5] <= a.eps_abs + a.eps_rel * max_nn(v[3], v[4])) {
         converged = true;
         break;
       }

@@ -23,11 +23,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 /// Row i of (block * vec): sum_j M[i][j] v[j], ascending j (mat_vec, smallmat.hpp:93-97).
 __device__ __forceinline__ double row_dot(const double* __restrict__ M, int cols, int i,
@@ -168,7 +163,7 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) power_generic_kernel(Po
       sigma = 0.0;
       break;
     }
-    if (fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma)) {
+    if (fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma)) {
       sigma = sigma_star;
       break;
     }
@@ -287,9 +282,9 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(Pip
       x_cur[e] = xn;
       x_rf[e] = 2.0 * xn - xe;
       if (check) {
-        z_cur = fmax(z_cur, fabs(xn));
-        z_prev = fmax(z_prev, fabs(old));
-        z_del = fmax(z_del, fabs(xn - old));
+        z_cur = max_nn(z_cur, fabs(xn));
+        z_prev = max_nn(z_prev, fabs(old));
+        z_del = max_nn(z_del, fabs(xn - old));
         if (!pt_finite(xn)) bad = 1.0;
       }
     }
@@ -312,22 +307,22 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(Pip
       u_cur[e] = un;
       u_rf[e] = 2.0 * un - ue;
       if (check) {
-        z_cur = fmax(z_cur, fabs(un));
-        z_prev = fmax(z_prev, fabs(old));
-        z_del = fmax(z_del, fabs(un - old));
+        z_cur = max_nn(z_cur, fabs(un));
+        z_prev = max_nn(z_prev, fabs(old));
+        z_del = max_nn(z_del, fabs(un - old));
         if (!pt_finite(un)) bad = 1.0;
       }
     }
     // ---- virtual-control slacks, pipg.hpp:423-430
     for (int e = tid; e < NM; e += T) {
       const double ph = ph_ex[e];
-      const double vp = fmax(0.0, vp_ex[e] - alpha * (w_ep + ph));
-      const double vn = fmax(0.0, vn_ex[e] - alpha * (w_ep - ph));
+      const double vp = clip0(vp_ex[e] - alpha * (w_ep + ph));
+      const double vn = clip0(vn_ex[e] - alpha * (w_ep - ph));
       if (check) {
         const double op = vp_cur[e], on = vn_cur[e];
-        z_cur = fmax(z_cur, fmax(fabs(vp), fabs(vn)));
-        z_prev = fmax(z_prev, fmax(fabs(op), fabs(on)));
-        z_del = fmax(z_del, fmax(fabs(vp - op), fabs(vn - on)));
+        z_cur = max_nn(max_nn(z_cur, fabs(vp)), fabs(vn));
+        z_prev = max_nn(max_nn(z_prev, fabs(op)), fabs(on));
+        z_del = max_nn(max_nn(z_del, fabs(vp - op)), fabs(vn - on));
       }
       vp_cur[e] = vp;
       vn_cur[e] = vn;
@@ -349,9 +344,9 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(Pip
       const double phn = phe + beta * resid;
       if (check) {
         const double old = ph_cur[e];
-        r_cur = fmax(r_cur, fabs(phn));
-        r_prev = fmax(r_prev, fabs(old));
-        r_del = fmax(r_del, fabs(phn - old));
+        r_cur = max_nn(r_cur, fabs(phn));
+        r_prev = max_nn(r_prev, fabs(old));
+        r_del = max_nn(r_del, fabs(phn - old));
         if (!pt_finite(phn)) bad = 1.0;
       }
       ph_cur[e] = phn;
@@ -367,21 +362,21 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(Pip
       }
       const double drift = d1 - d0 - __ldg(epsr + k);
       const double the = th_ex[k];
-      const double thn = fmax(0.0, the + beta * drift);
+      const double thn = clip0(the + beta * drift);
       if (check) {
         const double old = th_cur[k];
-        r_cur = fmax(r_cur, fabs(thn));
-        r_prev = fmax(r_prev, fabs(old));
-        r_del = fmax(r_del, fabs(thn - old));
+        r_cur = max_nn(r_cur, fabs(thn));
+        r_prev = max_nn(r_prev, fabs(old));
+        r_del = max_nn(r_del, fabs(thn - old));
       }
       th_cur[k] = thn;
       th_ex[k] = (1.0 - rho) * the + rho * thn;
     }
     iters = j;
     if (check) {
-      z_cur = warp_max(z_cur); z_prev = warp_max(z_prev); z_del = warp_max(z_del);
-      r_cur = warp_max(r_cur); r_prev = warp_max(r_prev); r_del = warp_max(r_del);
-      bad = warp_max(bad);
+      z_cur = warp_max_nn(z_cur); z_prev = warp_max_nn(z_prev); z_del = warp_max_nn(z_del);
+      r_cur = warp_max_nn(r_cur); r_prev = warp_max_nn(r_prev); r_del = warp_max_nn(r_del);
+      bad = warp_max_nn(bad);
       if (lane == 0) {
         red[0 * kMaxWarps + warp] = z_cur; red[1 * kMaxWarps + warp] = z_prev;
         red[2 * kMaxWarps + warp] = z_del; red[3 * kMaxWarps + warp] = r_cur;
@@ -395,15 +390,15 @@ __global__ void __launch_bounds__(kMaxGenericThreads, 1) pipg_generic_kernel(Pip
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
         double mx = 0.0;
-        for (int w = 0; w < nwarps; ++w) mx = fmax(mx, red[q * kMaxWarps + w]);
+        for (int w = 0; w < nwarps; ++w) mx = max_nn(mx, red[q * kMaxWarps + w]);
         v[q] = mx;
       }
       if (v[6] > 0.0) {
         diverged = true;
         break;
       }
-      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) &&
-          v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+      if (v[2] <= a.eps_abs + a.eps_rel * max_nn(v[0], v[1]) &&
+          v[5] <= a.eps_abs + a.eps_rel * max_nn(v[3], v[4])) {
         converged = true;
         break;
       }

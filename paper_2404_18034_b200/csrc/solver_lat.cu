@@ -51,11 +51,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ double xor_get(double v, int mask) { return __shfl_xor_sync(0xffffffffu, v, mask); }
 
 // Shared memory of one CTA.  Node arrays carry slot -1 in front (previous node: the zero guard of
@@ -464,7 +459,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
       }
       inv = rsqrt(ss);
       const double sigma_star = ss * inv;
-      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * fmax(sigma_star, sigma);
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;
       if (hit) {
         done = true;
@@ -679,21 +674,21 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, bad = 0.0;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        z_cur = fmax(z_cur, fabs(cur_p[e]));
-        z_prev = fmax(z_prev, fabs(prv_p[e]));
-        z_del = fmax(z_del, fabs(cur_p[e] - prv_p[e]));
+        z_cur = max_nn(z_cur, fabs(cur_p[e]));
+        z_prev = max_nn(z_prev, fabs(prv_p[e]));
+        z_del = max_nn(z_del, fabs(cur_p[e] - prv_p[e]));
         if (!pt_finite(cur_p[e])) bad = 1.0;
       }
-      z_cur = fmax(z_cur, fmax(fabs(cur_vp), fabs(cur_vn)));
-      z_prev = fmax(z_prev, fmax(fabs(prv_vp), fabs(prv_vn)));
-      z_del = fmax(z_del, fmax(fabs(cur_vp - prv_vp), fabs(cur_vn - prv_vn)));
+      z_cur = max_nn(max_nn(z_cur, fabs(cur_vp)), fabs(cur_vn));
+      z_prev = max_nn(max_nn(z_prev, fabs(prv_vp)), fabs(prv_vn));
+      z_del = max_nn(max_nn(z_del, fabs(cur_vp - prv_vp)), fabs(cur_vn - prv_vn));
       if (!t.theta_lane && !pt_finite(cur_d)) bad = 1.0;
       r_cur = fabs(cur_d);
       r_prev = fabs(prv_d);
       r_del = fabs(cur_d - prv_d);
       double v[7] = {z_cur, z_prev, z_del, r_cur, r_prev, r_del, bad};
 #pragma unroll
-      for (int k = 0; k < 7; ++k) v[k] = warp_max(v[k]);
+      for (int k = 0; k < 7; ++k) v[k] = warp_max_nn(v[k]);
       if (t.lane == 0) {
 #pragma unroll
         for (int k = 0; k < 7; ++k) S->red[t.warp * 8 + k] = v[k];
@@ -701,14 +696,14 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
       __syncthreads();
       if (t.tid < 7) {  // this CTA's maxima into every rank's table
         double mx = 0.0;
-        for (int w = 0; w < t.nwarps; ++w) mx = fmax(mx, S->red[w * 8 + t.tid]);
+        for (int w = 0; w < t.nwarps; ++w) mx = max_nn(mx, S->red[w * 8 + t.tid]);
         for (int r = 0; r < cut.ranks; ++r) *cg::this_cluster().map_shared_rank(S->redc + cut.rank * 8 + t.tid, r) = mx;
       }
       cg::this_cluster().sync();
 #pragma unroll
       for (int k = 0; k < 7; ++k) {
         double mx = 0.0;
-        for (int r = 0; r < cut.ranks; ++r) mx = fmax(mx, S->redc[r * 8 + k]);
+        for (int r = 0; r < cut.ranks; ++r) mx = max_nn(mx, S->redc[r * 8 + k]);
         v[k] = mx;
       }
       cg::this_cluster().sync();  // the tables are rewritten at the next check
@@ -716,7 +711,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) pipg_lat_kernel(PipgArgs a)
         diverged = true;
         break;
       }
-      if (v[2] <= a.eps_abs + a.eps_rel * fmax(v[0], v[1]) && v[5] <= a.eps_abs + a.eps_rel * fmax(v[3], v[4])) {
+      if (v[2] <= a.eps_abs + a.eps_rel * max_nn(v[0], v[1]) && v[5] <= a.eps_abs + a.eps_rel * max_nn(v[3], v[4])) {
         converged = true;
         break;
       }

@@ -486,8 +486,11 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   // tolerance is four orders of magnitude wider) and the scale 1 / sigma of pipg.hpp:243 is the
   // same rsqrt: no square root and no division on the trip's critical path.  The value returned is
   // the correctly rounded sqrt of the last squared norm.
-  double inv = rsqrt(ss);
-  double sigma = ss * inv;
+  // The stopping test runs in every trip, also the first (no `if (j > 1)` block that would keep the
+  // norm -> rsqrt -> test chain out of the basic block of the gathers it can overlap with): the first
+  // one reads the seed's norm again and compares it with a NaN, which no tolerance accepts.
+  double inv;
+  double sigma = __longlong_as_double(0x7ff8000000000000ll);
 
   // The forward products of trip j + 1 are issued right behind the adjoint map of trip j, in front
   // of the barrier, so that the warp reduction of trip j's norm shares overlaps them.
@@ -525,17 +528,13 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
       const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
       s[r] = (s[r] - xn) + vcd[r];
     }
-    if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+    {  // stopping test of trip j-1 (pipg.hpp:277-289); j = 1: the seed against NaN, never met
       ss = norm_sq((j - 1) & 1);
-      if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284
-        done = true;
-        break;
-      }
       inv = rsqrt(ss);
       const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;
-      if (hit) {
+      if (hit || ss == 0.0) {  // met, or the iterate is in the null space (pipg.hpp:280-284)
         done = true;
         break;
       }
@@ -749,6 +748,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     for (int q = 0; q < RT::nxc; ++q)
       if (on[RT::xc(q)] != 0.0) fix_bits |= 1 << q;
   }
+
   const bool warp_fix = __any_sync(kFull, fix_bits != 0);  // warp-uniform
 
   // owner-private extrapolated copies
@@ -795,7 +795,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         if (c == kNX - 1) base += th_s[-1] - th_s[0];
         const double grad = base + gx_[q];
         double xn = x0 + -alpha * grad;
-        if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;
+        if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;  // (measured: faster than unconditional)
         rx[q] = fma(2.0, xn, -x0);
         if (kStore && t.auth) snap[SN.x + t.k * kNX + c] = xn;
         xe[q] = extrapolate(x0, xn);

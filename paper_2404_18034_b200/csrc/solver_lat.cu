@@ -436,9 +436,13 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test) and
   // the scale 1 / sigma the same rsqrt: no square root on the trip's critical path.  The value
   // returned is the correctly rounded sqrt of the last squared norm.
+  // In a single CTA the stopping test runs in every trip, also the first -- no `if (j > 1)` block that
+  // would keep the norm -> rsqrt -> test chain out of the basic block of the products it can overlap
+  // with: the first test reads the seed's norm again and compares it with a NaN, which no tolerance
+  // accepts.  (In a cluster the norm of a trip is received once through a mailbox.)
   double ss_last = sigma;
   double inv = rsqrt(ss_last);
-  sigma = ss_last * inv;
+  sigma = kLone ? __longlong_as_double(0x7ff8000000000000ll) : ss_last * inv;
   // row lanes scale (forward row - x_{k+1}[row]) + vcd; the relaxation-dual lane x_{k+1}[14] - x_k[14]
   const double live = (t.row_alive || (t.theta_lane && t.ival)) ? 1.0 : 0.0;
 
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     const double xn1 = q.x_next[0], xc = q.x_cur[0];
     const double r = forward_row(aop, q.seg, t.rg);
     const double s = t.theta_lane ? xn1 - xc : (r - xn1) + vcd;
-    if (j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+    if (kLone || j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
       const double ss = norm_sq(j - 1);
       ss_last = ss;
       if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284

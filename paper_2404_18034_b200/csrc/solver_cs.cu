@@ -530,7 +530,7 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
     }
     {  // stopping test of trip j-1 (pipg.hpp:277-289); j = 1: the seed against NaN, never met
       ss = norm_sq((j - 1) & 1);
-      inv = rsqrt(ss);
+      inv = rsqrt_pos(ss);
       const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;

@@ -514,7 +514,7 @@ power_fast_kernel(PowerArgs a) {
         done = true;
         break;
       }
-      inv = rsqrt(ss);
+      inv = rsqrt_pos(ss);
       const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;

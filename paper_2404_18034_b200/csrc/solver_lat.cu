@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
         done = true;
         break;
       }
-      inv = rsqrt(ss);
+      inv = rsqrt_pos(ss);
       const double sigma_star = ss * inv;
       const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
       sigma = sigma_star;

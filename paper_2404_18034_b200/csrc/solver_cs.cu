@@ -30,8 +30,8 @@
 //     either side (lane 31 of the first warp repeats node 31, lane 0 of the second warp node 30),
 //     so no value ever has to cross warps in the middle of a phase.
 // Two block barriers per iteration / trip, as in solver_fast.cu, but 0.4x the shared-memory
-// wavefronts, 0.72x the FMAs and 320 / 400 instead of 397 / 540 instructions per warp and trip /
-// iteration: 2 030 / 2 400 clk against 2 750 / 3 160 (B200, N = 50).  The four role bodies of a loop
+// wavefronts, 0.72x the FMAs and 360 / 400 instead of 397 / 540 instructions per warp and trip /
+// iteration: 1 850 / 2 400 clk against 2 750 / 3 160 (B200, N = 50).  The four role bodies of a loop
 // share the SM's 32 KB instruction cache; the PIPG loop (25.6 KB) only became faster than the dense
 // kernel once it fitted, and its speed follows its instruction count: keep
 // role-independent work (stopping test, set-up) in shared functions and out of the role bodies.

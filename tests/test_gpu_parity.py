@@ -394,6 +394,32 @@ def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor):
                 assert np.abs(ws[f][b] - getattr(ref, f)).max() <= TOL_ITER, (b, f)
 
 
+def test_scp_solve_general_vehicle_fills_the_whole_pattern(ptor):
+    """The default vehicle (diagonal inertia, thrust lever along the body x axis) leaves entries of
+    the structural pattern zero (tests/test_block_structure.py); a vehicle with a full inertia matrix
+    and an oblique lever arm does not.  The pattern is parameter-independent, so the column-sparse
+    kernels take these instances too, and the solves agree with the oracle on both families."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(20)
+    sc.inertia = (0.1, 0.01, -0.02, 0.01, 0.25, 0.015, -0.02, 0.015, 0.22)
+    sc.r_thrust = (-0.5, 0.03, -0.02)
+    sc.max_iters, sc.pipg_j_max, sc.power_j_max = 3, 250, 300
+    d = sc.problem_desc()
+    batch = scenario.make_batch(sc, [0, 5, 9])
+    refs = [ptor.scp_solve(d, batch["init_state"][b], batch["x_guess"][b], batch["u_guess"][b],
+                           int(batch["rng_seed"][b]), with_trips=True) for b in range(3)]
+    rc, blocks = ptor.linearize_all(d, batch["x_guess"][0], batch["u_guess"][0])
+    assert rc == 0 and np.abs(blocks["Bm"][:, 11, 1]).max() > 0  # a torque row reached by a thrust column the default vehicle leaves at zero
+    for path in ("fast", "dense"):
+        with Solver(d) as s:
+            s.set_solver_path(path)
+            out = s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+        for b, (rc, ref) in enumerate(refs):
+            assert rc == 0
+            check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
+
+
 def check_scp_against_oracle(sc, out, b, ref, trips_ref=None):
     assert out["status"][b] == 0
     assert out["scp_iterations"][b] == ref["scp_iterations"]

@@ -359,6 +359,20 @@ def other_configs(device_index, fp64_peak):
         "power_trips_mean": float(res["power_trips"].sum(axis=1).mean()),
         "what": "full SCP solves at N=100 on one GPU (2-CTA cluster per instance, two waves), device time of "
                 "the graph"}
+    # ---- the headline configuration on the dense register-resident kernels alone (round-1 path), for
+    #      the gain of the column-sparse kernels in the same run
+    n, B = 50, 4096
+    sc = scenario.default_scenario(n)
+    batch = scenario.make_batch(sc, range(B))
+    with Solver(sc.problem_desc(), device=device_index) as s:
+        s.set_solver_path("dense")
+        s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+        s.scp_solve(batch["init_state"], batch["x_guess"], batch["u_guess"], batch["rng_seed"])
+        st = s.scp_stage_times()
+    out["config4_on_the_dense_kernels_4096xN50"] = {
+        "solves_per_s": B / (st["graph_total"] * 1e-3), "stages_ms": st,
+        "what": "the step of the headline metric with ptopt_cuda_set_solver_path(PTOPT_SOLVER_FAST_DENSE): five "
+                "threads per node, dense operator (no zero pattern assumed), device time of the graph"}
     # ---- config 1 shape: the default scenario (N=15), one instance, full SCP loop
     sc = scenario.default_scenario(15)
     one = scenario.make_batch(sc, range(1))

@@ -422,42 +422,53 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
   if (t.lane == 0) shares[t.warp] = acc;
   __syncthreads();
   if constexpr (!kLone) send_total(0);
-  double sigma = norm_sq(0);
-  if (sigma == 0.0) {  // pipg.hpp:224-225
-    if (t.tid == 0 && cut.rank == 0) {
-      if (a.status) a.status[b] = kStSeedZero;
-      a.sigma[b] = 0.0;
-      if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
+  // The norm of trip j-1 (j = 1: the seed) is received and tested inside trip j, every trip alike --
+  // no `if (j > 1)` block that would keep the norm -> rsqrt -> test chain out of the basic block of
+  // the products it can overlap with.  The first test compares the seed's norm with a NaN, which no
+  // tolerance accepts; a zero seed (pipg.hpp:224-225) is found there too.  Inside the loop sigma is
+  // ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test) and the scale 1 / sigma the
+  // same rsqrt; the value returned is the correctly rounded sqrt of the last squared norm.
+  // (A single CTA tests the seed in front of the loop as well: its norm needs no mailbox, and the
+  // kernel measures 4 % faster that way.)
+  double ss_last = 0.0, inv = 0.0;
+  double sigma = __longlong_as_double(0x7ff8000000000000ll);
+  bool seed_zero = false;
+  if constexpr (kLone) {
+    ss_last = norm_sq(0);
+    if (ss_last == 0.0) {  // pipg.hpp:224-225
+      if (t.tid == 0) {
+        if (a.status) a.status[b] = kStSeedZero;
+        a.sigma[b] = 0.0;
+        if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
+      }
+      return;
     }
-    recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
-    cg::this_cluster().sync();
-    return;
+    inv = rsqrt(ss_last);
   }
-  // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test) and
-  // the scale 1 / sigma the same rsqrt: no square root on the trip's critical path.  The value
-  // returned is the correctly rounded sqrt of the last squared norm.
-  // In a single CTA the stopping test runs in every trip, also the first -- no `if (j > 1)` block that
-  // would keep the norm -> rsqrt -> test chain out of the basic block of the products it can overlap
-  // with: the first test reads the seed's norm again and compares it with a NaN, which no tolerance
-  // accepts.  (In a cluster the norm of a trip is received once through a mailbox.)
-  double ss_last = sigma;
-  double inv = rsqrt(ss_last);
-  sigma = kLone ? __longlong_as_double(0x7ff8000000000000ll) : ss_last * inv;
   // row lanes scale (forward row - x_{k+1}[row]) + vcd; the relaxation-dual lane x_{k+1}[14] - x_k[14]
   const double live = (t.row_alive || (t.theta_lane && t.ival)) ? 1.0 : 0.0;
 
   int trips = 0;
   bool done = false;
+  if constexpr (!kLone) {
+    if (a.j_max < 1) {  // no trip at all: the seed's norm is the result
+      ss_last = norm_sq(0);
+      seed_zero = ss_last == 0.0;
+      recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, 0);
+      done = true;
+    }
+  }
   for (int j = 1; j <= a.j_max; ++j) {
     // ---- forward map (pipg.hpp:234-245); the norm of trip j-1 arrives while the products run
     recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, j - 1);  // the next rank's first node of trip j-1
     const double xn1 = q.x_next[0], xc = q.x_cur[0];
     const double r = forward_row(aop, q.seg, t.rg);
     const double s = t.theta_lane ? xn1 - xc : (r - xn1) + vcd;
-    if (kLone || j > 1) {  // stopping test of trip j-1 (pipg.hpp:277-289)
+    {  // stopping test of trip j-1 (pipg.hpp:277-289); j = 1: the seed against NaN, never met
       const double ss = norm_sq(j - 1);
       ss_last = ss;
-      if (ss == 0.0) {  // iterate in the null space, pipg.hpp:280-284
+      if (ss == 0.0) {  // a zero seed (pipg.hpp:224-225), or an iterate in the null space (:280-284)
+        if constexpr (!kLone) seed_zero = j == 1;
         done = true;
         break;
       }
@@ -499,7 +510,8 @@ __global__ void __launch_bounds__(kLatThreadsMax, 1) power_lat_kernel(PowerArgs 
     if (a.j_max >= 1) recv(kBoxNext, t.next_warp, t.next_armer, kNextBytes, a.j_max);  // still on its way
   }
   if (t.tid == 0 && cut.rank == 0) {
-    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss_last);
+    if (seed_zero && a.status) a.status[b] = kStSeedZero;
+    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss_last);  // 0 for a zero seed
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
   }
   cg::this_cluster().sync();  // nobody leaves while a neighbour may still write into it

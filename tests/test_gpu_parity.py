@@ -219,6 +219,30 @@ def test_power_iteration_zero_seed_and_explicit_a_plus(solver15, ptor):
     assert status[0] == 0 and abs(sigma[0] - sig_ref) <= TOL_SIGMA * sig_ref
 
 
+@pytest.mark.parametrize("nodes", [15, 50])
+def test_power_iteration_zero_seed_on_the_rocket_kernels(ptor, nodes):
+    """pipg.hpp:224-225 on every register-resident family: a zero seed next to a regular one in the same
+    batch (the latency family finds it inside its first trip when the instance is spread over a
+    cluster, in front of the loop when it is not)."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(nodes)
+    d, shape, sub = rocket_subproblem(sc, ptor, 0)
+    n, m = d.nodes, d.nodes - 1
+    sx, su = ptor.scp_seed(scenario.run_seed(sc.dispersion.seed, 0), n)
+    z = np.zeros((m, NX))
+    rc, sig_ref, _ = ptor.power_iteration(shape, sub, sx, su, z, z, 1e-12, 1e-12, 0.05, 300, with_trips=True)
+    assert rc == 0
+    two = {f: (None if getattr(sub, f) is None else np.stack([getattr(sub, f)] * 2)) for f in sub.FIELDS}
+    seeds = [np.stack([np.zeros_like(a), a]) for a in (sx, su, z, z)]
+    for path in ("fast", "dense", "latency"):
+        with Solver(d) as s:
+            s.set_solver_path(path)
+            sigma, trips, status = s.power_iteration_custom(shape, two, *seeds, 1e-12, 1e-12, 0.05, 300)
+        assert status[0] == abi.ST_POWER_SEED_ZERO and sigma[0] == 0.0 and trips[0] == 0, path
+        assert status[1] == 0 and abs(sigma[1] - sig_ref) <= TOL_SIGMA * sig_ref, path
+
+
 def ws_dict(ws: Workspace):
     return {f: getattr(ws, f)[None].copy() for f in ws.FIELDS}
 

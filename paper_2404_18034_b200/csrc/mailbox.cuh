@@ -24,6 +24,42 @@ __device__ __forceinline__ void push_f64(unsigned dst, double v, unsigned box) {
                "r"(box)
                : "memory");
 }
+/// The same as one predicated instruction (no branch round the store).
+__device__ __forceinline__ void push_f64_pred(unsigned pred, unsigned dst, double v, unsigned box) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.u32 p, %3, 0;\n"
+      "  @p st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2]; }" ::"r"(dst),
+      "d"(v), "r"(box), "r"(pred)
+      : "memory");
+}
+/// Arms the mailbox at shared-memory address `bar` when `pred` is set (one predicated instruction).
+__device__ __forceinline__ void mbar_expect_pred(unsigned pred, unsigned bar, int bytes) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0;\n"
+               "  @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1; }" ::"r"(bar),
+               "r"(bytes), "r"(pred)
+               : "memory");
+}
+/// mbar_wait on a shared-memory address.
+__device__ __forceinline__ void mbar_wait_at(unsigned bar, unsigned parity) {
+  unsigned ok, polls = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(bar), "r"(parity & 1u)
+                 : "memory");
+  } while (!ok && ++polls < (1u << 26));
+  if (!ok) __trap();
+}
+/// One non-blocking test of a mailbox phase (no memory clobber: ordinary loads and arithmetic may be
+/// scheduled round it; other volatile asm statements -- the loads of the received entries -- stay
+/// behind it).  Returns non-zero when the phase is complete.
+__device__ __forceinline__ unsigned mbar_test_at(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(ok)
+               : "r"(bar), "r"(parity & 1u));
+  return ok;
+}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

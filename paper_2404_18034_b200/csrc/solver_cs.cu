@@ -43,7 +43,12 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+#include "mailbox.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ptopt_b200 {
 
@@ -199,32 +204,117 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+/// The part of the horizon a CTA works on.  Without a cluster: everything.  In a cluster of two
+/// (62..kCsClusterMaxNodes nodes, power iteration) rank 0 owns nodes [0, c), c = ceil(n / 2), and
+/// carries a redundant copy of node c behind its last node; rank 1 owns [c, n) and carries a copy of
+/// node c - 1 in front of its first one (only as the source of B+^T phi of interval c - 1).  The
+/// duals of the two boundary intervals are the only values that cross the cut (see Port).
+struct Cut {
+  int rank;  // CTA rank in the cluster
+  int base;  // global node of local node 0
+  int lo, hi;  // owned nodes [lo, hi)
+  int hip;   // primal entries are maintained for nodes [lo, hip): hi + 1 in rank 0 of a cluster
+};
+template <bool kCluster>
+__device__ __forceinline__ Cut make_cut(int n) {
+  Cut c;
+  if constexpr (kCluster) {
+    const int mid = (n + 1) / 2;
+    c.rank = (int)cg::this_cluster().block_rank();
+    c.base = c.rank == 0 ? 0 : mid - 1;
+    c.lo = c.rank == 0 ? 0 : mid;
+    c.hi = c.rank == 0 ? mid : n;
+    c.hip = c.rank == 0 ? mid + 1 : n;
+  } else {
+    c.rank = 0;
+    c.base = 0;
+    c.lo = 0;
+    c.hi = c.hip = n;
+  }
+  return c;
+}
+
 /// Which node a lane holds and in what capacity.
 struct Lane {
-  int k;        // node
-  int slot;     // k + 1
+  int k;        // node (global)
+  int slot;     // local node + 1
   bool halo;    // a redundant copy of a node another warp owns
-  bool auth;    // this thread is THE owner of node k (k < n, not a halo copy)
-  bool primal;  // its primal entries are valid (owner, or the halo copy of node 31 in the first warp)
+  bool auth;    // this thread is THE owner of node k (an owned node of this CTA, not a halo copy)
+  bool primal;  // its primal entries are valid (owner, the halo copy of node 31 in the first warp, or
+                // rank 0's copy of the first node of rank 1)
+  bool pubx;    // it publishes the primal entries other roles read through shared memory
   bool ival;    // auth and k is an interval (k < n - 1)
+  bool have;    // it loads the operator block of interval k
 };
 template <int kHalves>
-__device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
+__device__ __forceinline__ Lane make_lane(const Cut& c, int n, int half, int lane) {
   Lane t;
-  if (kHalves == 1) {
-    t.k = lane;
-    t.halo = false;
-    t.auth = t.k < n;
-    t.primal = t.auth;
-  } else {
-    t.k = half == 0 ? lane : 30 + lane;
-    t.halo = half == 0 ? lane == 31 : lane == 0;
-    t.auth = !t.halo && t.k < n;
-    t.primal = t.k < n && (half == 0 || lane != 0);
-  }
-  t.slot = t.k + 1;
+  const int l = kHalves == 1 ? lane : (half == 0 ? lane : 30 + lane);
+  t.k = c.base + l;
+  t.halo = kHalves == 2 && (half == 0 ? lane == 31 : lane == 0);
+  t.auth = !t.halo && t.k >= c.lo && t.k < c.hi;
+  t.primal = t.k >= c.lo && t.k < c.hip && (kHalves == 1 || half == 0 || lane != 0);
+  t.pubx = t.primal && !t.halo;
+  t.slot = l + 1;
   t.ival = t.auth && t.k < n - 1;
+  t.have = t.k < n - 1 && t.k <= c.hi;  // halo copies load their node's block too
   return t;
+}
+template <int kHalves>
+__device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
+  return make_lane<kHalves>(make_cut<false>(n), n, half, lane);
+}
+
+/// Hand-off between the two CTAs of a cluster (mailbox.cuh): per trip each CTA pushes the duals of
+/// its boundary interval (fifteen rows and the relaxation dual, 128 bytes) into the partner's phi /
+/// theta slots, and every warp its share of the squared norm into the partner's copy of `red`.
+/// Nothing is read remotely in the loop.  The norm mailboxes alternate by trip parity (both CTAs
+/// send every trip; a CTA is never two trips ahead, see solver_fast.cu).
+struct Port {
+  static constexpr int kBoxAt = 64;   // doubles into `red`: three mbarriers, then the pattern flag
+  static constexpr int kPhiBytes = 8 * (kNX + 1);
+  unsigned red;     // shared-memory address of the norm shares, held in a register
+  unsigned box;     // [3] mbarriers (shared-memory address): phi, norm of even trips, norm of odd trips
+  unsigned rbox;    // the partner's
+  unsigned rsm;     // the partner's shared memory (shared::cluster address of sm[0])
+  unsigned armer;   // thread 0
+  bool need_phi;    // this warp reads a slot the partner fills
+  __device__ __forceinline__ void recv_phi(int phase) const {
+    if (!need_phi) return;
+    mbar_expect_pred(armer, box, kPhiBytes);
+    mbar_wait_at(box, (unsigned)phase);
+  }
+  __device__ __forceinline__ void recv_norm(int trip, int bytes) const {
+    const unsigned at = box + 8u + 8u * (unsigned)(trip & 1);
+    mbar_expect_pred(armer, at, bytes);
+    mbar_wait_at(at, (unsigned)(trip >> 1));
+  }
+  __device__ __forceinline__ unsigned norm_box(int trip) const { return rbox + 8u * (1u + (unsigned)(trip & 1)); }
+};
+/// Opens the mailboxes (the shared memory is cleared and a block barrier passed), exchanges the
+/// pattern verdicts and returns the cluster-wide one.
+__device__ __forceinline__ bool open_port(Port& pt, double* sm, double* red, const Cut& c, const Lane& t, bool bad) {
+  const int tid = threadIdx.x;
+  unsigned long long* box = reinterpret_cast<unsigned long long*>(red + Port::kBoxAt);
+  pt.red = smem_u32(red);
+  asm volatile("mov.u32 %0, %0;" : "+r"(pt.red));  // opaque: not to be rematerialised inside the loop
+  pt.box = pt.red + 8u * (unsigned)Port::kBoxAt;
+  int* flag = reinterpret_cast<int*>(red + Port::kBoxAt + 4);
+  if (tid == 0) {
+    mbar_init(box, 1);
+    mbar_init(box + 1, 1);
+    mbar_init(box + 2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *flag = bad ? 1 : 0;
+  }
+  cg::this_cluster().sync();
+  pt.rbox = partner_u32(box, c.rank ^ 1);
+  pt.rsm = partner_u32(sm, c.rank ^ 1);
+  pt.armer = tid == 0 ? 1u : 0u;
+  const bool reads = c.rank == 0 ? t.k == c.hi : (t.k == c.lo - 1 || t.k == c.lo);
+  pt.need_phi = __any_sync(kFull, reads) || tid < 32;  // the armer's warp always waits
+  const int theirs = *cg::this_cluster().map_shared_rank(flag, c.rank ^ 1);
+  return bad || theirs != 0;
 }
 
 /// The operator columns of role R of one interval, and whether the block has the expected zeros.
@@ -412,7 +502,7 @@ __device__ __forceinline__ void gather_rows(const double (&own)[RoleT<K, R>::nro
 // ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
-template <int K, int R, int kHalves>
+template <int K, int R, int kHalves, bool kCluster>
 __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b, unsigned char* handled) {
   using RT = RoleT<K, R>;
   using Cfg = CsCfg<K, kHalves>;
@@ -420,23 +510,34 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   constexpr CsLayout L = cs_layout<K, kHalves>(false);
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
-  const Lane t = make_lane<kHalves>(n, half, lane);
+  const Cut cut = make_cut<kCluster>(n);
+  const Lane t = make_lane<kHalves>(cut, n, half, lane);
   for (int e = tid; e < L.total; e += Cfg::threads) sm[e] = 0.0;
 
   OpCols<K, R> op;
-  const bool have = t.k < m;  // halo copies load their node's block too
-  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
-  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
-    if (tid == 0) handled[b] = 0;
+  bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (t.have ? t.k : 0), t.have, op);
+  bad = __syncthreads_or(bad ? 1 : 0) != 0;
+  double* red = sm + L.red;               // [2][kCsWarps] shares of the squared norm, by trip parity
+  Port port{};
+  if constexpr (kCluster) bad = open_port(port, sm, red, cut, t, bad);
+  if (bad) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0 && cut.rank == 0) handled[b] = 0;
+    if constexpr (kCluster) cg::this_cluster().sync();  // the partner reads this CTA's verdict
     return;
   }
-  if (tid == 0) handled[b] = 1;
+  if (tid == 0 && cut.rank == 0) handled[b] = 1;
 
   double* phi_s = sm + L.phi + t.slot;    // row i at + i * S; interval k-1 at -1
   double* th_s = sm + L.th + t.slot;
   double* part_s = sm + L.part + t.slot;  // [role][row] at + (role * 15 + row) * S
   double* xn_s = sm + L.xn + t.slot;      // [3] at + q * S; node k+1 at +1
-  double* red = sm + L.red;               // [2][kCsWarps] shares of the squared norm, by trip parity
+  // cluster: the owners of the boundary interval store its duals in the partner's slots as well
+  const bool pusher = kCluster && t.auth && t.k == (cut.rank == 0 ? cut.hi - 1 : cut.lo);
+  const int pslot = cut.rank == 0 ? 1 : cut.lo + 1;  // slot of that interval over there
+  const unsigned rphi = port.rsm + 8u * (unsigned)(L.phi + pslot), rth = port.rsm + 8u * (unsigned)(L.th + pslot);
+  const unsigned rred = port.rsm + 8u * (unsigned)(L.red + cut.rank * (kCsWarps / 2) + warp);
+  double* red_mine = red + cut.rank * (kCsWarps / 2) + warp;
+  constexpr int kShareBytes = 8 * Cfg::warps;
 
   // seed (pipg.hpp:213-230)
   double zx[RT::nxc], zu[RT::nuc], vcd[RT::nrow];
@@ -463,23 +564,40 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
     acc0 = fma(vn, vn, acc0);
   }
   acc0 = warp_sum(t.auth ? acc0 : 0.0);
-  if (lane == 0) red[warp] = acc0;
+  if (lane == 0) {
+    if constexpr (kCluster) push_f64(rred, acc0, port.norm_box(0));
+    red_mine[0] = acc0;
+  }
   block_barrier();
+  if constexpr (kCluster) port.recv_norm(0, kShareBytes);
   auto norm_sq = [&](int parity) {
-    const double2* p = reinterpret_cast<const double2*>(red + parity * kCsWarps);
-    const double2 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
-    const double lo = ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
-    if (Cfg::warps <= 8) return lo;
-    const double2 q4 = p[4], q5 = p[5], q6 = p[6], q7 = p[7];
-    return lo + (((q4.x + q4.y) + (q5.x + q5.y)) + ((q6.x + q6.y) + (q7.x + q7.y)));
+    if constexpr (kCluster) {
+      // (the address is a register: derived from the generic pointer it costs a special-register
+      // read of the CTA's cluster rank on the trip's critical path)
+      const unsigned at = port.red + 8u * (unsigned)(parity * kCsWarps);
+      double2 q[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(q[e].x), "=d"(q[e].y) : "r"(at + 16u * e));
+      const double lo = ((q[0].x + q[0].y) + (q[1].x + q[1].y)) + ((q[2].x + q[2].y) + (q[3].x + q[3].y));
+      return lo + (((q[4].x + q[4].y) + (q[5].x + q[5].y)) + ((q[6].x + q[6].y) + (q[7].x + q[7].y)));
+    } else {
+      const double2* p = reinterpret_cast<const double2*>(red + parity * kCsWarps);
+      const double2 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
+      const double lo = ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
+      if (Cfg::warps <= 8) return lo;
+      const double2 q4 = p[4], q5 = p[5], q6 = p[6], q7 = p[7];
+      return lo + (((q4.x + q4.y) + (q5.x + q5.y)) + ((q6.x + q6.y) + (q7.x + q7.y)));
+    }
   };
   double ss = norm_sq(0);  // squared norm of the current iterate
   if (ss == 0.0) {  // pipg.hpp:224-225
-    if (tid == 0) {
+    if (tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSeedZero;
       a.sigma[b] = 0.0;
       if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
     }
+    if constexpr (kCluster) cg::this_cluster().sync();
     return;
   }
   // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test, whose
@@ -509,9 +627,9 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
 #pragma unroll
     for (int q = 0; q < RT::nxc; ++q) {
       const int slot = xn_slot<K>(RT::xc(q));
-      if (slot >= 0 && t.auth) xn_s[slot * S] = zx[q];
+      if (slot >= 0 && t.pubx) xn_s[slot * S] = zx[q];
     }
-    forward_publish<K, R, S, true>(op, zx, zu, zun, part_s, t.auth, own);
+    forward_publish<K, R, S, !kCluster>(op, zx, zu, zun, part_s, t.auth, own);  // (cluster: the leaner code)
   };
   forward_map();
 
@@ -519,6 +637,15 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   bool done = false;
   for (int j = 1; j <= a.j_max; ++j) {
     block_barrier();
+    // The partner's norm shares of trip j - 1 have normally arrived by now (they were sent in front
+    // of its forward products): the mailbox is armed here, tested once behind the gathers -- which
+    // do not need the shares and overlap the test -- and polled only if that test fails.
+    unsigned norm_at = 0, norm_par = 0;
+    if constexpr (kCluster) {
+      norm_at = port.box + 8u + 8u * (unsigned)((j - 1) & 1);
+      norm_par = (unsigned)((j - 1) >> 1);
+      mbar_expect_pred(j > 1 ? port.armer : 0u, norm_at, kShareBytes);  // (the seed's were received above)
+    }
     // ---- rows: sum of the partials, scale by 1 / sigma
     double s[RT::nrow];
     gather_rows<K, R, S>(own, part_s, s);
@@ -527,6 +654,9 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
       const int i = RT::row(r);
       const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
       s[r] = (s[r] - xn) + vcd[r];
+    }
+    if constexpr (kCluster) {
+      if (!mbar_test_at(norm_at, norm_par)) mbar_wait_at(norm_at, norm_par);
     }
     {  // stopping test of trip j-1 (pipg.hpp:277-289); j = 1: the seed against NaN, never met
       ss = norm_sq((j - 1) & 1);
@@ -545,19 +675,27 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
     double acc_d = 0.0;
 #pragma unroll
     for (int r = 0; r < RT::nrow; ++r) {
-      const double p = s[r] * inv;
-      if (t.ival) phi_s[RT::row(r) * S] = p;
-      vcd[r] = 2.0 * p;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
-      acc_d = fma(vcd[r], p, acc_d);
+      s[r] *= inv;
+      if (t.ival) phi_s[RT::row(r) * S] = s[r];
+      vcd[r] = 2.0 * s[r];  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
+      acc_d = fma(vcd[r], s[r], acc_d);
     }
     if (kJy >= 0) {
       if (t.ival) th_s[0] = dy * inv;
     }
+    if constexpr (kCluster) {  // one divergent block for all the remote stores of the boundary lane
+      if (pusher) {
+#pragma unroll
+        for (int r = 0; r < RT::nrow; ++r) push_f64(rphi + 8u * (unsigned)(RT::row(r) * S), s[r], port.rbox);
+        if (kJy >= 0) push_f64(rth, dy * inv, port.rbox);
+      }
+    }
     block_barrier();
+    if constexpr (kCluster) port.recv_phi(j - 1);
     // ---- adjoint map (pipg.hpp:247-275)
     {
       double gx[RT::nxc], gm[RT::nuc], gp[RT::nuc];
-      transposed<K, R, S>(op, phi_s, gx, gm, gp);
+      transposed<K, R, S, kCluster>(op, phi_s, gx, gm, gp);
 #pragma unroll
       for (int q = 0; q < RT::nxc; ++q) {
         const int c = RT::xc(q);
@@ -580,29 +718,34 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
 #pragma unroll
     for (int q = 0; q < RT::nuc; ++q) az1 = fma(zu[q], zu[q], az1);
     const double share = warp_sum(t.auth ? az0 + az1 : 0.0);
+    if constexpr (kCluster) {  // in flight while the forward products run
+      push_f64_pred(lane == 0, rred + 8u * (unsigned)((j & 1) * kCsWarps), share, port.norm_box(j));
+    }
     forward_map();  // of trip j + 1
-    if (lane == 0) red[(j & 1) * kCsWarps + warp] = share;
+    if (lane == 0) red_mine[(j & 1) * kCsWarps] = share;
   }
   if (!done) {  // j_max trips without meeting the tolerance
     block_barrier();
+    if constexpr (kCluster) port.recv_norm(a.j_max, kShareBytes);
     ss = norm_sq(a.j_max & 1);
   }
-  if (tid == 0) {
+  if (tid == 0 && cut.rank == 0) {
     a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss);
     if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
   }
+  if constexpr (kCluster) cg::this_cluster().sync();  // nobody leaves while the partner may still store here
 }
 
-template <int K, int kHalves>
+template <int K, int kHalves, bool kCluster>
 __global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
-  const int b = blockIdx.x;
-  if (a.active && !a.active[b]) return;
+  const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
+  if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   switch ((threadIdx.x >> 5) % K) {
-    case 0: power_role<4, 0, kHalves>(a, sm, b, handled); break;
-    case 1: power_role<4, 1, kHalves>(a, sm, b, handled); break;
-    case 2: power_role<4, 2, kHalves>(a, sm, b, handled); break;
-    default: power_role<4, 3, kHalves>(a, sm, b, handled); break;
+    case 0: power_role<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
+    case 1: power_role<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
+    case 2: power_role<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
+    default: power_role<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
   }
 }
 
@@ -946,11 +1089,14 @@ __global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_kernel(
 bool solver_cs_supports(const SubShape& s, bool has_a_plus) {
   return solver_fast_supports(s, has_a_plus) && s.n <= kCsMaxNodes;
 }
+bool solver_cs_power_supports(const SubShape& s, bool has_a_plus) {
+  return solver_fast_supports(s, has_a_plus) && s.n <= kCsClusterMaxNodes;
+}
 
 namespace {
-template <int K, int kHalves>
+template <int K, int kHalves, bool kCluster = false>
 cudaError_t opt_in_power() {
-  return cudaFuncSetAttribute(power_cs_kernel<K, kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(power_cs_kernel<K, kHalves, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(double) * cs_layout<K, kHalves>(false).total));
 }
 template <int kHalves>
@@ -960,7 +1106,23 @@ cudaError_t opt_in_pipg() {
 }
 template <int K, int kHalves>
 void launch_power(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
-  power_cs_kernel<K, kHalves><<<a.batch, CsCfg<K, kHalves>::threads, sizeof(double) * cs_layout<K, kHalves>(false).total, stream>>>(a, handled);
+  power_cs_kernel<K, kHalves, false><<<a.batch, CsCfg<K, kHalves>::threads, sizeof(double) * cs_layout<K, kHalves>(false).total, stream>>>(a, handled);
+}
+/// One instance over a cluster of two CTAs (kCsMaxNodes < n <= kCsClusterMaxNodes).
+cudaError_t launch_power_cluster(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2u * (unsigned)a.batch);
+  cfg.blockDim = dim3(CsCfg<4, 2>::threads);
+  cfg.dynamicSmemBytes = sizeof(double) * cs_layout<4, 2>(false).total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, power_cs_kernel<4, 2, true>, a, handled);
 }
 }  // namespace
 
@@ -971,12 +1133,14 @@ size_t pipg_cs_smem(const SubShape& s) {
 cudaError_t configure_solver_cs(const SubShape&) {
   cudaError_t e = opt_in_power<4, 1>();
   if (e == cudaSuccess) e = opt_in_power<4, 2>();
+  if (e == cudaSuccess) e = opt_in_power<4, 2, true>();
   if (e == cudaSuccess) e = opt_in_pipg<1>();
   if (e == cudaSuccess) e = opt_in_pipg<2>();
   return e;
 }
 
 cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n > kCsMaxNodes) return launch_power_cluster(a, handled, stream);
   if (a.shape.n <= CsCfg<4, 1>::cap) launch_power<4, 1>(a, handled, stream);
   else launch_power<4, 2>(a, handled, stream);
   return cudaGetLastError();

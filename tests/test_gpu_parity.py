@@ -825,7 +825,7 @@ def test_config5_n100_cluster_and_generic_kernels(ptor, path):
         check_scp_against_oracle(sc, out, b, ref, ref["power_trips"])
 
 
-@pytest.mark.parametrize("nodes", [2, 3, 30, 31, 32, 50, 51, 52, 61, 62, 64, 77, 102, 103])
+@pytest.mark.parametrize("nodes", [2, 3, 30, 31, 32, 50, 51, 52, 61, 62, 63, 64, 77, 102, 103])
 def test_scp_solve_node_count_edges(ptor, nodes):
     """Node counts at the edges of the register-resident kernels: the minimum grid, the last count
     the column-sparse kernels hold in one warp per role (31) and its neighbours (30; 32: two warps

@@ -356,9 +356,10 @@ def other_configs(device_index, fp64_peak):
         st = s.scp_stage_times()
     out["config5_shape_296xN100"] = {
         "solves_per_s": B / (st["graph_total"] * 1e-3), "graph_ms": st["graph_total"],
+        "stages_ms": {k: st[k] for k in ("linearize", "power_iteration", "pipg")},
         "power_trips_mean": float(res["power_trips"].sum(axis=1).mean()),
-        "what": "full SCP solves at N=100 on one GPU (2-CTA cluster per instance, two waves), device time of "
-                "the graph"}
+        "what": "full SCP solves at N=100 on one GPU (column-sparse kernels, one instance over a 2-CTA cluster: "
+                "74 instances at a time, four waves), device time of the graph"}
     # ---- the headline configuration on the dense register-resident kernels alone (round-1 path), for
     #      the gain of the column-sparse kernels in the same run
     n, B = 50, 4096

@@ -249,11 +249,6 @@ bool use_cs_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plu
   return (h->solver_path == PTOPT_SOLVER_AUTO || h->solver_path == PTOPT_SOLVER_FAST_THROUGHPUT) &&
          solver_cs_supports(s, has_a_plus);
 }
-/// The column-sparse power iteration reaches further (a cluster of two CTAs above kCsMaxNodes).
-bool use_cs_power(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plus) {
-  return (h->solver_path == PTOPT_SOLVER_AUTO || h->solver_path == PTOPT_SOLVER_FAST_THROUGHPUT) &&
-         solver_cs_power_supports(s, has_a_plus);
-}
 
 /// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
 /// handle asks for it (and the node count allows it).  Measured on B200 it loses to one CTA per
@@ -275,7 +270,7 @@ int configure_solver(ptopt_cuda_handle* h, const SubShape& s, bool fast) {
   if (fast) {
     PT_TRY(check_smem(h, pipg_fast_smem(s, false)));
     PT_CUDA(configure_solver_fast(s));
-    if (solver_cs_power_supports(s, false)) {
+    if (solver_cs_supports(s, false)) {
       PT_TRY(check_smem(h, pipg_cs_smem(s)));
       PT_CUDA(configure_solver_cs(s));
     }
@@ -294,7 +289,7 @@ int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  if (fast && use_cs_power(h, a.shape, a.sp.A_plus != nullptr)) {
+  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr)) {
     unsigned char* handled = nullptr;
     PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
     PT_CUDA(launch_power_cs(a, handled, h->stream));
@@ -501,7 +496,6 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
   const int lat = latency_ranks(h, h->rocket_shape, false, batch);
   const bool cs = !lat && fast && use_cs_solver(h, h->rocket_shape, false);
-  const bool cs_power = !lat && fast && use_cs_power(h, h->rocket_shape, false);
   unsigned char* handled = h->buf[S_HANDLED].as<unsigned char>();
   PowerArgs pa_rest = pa;
   PipgArgs ga_rest = ga;
@@ -514,7 +508,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 1;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    if (cs_power) {  // column-sparse kernels, then the dense ones on whatever they did not take
+    if (cs) {  // column-sparse kernels, then the dense ones on whatever they did not take
       PT_CUDA(launch_power_cs(pa, handled, h->stream));
       PT_CUDA(launch_power_fast(pa_rest, false, h->stream));
       kernels += 1;

@@ -29,6 +29,12 @@
 //     boundary between the two warps of a role is covered by one redundantly computed halo node on
 //     either side (lane 31 of the first warp repeats node 31, lane 0 of the second warp node 30),
 //     so no value ever has to cross warps in the middle of a phase.
+//   * above kCsMaxNodes nodes (up to kCsClusterMaxNodes) one instance runs over a CLUSTER of two
+//     CTAs with the same trick across the cut: rank 0 carries a redundant copy of rank 1's first
+//     node, rank 1 a copy of rank 0's last node (as the source of B+^T phi), and the only values
+//     that cross are the duals of the two boundary intervals (and, in the power iteration, every
+//     warp's share of the squared norm), stored into the partner's shared memory through mailboxes
+//     (struct Cut, struct Port; mailbox.cuh).
 // Two block barriers per iteration / trip, as in solver_fast.cu, but 0.4x the shared-memory
 // wavefronts, 0.72x the FMAs and 360 / 400 instead of 397 / 540 instructions per warp and trip /
 // iteration: 1 850 / 2 400 clk against 2 750 / 3 160 (B200, N = 50).  The four role bodies of a loop
@@ -158,7 +164,7 @@ struct SnapCs {
 };
 template <int K, int kHalves>
 __host__ __device__ constexpr SnapCs snap_cs() {
-  constexpr int n = CsCfg<K, kHalves>::cap;
+  constexpr int n = CsCfg<K, kHalves>::cap + 1;  // (+ 1: rank 0's copy of the partner's first node)
   SnapCs s{};
   int o = 0;
   s.x = o; o += n * kNX;
@@ -205,7 +211,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 /// The part of the horizon a CTA works on.  Without a cluster: everything.  In a cluster of two
-/// (62..kCsClusterMaxNodes nodes, power iteration) rank 0 owns nodes [0, c), c = ceil(n / 2), and
+/// (62..kCsClusterMaxNodes nodes) rank 0 owns nodes [0, c), c = ceil(n / 2), and
 /// carries a redundant copy of node c behind its last node; rank 1 owns [c, n) and carries a copy of
 /// node c - 1 in front of its first one (only as the source of B+^T phi of interval c - 1).  The
 /// duals of the two boundary intervals are the only values that cross the cut (see Port).
@@ -755,13 +761,13 @@ __global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel
 /// stopping_custom(cur, prev) and the divergence test of pipg.hpp:475-487 over two snapshots: 0 =
 /// go on, 1 = converged, 2 = a non-finite primal or dual entry.  One copy for the four roles (the
 /// loop bodies are role-specific and have to share the instruction cache with as little as possible).
-template <int kHalves>
-__device__ __noinline__ int pipg_check(const double* cur, const double* prev, int n, double* red, double eps_abs,
-                                       double eps_rel) {
+template <int kHalves, bool kCluster>
+__device__ __noinline__ int pipg_check(const double* cur, const double* prev, int l0, int nn, int mm, double* red,
+                                       double eps_abs, double eps_rel) {
+  // l0: first owned local node, nn / mm: owned nodes / intervals of this CTA
   constexpr SnapCs SN = snap_cs<4, kHalves>();
   constexpr int T = CsCfg<4, kHalves>::threads;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = n - 1;
   double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, badv = 0.0;
   auto scan = [&](int off, int count, bool dual, bool finite_checked) {
 #pragma unroll 1
@@ -779,12 +785,12 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
       if (finite_checked && !pt_finite(c)) badv = 1.0;
     }
   };
-  scan(SN.x, n * kNX, false, true);
-  scan(SN.u, n * kNU, false, true);
-  scan(SN.vp, m * kNX, false, false);
-  scan(SN.vn, m * kNX, false, false);
-  scan(SN.ph, m * kNX, true, true);
-  scan(SN.th, m, true, false);
+  scan(SN.x + l0 * kNX, nn * kNX, false, true);
+  scan(SN.u + l0 * kNU, nn * kNU, false, true);
+  scan(SN.vp + l0 * kNX, mm * kNX, false, false);
+  scan(SN.vn + l0 * kNX, mm * kNX, false, false);
+  scan(SN.ph + l0 * kNX, mm * kNX, true, true);
+  scan(SN.th + l0, mm, true, false);
   z_cur = warp_max_nn(z_cur); z_prev = warp_max_nn(z_prev); z_del = warp_max_nn(z_del);
   r_cur = warp_max_nn(r_cur); r_prev = warp_max_nn(r_prev); r_del = warp_max_nn(r_del);
   badv = warp_max_nn(badv);
@@ -802,12 +808,25 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
     for (int w = 0; w < CsCfg<4, kHalves>::warps; ++w) mx = max_nn(mx, red[w * 8 + q]);
     v[q] = mx;
   }
-  block_barrier();  // red and the snapshots are rewritten later
+  if constexpr (kCluster) {  // the partner's maxima (a stopping test is rare: two cluster barriers)
+    double* mine = red + Port::kBoxAt + 8;  // [7], behind the mailboxes and the pattern flag
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) mine[q] = v[q];
+    }
+    cg::this_cluster().sync();
+    const double* theirs = cg::this_cluster().map_shared_rank(mine, (int)cg::this_cluster().block_rank() ^ 1);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) v[q] = max_nn(v[q], theirs[q]);
+    cg::this_cluster().sync();  // red and the snapshots are rewritten later
+  } else {
+    block_barrier();  // red and the snapshots are rewritten later
+  }
   if (v[6] > 0.0) return 2;
   return (v[2] <= eps_abs + eps_rel * max_nn(v[0], v[1]) && v[5] <= eps_abs + eps_rel * max_nn(v[3], v[4])) ? 1 : 0;
 }
 
-template <int K, int R, int kHalves>
+template <int K, int R, int kHalves, bool kCluster>
 __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
   using RT = RoleT<K, R>;
   using Cfg = CsCfg<K, kHalves>;
@@ -817,17 +836,22 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   constexpr SnapCs SN = snap_cs<K, kHalves>();
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
-  const Lane t = make_lane<kHalves>(n, half, lane);
+  const Cut cut = make_cut<kCluster>(n);
+  const Lane t = make_lane<kHalves>(cut, n, half, lane);
+  const int tl = t.slot - 1;  // local node: the snapshots are indexed by it
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
 
   OpCols<K, R> op;
-  const bool have = t.k < m;  // halo copies load their node's block too
-  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
-  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
-    if (tid == 0) handled[b] = 0;
+  bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (t.have ? t.k : 0), t.have, op);
+  bad = __syncthreads_or(bad ? 1 : 0) != 0;
+  Port port{};
+  if constexpr (kCluster) bad = open_port(port, sm, sm + L.red, cut, t, bad);
+  if (bad) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0 && cut.rank == 0) handled[b] = 0;
+    if constexpr (kCluster) cg::this_cluster().sync();  // the partner reads this CTA's verdict
     return;
   }
-  if (tid == 0) handled[b] = 1;
+  if (tid == 0 && cut.rank == 0) handled[b] = 1;
 
   double* phi_s = sm + L.phi + t.slot;    // extrapolated dynamics dual, row i at + i * S; interval k-1 at -1
   double* th_s = sm + L.th + t.slot;      // extrapolated relaxation dual
@@ -846,7 +870,8 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
 
   const size_t gx = (size_t)b * n * kNX, gu = (size_t)b * n * kNU, gm_ = (size_t)b * m * kNX, gt = (size_t)b * m;
   const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
-  if (tid < kNX) sm[L.ecost + tid * S + n] = a.shape.w_cost * a.shape.e_cost[tid];  // slot of node n - 1
+  if (tid < kNX && n - 1 >= cut.lo && n - 1 < cut.hip)  // slot of node n - 1, in the CTA that holds it
+    sm[L.ecost + tid * S + n - cut.base] = a.shape.w_cost * a.shape.e_cost[tid];
   if (tid == 0) {
     // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
     for (int i = 0; i < a.shape.n_init_fix; ++i) {
@@ -858,26 +883,36 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
       final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
     }
   }
+  // the nodes / intervals this CTA holds a slot for: local 0 .. kLoc - 1
+  constexpr int kLoc = Cfg::cap + 1;
   for (int e = tid; e < NM; e += T) {  // [interval][row] -> [row][slot]
-    const int k = e / kNX, i = e - k * kNX;
-    sm[L.wv + i * S + k + 1] = a.sp.w[gm_ + e];
+    const int k = e / kNX, i = e - k * kNX, l = k - cut.base;
+    if (l >= 0 && l < kLoc) sm[L.wv + i * S + l + 1] = a.sp.w[gm_ + e];
   }
-  for (int e = tid; e < m; e += T) sm[L.eps + e + 1] = a.sp.eps_relax[gt + e];
+  for (int e = tid; e < m; e += T) {
+    const int l = e - cut.base;
+    if (l >= 0 && l < kLoc) sm[L.eps + l + 1] = a.sp.eps_relax[gt + e];
+  }
 #pragma unroll
   for (int q = 0; q < RT::nuc; ++q) {  // box of the own control entries (pipg.hpp:418-419); unbounded where there is no node
     if (t.halo) continue;  // the owner's warp fills the slot; the halo copy reads it behind the barrier
-    bnd_s[(2 * q) * S] = t.auth ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
-    bnd_s[(2 * q + 1) * S] = t.auth ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
+    bnd_s[(2 * q) * S] = t.pubx ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
+    bnd_s[(2 * q + 1) * S] = t.pubx ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
   }
   // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
-  for (int e = tid; e < NXn; e += T) snap0[SN.x + e] = a.ws.x[gx + e];
-  for (int e = tid; e < NUn; e += T) snap0[SN.u + e] = a.ws.u[gu + e];
-  for (int e = tid; e < NM; e += T) {
-    snap0[SN.vp + e] = a.ws.vc_pos[gm_ + e];
-    snap0[SN.vn + e] = a.ws.vc_neg[gm_ + e];
-    snap0[SN.ph + e] = a.ws.dyn_dual[gm_ + e];
-  }
-  for (int e = tid; e < m; e += T) snap0[SN.th + e] = a.ws.relax_dual[gt + e];
+  const int sx = cut.base * kNX, su = cut.base * kNU;  // global index - this = local index
+  for (int e = tid; e < NXn; e += T)
+    if (e >= sx && e < sx + kLoc * kNX) snap0[SN.x + e - sx] = a.ws.x[gx + e];
+  for (int e = tid; e < NUn; e += T)
+    if (e >= su && e < su + kLoc * kNU) snap0[SN.u + e - su] = a.ws.u[gu + e];
+  for (int e = tid; e < NM; e += T)
+    if (e >= sx && e < sx + kLoc * kNX) {
+      snap0[SN.vp + e - sx] = a.ws.vc_pos[gm_ + e];
+      snap0[SN.vn + e - sx] = a.ws.vc_neg[gm_ + e];
+      snap0[SN.ph + e - sx] = a.ws.dyn_dual[gm_ + e];
+    }
+  for (int e = tid; e < m; e += T)
+    if (e >= cut.base && e < cut.base + kLoc) snap0[SN.th + e - cut.base] = a.ws.relax_dual[gt + e];
   block_barrier();
 
   // boundary columns of this thread (pipg.hpp:408-413): bit q set when own x column q is assigned
@@ -897,21 +932,35 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   // owner-private extrapolated copies
   double xe[RT::nxc], ue[RT::nuc], vpe[RT::nrow], vne[RT::nrow], phe[RT::nrow], the = 0.0;
 #pragma unroll
-  for (int q = 0; q < RT::nxc; ++q) xe[q] = t.primal ? snap0[SN.x + t.k * kNX + RT::xc(q)] : 0.0;
+  for (int q = 0; q < RT::nxc; ++q) xe[q] = t.primal ? snap0[SN.x + tl * kNX + RT::xc(q)] : 0.0;
 #pragma unroll
-  for (int q = 0; q < RT::nuc; ++q) ue[q] = t.primal ? snap0[SN.u + t.k * kNU + RT::uc(q)] : 0.0;
+  for (int q = 0; q < RT::nuc; ++q) ue[q] = t.primal ? snap0[SN.u + tl * kNU + RT::uc(q)] : 0.0;
 #pragma unroll
   for (int r = 0; r < RT::nrow; ++r) {
-    const int e = t.k * kNX + RT::row(r);
+    const int e = tl * kNX + RT::row(r);
     vpe[r] = t.ival ? snap0[SN.vp + e] : 0.0;
     vne[r] = t.ival ? snap0[SN.vn + e] : 0.0;
     phe[r] = t.ival ? snap0[SN.ph + e] : 0.0;
     if (t.auth) phi_s[RT::row(r) * S] = phe[r];
   }
   if (R == 0) {
-    the = t.ival ? snap0[SN.th + t.k] : 0.0;
+    the = t.ival ? snap0[SN.th + tl] : 0.0;
     if (t.auth) th_s[0] = the;
   }
+  // cluster: the owners of the boundary interval store its (extrapolated) duals in the partner's
+  // slots as well, after the warm start (phase 0) and after every iteration j (phase j)
+  const bool pusher = kCluster && t.auth && t.k == (cut.rank == 0 ? cut.hi - 1 : cut.lo);
+  const int pslot = cut.rank == 0 ? 1 : cut.lo + 1;  // slot of that interval over there
+  const unsigned rphi = port.rsm + 8u * (unsigned)(L.phi + pslot), rth = port.rsm + 8u * (unsigned)(L.th + pslot);
+  auto push_duals = [&]() {
+    if (pusher) {
+#pragma unroll
+      for (int r = 0; r < RT::nrow; ++r) push_f64(rphi + 8u * (unsigned)(RT::row(r) * S), phe[r], port.rbox);
+      if (R == 0) push_f64(rth, the, port.rbox);
+    }
+  };
+  if constexpr (kCluster) push_duals();
+  int phase = 0;  // of the duals' mailbox
 
   const double sigma = a.sigma[b];
   const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
@@ -923,6 +972,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   // One iteration.  kStore additionally writes the new *_cur values of every owner into `snap`.
   auto iteration = [&](auto store_tag, double* snap) {
     constexpr bool kStore = decltype(store_tag)::value;
+    if constexpr (kCluster) port.recv_phi(phase++);
     // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
     double rx[RT::nxc], ru[RT::nuc];
     {
@@ -940,7 +990,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         double xn = x0 + -alpha * grad;
         if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;  // (measured: faster than unconditional)
         rx[q] = fma(2.0, xn, -x0);
-        if (kStore && t.auth) snap[SN.x + t.k * kNX + c] = xn;
+        if (kStore && t.auth) snap[SN.x + tl * kNX + c] = xn;
         xe[q] = extrapolate(x0, xn);
       }
 #pragma unroll
@@ -954,7 +1004,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
         // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
         un = clamp_box(lo, hi, un);
         ru[q] = fma(2.0, un, -u0);
-        if (kStore && t.auth) snap[SN.u + t.k * kNU + RT::uc(q)] = un;
+        if (kStore && t.auth) snap[SN.u + tl * kNU + RT::uc(q)] = un;
         ue[q] = extrapolate(u0, un);
       }
     }
@@ -973,7 +1023,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
 #pragma unroll
     for (int q = 0; q < RT::nxc; ++q) {
       const int slot = xn_slot<K>(RT::xc(q));
-      if (slot >= 0 && t.auth) xn_s[slot * S] = rx[q];
+      if (slot >= 0 && t.pubx) xn_s[slot * S] = rx[q];
     }
     double own[RT::nrow];
     forward_publish<K, R, S, false>(op, rx, ru, run, part_s, t.auth, own);
@@ -993,7 +1043,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
       resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv_s[i * S];
       const double pn = p0 + beta * resid;
       if (kStore && t.ival) {
-        const int e = t.k * kNX + i;
+        const int e = tl * kNX + i;
         snap[SN.vp + e] = vp;
         snap[SN.vn + e] = vn;
         snap[SN.ph + e] = pn;
@@ -1007,10 +1057,11 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     }
     if (R == 0) {
       const double tn = clip0(the + beta * (drift - eps_s[0]));
-      if (kStore && t.ival) snap[SN.th + t.k] = tn;
+      if (kStore && t.ival) snap[SN.th + tl] = tn;
       the = extrapolate(the, tn);
       if (t.ival) th_s[0] = the;
     }
+    if constexpr (kCluster) push_duals();
     block_barrier();
   };
 
@@ -1032,8 +1083,9 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     }
     iters = j;
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
-      const int verdict = pipg_check<kHalves>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total, n, red,
-                                              a.eps_abs, a.eps_rel);
+      const int verdict = pipg_check<kHalves, kCluster>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total,
+                                                        cut.lo - cut.base, cut.hi - cut.lo,
+                                                        (cut.hi < m ? cut.hi : m) - cut.lo, red, a.eps_abs, a.eps_rel);
       if (verdict == 2) {
         diverged = true;
         break;
@@ -1045,8 +1097,12 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     }
   }
 
+  if constexpr (kCluster) {  // the duals sent after the last iteration: nothing may be in flight at the exit
+    port.recv_phi(phase);
+    cg::this_cluster().sync();
+  }
   if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
-    if (tid == 0) {
+    if (tid == 0 && cut.rank == 0) {
       if (a.status) a.status[b] = kStSolverDiverged;
       if (a.fail_index) a.fail_index[b] = iters;
       if (a.iterations) a.iterations[b] = iters;
@@ -1057,39 +1113,37 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
   }
   // solution = the *_cur groups, pipg.hpp:490-495 (every iteration ends with a barrier)
   const double* cur = snap0 + cur_set * SN.total;
-  for (int e = tid; e < NXn; e += T) a.ws.x[gx + e] = cur[SN.x + e];
-  for (int e = tid; e < NUn; e += T) a.ws.u[gu + e] = cur[SN.u + e];
-  for (int e = tid; e < NM; e += T) {
-    a.ws.vc_pos[gm_ + e] = cur[SN.vp + e];
-    a.ws.vc_neg[gm_ + e] = cur[SN.vn + e];
-    a.ws.dyn_dual[gm_ + e] = cur[SN.ph + e];
+  const int hi_m = cut.hi < m ? cut.hi : m;  // owned nodes [lo, hi), owned intervals [lo, hi_m)
+  for (int e = tid + cut.lo * kNX; e < cut.hi * kNX; e += T) a.ws.x[gx + e] = cur[SN.x + e - sx];
+  for (int e = tid + cut.lo * kNU; e < cut.hi * kNU; e += T) a.ws.u[gu + e] = cur[SN.u + e - su];
+  for (int e = tid + cut.lo * kNX; e < hi_m * kNX; e += T) {
+    a.ws.vc_pos[gm_ + e] = cur[SN.vp + e - sx];
+    a.ws.vc_neg[gm_ + e] = cur[SN.vn + e - sx];
+    a.ws.dyn_dual[gm_ + e] = cur[SN.ph + e - sx];
   }
-  for (int e = tid; e < m; e += T) a.ws.relax_dual[gt + e] = cur[SN.th + e];
-  if (tid == 0) {
+  for (int e = tid + cut.lo; e < hi_m; e += T) a.ws.relax_dual[gt + e] = cur[SN.th + e - cut.base];
+  if (tid == 0 && cut.rank == 0) {
     if (a.iterations) a.iterations[b] = iters;
     if (a.converged) a.converged[b] = converged ? 1 : 0;
   }
 }
 
-template <int kHalves>
+template <int kHalves, bool kCluster>
 __global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
-  const int b = blockIdx.x;
-  if (a.active && !a.active[b]) return;
+  const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
+  if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   switch ((threadIdx.x >> 5) & 3) {
-    case 0: pipg_role<4, 0, kHalves>(a, sm, b, handled); break;
-    case 1: pipg_role<4, 1, kHalves>(a, sm, b, handled); break;
-    case 2: pipg_role<4, 2, kHalves>(a, sm, b, handled); break;
-    default: pipg_role<4, 3, kHalves>(a, sm, b, handled); break;
+    case 0: pipg_role<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
+    case 1: pipg_role<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
+    case 2: pipg_role<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
+    default: pipg_role<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
   }
 }
 
 }  // namespace
 
 bool solver_cs_supports(const SubShape& s, bool has_a_plus) {
-  return solver_fast_supports(s, has_a_plus) && s.n <= kCsMaxNodes;
-}
-bool solver_cs_power_supports(const SubShape& s, bool has_a_plus) {
   return solver_fast_supports(s, has_a_plus) && s.n <= kCsClusterMaxNodes;
 }
 
@@ -1099,9 +1153,9 @@ cudaError_t opt_in_power() {
   return cudaFuncSetAttribute(power_cs_kernel<K, kHalves, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(double) * cs_layout<K, kHalves>(false).total));
 }
-template <int kHalves>
+template <int kHalves, bool kCluster = false>
 cudaError_t opt_in_pipg() {
-  return cudaFuncSetAttribute(pipg_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(pipg_cs_kernel<kHalves, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(double) * cs_layout<4, kHalves>(true).total));
 }
 template <int K, int kHalves>
@@ -1136,6 +1190,7 @@ cudaError_t configure_solver_cs(const SubShape&) {
   if (e == cudaSuccess) e = opt_in_power<4, 2, true>();
   if (e == cudaSuccess) e = opt_in_pipg<1>();
   if (e == cudaSuccess) e = opt_in_pipg<2>();
+  if (e == cudaSuccess) e = opt_in_pipg<2, true>();
   return e;
 }
 
@@ -1147,10 +1202,25 @@ cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStre
 }
 
 cudaError_t launch_pipg_cs(const PipgArgs& a, unsigned char* handled, cudaStream_t stream) {
+  if (a.shape.n > kCsMaxNodes) {  // one instance over a cluster of two CTAs
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2u * (unsigned)a.batch);
+    cfg.blockDim = dim3(CsCfg<4, 2>::threads);
+    cfg.dynamicSmemBytes = sizeof(double) * cs_layout<4, 2>(true).total;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, pipg_cs_kernel<2, true>, a, handled);
+  }
   if (a.shape.n <= CsCfg<4, 1>::cap) {
-    pipg_cs_kernel<1><<<a.batch, CsCfg<4, 1>::threads, sizeof(double) * cs_layout<4, 1>(true).total, stream>>>(a, handled);
+    pipg_cs_kernel<1, false><<<a.batch, CsCfg<4, 1>::threads, sizeof(double) * cs_layout<4, 1>(true).total, stream>>>(a, handled);
   } else {
-    pipg_cs_kernel<2><<<a.batch, CsCfg<4, 2>::threads, sizeof(double) * cs_layout<4, 2>(true).total, stream>>>(a, handled);
+    pipg_cs_kernel<2, false><<<a.batch, CsCfg<4, 2>::threads, sizeof(double) * cs_layout<4, 2>(true).total, stream>>>(a, handled);
   }
   return cudaGetLastError();
 }

@@ -368,22 +368,25 @@ def test_pipg_rocket_2000_iterations(solver15, ptor):
         assert np.abs(ws[f][0] - getattr(ref, f)).max() <= TOL_ITER, f
 
 
-def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor):
+@pytest.mark.parametrize("nodes,where", [(15, 3), (100, 3), (100, 80)])
+def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor, nodes, where):
     """The column-sparse kernels check the zero pattern of every instance while they load it.  A
     batch of three rocket subproblems whose middle one carries an entry outside the pattern (rate
     row, position column: never produced by the model) and whose last one a NaN there: under
     'fast' the first instance is solved by the column-sparse kernels, the other two by the dense
-    kernels behind them -- all three as the CPU oracle solves them."""
+    kernels behind them -- all three as the CPU oracle solves them.  At N=100 an instance is shared
+    by a cluster of two CTAs and the foreign entry sits in the half of rank 0 (interval 3) or of
+    rank 1 (interval 80): the CTA that does not see it has to leave with its partner."""
     from paper_2404_18034_b200.binding import Solver
 
-    sc = scenario.default_scenario(15)
+    sc = scenario.default_scenario(nodes)
     d, shape, sub = rocket_subproblem(sc, ptor, 1)
     n, m = d.nodes, d.nodes - 1
     subs = [sub]
     for bad in (0.37, np.nan):
         other = SubArrays(**{f: (None if getattr(sub, f) is None else getattr(sub, f).copy())
                              for f in sub.FIELDS})
-        other.A_minus[3, 11, 2] = bad
+        other.A_minus[where, 11, 2] = bad
         subs.append(other)
 
     def stack(items):
@@ -806,7 +809,8 @@ def test_config4_scp_batch4096_n50_properties():
 @pytest.mark.parametrize("path", ["fast", "generic", "latency"])
 def test_config5_n100_cluster_and_generic_kernels(ptor, path):
     """BASELINE config 5 shape (N=100): above the single-CTA node limit, so each instance is split
-    over a two-CTA cluster ('fast'); the shape-generic kernels serve it too ('generic'), and the
+    over a two-CTA cluster ('fast': the column-sparse kernels with a copy of the partner's boundary
+    node on either side of the cut); the shape-generic kernels serve it too ('generic'), and the
     latency mode spreads it over eight CTAs of 12-13 nodes ('latency').  Reduced
     budget with stopping checks, parity with the oracle on three instances."""
     from paper_2404_18034_b200.binding import Solver
@@ -829,11 +833,11 @@ def test_config5_n100_cluster_and_generic_kernels(ptor, path):
 def test_scp_solve_node_count_edges(ptor, nodes):
     """Node counts at the edges of the register-resident kernels: the minimum grid, the last count
     the column-sparse kernels hold in one warp per role (31) and its neighbours (30; 32: two warps
-    per role with a halo lane each), their largest count (61) and the first one that only the
-    dense kernels serve (62), the largest dense single-CTA count (51), the first one that is split
-    over a two-CTA cluster (52), cluster splits with an even / odd node count and no
-    idle threads (64, 77), the largest cluster count (102) and the first one that falls back to
-    the shape-generic kernels (103)."""
+    per role with a halo lane each), their largest single-CTA count (61) and the first ones they
+    split over a two-CTA cluster (62, 63: the copy of the partner's boundary node falls on the
+    halo lanes between the two warps of a role; 64), the largest dense single-CTA count (51) and
+    the first one the dense kernels split (52), an odd cluster split (77), the largest cluster
+    count (102) and the first one that falls back to the shape-generic kernels (103)."""
     from paper_2404_18034_b200.binding import Solver
 
     sc = scenario.default_scenario(nodes)
@@ -949,7 +953,7 @@ def test_config4_full_budget_batch4096_subset_vs_cpu():
 
 @pytest.mark.parametrize("path", ["fast", "latency"])
 def test_config5_n100_full_budget_cluster_kernels_vs_cpu(path):
-    """BASELINE config 5 at the depth it runs: N=100 on the two-CTA cluster kernels ('fast') and on
+    """BASELINE config 5 at the depth it runs: N=100 on the two-CTA cluster kernels ('fast': column-sparse) and on
     the eight-CTA latency-mode clusters ('latency') with the full budget -- the power iteration
     mostly runs to its 10 000-trip cap, 25 x 2500 PIPG iterations, so the mailbox protocols run
     ~300 000 hand-offs per instance -- six dispersed ids against the CPU reference."""

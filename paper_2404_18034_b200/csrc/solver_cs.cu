@@ -35,6 +35,9 @@
 //     that cross are the duals of the two boundary intervals (and, in the power iteration, every
 //     warp's share of the squared norm), stored into the partner's shared memory through mailboxes
 //     (struct Cut, struct Port; mailbox.cuh).
+//     These cluster variants are separate functions (power_role_x, pipg_role_x): the single-CTA
+//     loops sit on a narrow optimum of instruction count and placement, and sharing one templated
+//     body with the cluster code cost the single-CTA PIPG kernel 20 % (2 134 -> 2 556 ms per step).
 // Two block barriers per iteration / trip, as in solver_fast.cu, but 0.4x the shared-memory
 // wavefronts, 0.72x the FMAs and 360 / 400 instead of 397 / 540 instructions per warp and trip /
 // iteration: 1 850 / 2 400 clk against 2 750 / 3 160 (B200, N = 50).  The four role bodies of a loop
@@ -162,9 +165,9 @@ struct CsCfg {
 struct SnapCs {
   int x, u, vp, vn, ph, th, total;
 };
-template <int K, int kHalves>
+template <int K, int kHalves, int kExtra = 0>  // kExtra: rank 0's copy of the partner's first node
 __host__ __device__ constexpr SnapCs snap_cs() {
-  constexpr int n = CsCfg<K, kHalves>::cap + 1;  // (+ 1: rank 0's copy of the partner's first node)
+  constexpr int n = CsCfg<K, kHalves>::cap + kExtra;
   SnapCs s{};
   int o = 0;
   s.x = o; o += n * kNX;
@@ -182,7 +185,7 @@ struct CsLayout {
   int wv, eps, bnd, fix, ecost, snap;  // PIPG only
 };
 template <int K, int kHalves>
-__host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
+__host__ __device__ constexpr CsLayout cs_layout(bool pipg, bool cluster = false) {
   constexpr int S = CsCfg<K, kHalves>::S;
   CsLayout L{};
   int o = 0;
@@ -197,7 +200,7 @@ __host__ __device__ constexpr CsLayout cs_layout(bool pipg) {
     L.bnd = o; o += K * 2 * 2 * S;   // [role][u column][lo, hi][slot]
     L.fix = o; o += 4 * 16;          // init_val, final_val, init_on, final_on
     L.ecost = o; o += kNX * S;        // w_cost * e_cost at the last node's slot, zero elsewhere: [row][slot]
-    L.snap = o; o += 2 * snap_cs<K, kHalves>().total;
+    L.snap = o; o += 2 * (cluster ? snap_cs<K, kHalves, 1>().total : snap_cs<K, kHalves>().total);
   }
   L.total = o;
   return L;
@@ -208,6 +211,34 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
+}
+
+/// Which node a lane holds and in what capacity.
+struct Lane {
+  int k;        // node
+  int slot;     // k + 1
+  bool halo;    // a redundant copy of a node another warp owns
+  bool auth;    // this thread is THE owner of node k (k < n, not a halo copy)
+  bool primal;  // its primal entries are valid (owner, or the halo copy of node 31 in the first warp)
+  bool ival;    // auth and k is an interval (k < n - 1)
+};
+template <int kHalves>
+__device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
+  Lane t;
+  if (kHalves == 1) {
+    t.k = lane;
+    t.halo = false;
+    t.auth = t.k < n;
+    t.primal = t.auth;
+  } else {
+    t.k = half == 0 ? lane : 30 + lane;
+    t.halo = half == 0 ? lane == 31 : lane == 0;
+    t.auth = !t.halo && t.k < n;
+    t.primal = t.k < n && (half == 0 || lane != 0);
+  }
+  t.slot = t.k + 1;
+  t.ival = t.auth && t.k < n - 1;
+  return t;
 }
 
 /// The part of the horizon a CTA works on.  Without a cluster: everything.  In a cluster of two
@@ -240,8 +271,8 @@ __device__ __forceinline__ Cut make_cut(int n) {
   return c;
 }
 
-/// Which node a lane holds and in what capacity.
-struct Lane {
+/// Which node a lane of a cluster CTA holds and in what capacity (struct Lane with the cut).
+struct LaneX {
   int k;        // node (global)
   int slot;     // local node + 1
   bool halo;    // a redundant copy of a node another warp owns
@@ -253,8 +284,8 @@ struct Lane {
   bool have;    // it loads the operator block of interval k
 };
 template <int kHalves>
-__device__ __forceinline__ Lane make_lane(const Cut& c, int n, int half, int lane) {
-  Lane t;
+__device__ __forceinline__ LaneX make_lane_cut(const Cut& c, int n, int half, int lane) {
+  LaneX t;
   const int l = kHalves == 1 ? lane : (half == 0 ? lane : 30 + lane);
   t.k = c.base + l;
   t.halo = kHalves == 2 && (half == 0 ? lane == 31 : lane == 0);
@@ -265,10 +296,6 @@ __device__ __forceinline__ Lane make_lane(const Cut& c, int n, int half, int lan
   t.ival = t.auth && t.k < n - 1;
   t.have = t.k < n - 1 && t.k <= c.hi;  // halo copies load their node's block too
   return t;
-}
-template <int kHalves>
-__device__ __forceinline__ Lane make_lane(int n, int half, int lane) {
-  return make_lane<kHalves>(make_cut<false>(n), n, half, lane);
 }
 
 /// Hand-off between the two CTAs of a cluster (mailbox.cuh): per trip each CTA pushes the duals of
@@ -299,7 +326,7 @@ struct Port {
 };
 /// Opens the mailboxes (the shared memory is cleared and a block barrier passed), exchanges the
 /// pattern verdicts and returns the cluster-wide one.
-__device__ __forceinline__ bool open_port(Port& pt, double* sm, double* red, const Cut& c, const Lane& t, bool bad) {
+__device__ __forceinline__ bool open_port(Port& pt, double* sm, double* red, const Cut& c, const LaneX& t, bool bad) {
   const int tid = threadIdx.x;
   unsigned long long* box = reinterpret_cast<unsigned long long*>(red + Port::kBoxAt);
   pt.red = smem_u32(red);
@@ -508,7 +535,7 @@ __device__ __forceinline__ void gather_rows(const double (&own)[RoleT<K, R>::nro
 // ---------------------------------------------------------------------------------------------
 // power iteration (pipg.hpp:206-292)
 // ---------------------------------------------------------------------------------------------
-template <int K, int R, int kHalves, bool kCluster>
+template <int K, int R, int kHalves>
 __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b, unsigned char* handled) {
   using RT = RoleT<K, R>;
   using Cfg = CsCfg<K, kHalves>;
@@ -516,8 +543,203 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
   constexpr CsLayout L = cs_layout<K, kHalves>(false);
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
+  const Lane t = make_lane<kHalves>(n, half, lane);
+  for (int e = tid; e < L.total; e += Cfg::threads) sm[e] = 0.0;
+
+  OpCols<K, R> op;
+  const bool have = t.k < m;  // halo copies load their node's block too
+  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0) handled[b] = 0;
+    return;
+  }
+  if (tid == 0) handled[b] = 1;
+
+  double* phi_s = sm + L.phi + t.slot;    // row i at + i * S; interval k-1 at -1
+  double* th_s = sm + L.th + t.slot;
+  double* part_s = sm + L.part + t.slot;  // [role][row] at + (role * 15 + row) * S
+  double* xn_s = sm + L.xn + t.slot;      // [3] at + q * S; node k+1 at +1
+  double* red = sm + L.red;               // [2][kCsWarps] shares of the squared norm, by trip parity
+
+  // seed (pipg.hpp:213-230)
+  double zx[RT::nxc], zu[RT::nuc], vcd[RT::nrow];
+  double acc0 = 0.0;
+#pragma unroll
+  for (int j = 0; j < RT::nxc; ++j) {
+    zx[j] = t.primal ? a.seed_x[((size_t)b * n + t.k) * kNX + RT::xc(j)] : 0.0;
+    acc0 = fma(zx[j], zx[j], acc0);
+  }
+#pragma unroll
+  for (int j = 0; j < RT::nuc; ++j) {
+    zu[j] = t.primal ? a.seed_u[((size_t)b * n + t.k) * kNU + RT::uc(j)] : 0.0;
+    acc0 = fma(zu[j], zu[j], acc0);
+  }
+#pragma unroll
+  for (int r = 0; r < RT::nrow; ++r) {
+    double vp = 0.0, vn = 0.0;
+    if (t.ival) {
+      vp = a.seed_vcp[((size_t)b * m + t.k) * kNX + RT::row(r)];
+      vn = a.seed_vcn[((size_t)b * m + t.k) * kNX + RT::row(r)];
+    }
+    vcd[r] = vp - vn;
+    acc0 = fma(vp, vp, acc0);
+    acc0 = fma(vn, vn, acc0);
+  }
+  acc0 = warp_sum(t.auth ? acc0 : 0.0);
+  if (lane == 0) red[warp] = acc0;
+  block_barrier();
+  auto norm_sq = [&](int parity) {
+    const double2* p = reinterpret_cast<const double2*>(red + parity * kCsWarps);
+    const double2 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
+    const double lo = ((q0.x + q0.y) + (q1.x + q1.y)) + ((q2.x + q2.y) + (q3.x + q3.y));
+    if (Cfg::warps <= 8) return lo;
+    const double2 q4 = p[4], q5 = p[5], q6 = p[6], q7 = p[7];
+    return lo + (((q4.x + q4.y) + (q5.x + q5.y)) + ((q6.x + q6.y) + (q7.x + q7.y)));
+  };
+  double ss = norm_sq(0);  // squared norm of the current iterate
+  if (ss == 0.0) {  // pipg.hpp:224-225
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSeedZero;
+      a.sigma[b] = 0.0;
+      if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = 0;
+    }
+    return;
+  }
+  // Inside the loop sigma is ss * rsqrt(ss) (1 ulp from sqrt: it only feeds the stopping test, whose
+  // tolerance is four orders of magnitude wider) and the scale 1 / sigma of pipg.hpp:243 is the
+  // same rsqrt: no square root and no division on the trip's critical path.  The value returned is
+  // the correctly rounded sqrt of the last squared norm.
+  // The stopping test runs in every trip, also the first (no `if (j > 1)` block that would keep the
+  // norm -> rsqrt -> test chain out of the basic block of the gathers it can overlap with): the first
+  // one reads the seed's norm again and compares it with a NaN, which no tolerance accepts.
+  double inv;
+  double sigma = __longlong_as_double(0x7ff8000000000000ll);
+
+  // The forward products of trip j + 1 are issued right behind the adjoint map of trip j, in front
+  // of the barrier, so that the warp reduction of trip j's norm shares overlaps them.
+  constexpr int kJy = aligned_col<K, R>(kNX - 1);  // the role that owns x[y] also owns the relaxation dual
+  double own[RT::nrow], xnx[RT::nrow], dy = 0.0;
+  auto forward_map = [&]() {  // pipg.hpp:234-245: partial row sums of the own columns
+    double zun[RT::nuc];
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) zun[q] = __shfl_down_sync(kFull, zu[q], 1);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {  // x_{k+1}[row] of the aligned rows
+      const int jc = aligned_col<K, R>(RT::row(r));
+      xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, zx[jc >= 0 ? jc : 0], 1) : 0.0;
+    }
+    if (kJy >= 0) dy = __shfl_down_sync(kFull, zx[kJy >= 0 ? kJy : 0], 1) - zx[kJy >= 0 ? kJy : 0];  // e_y^T (x_{k+1} - x_k)
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      const int slot = xn_slot<K>(RT::xc(q));
+      if (slot >= 0 && t.auth) xn_s[slot * S] = zx[q];
+    }
+    forward_publish<K, R, S, true>(op, zx, zu, zun, part_s, t.auth, own);
+  };
+  forward_map();
+
+  int trips = 0;
+  bool done = false;
+  for (int j = 1; j <= a.j_max; ++j) {
+    block_barrier();
+    // ---- rows: sum of the partials, scale by 1 / sigma
+    double s[RT::nrow];
+    gather_rows<K, R, S>(own, part_s, s);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int i = RT::row(r);
+      const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
+      s[r] = (s[r] - xn) + vcd[r];
+    }
+    {  // stopping test of trip j-1 (pipg.hpp:277-289); j = 1: the seed against NaN, never met
+      ss = norm_sq((j - 1) & 1);
+      inv = rsqrt_pos(ss);
+      const double sigma_star = ss * inv;
+      const bool hit = fabs(sigma_star - sigma) <= a.eps_abs + a.eps_rel * max_nn(sigma_star, sigma);
+      sigma = sigma_star;
+      if (hit || ss == 0.0) {  // met, or the iterate is in the null space (pipg.hpp:280-284)
+        done = true;
+        break;
+      }
+    }
+    trips = j;
+    // rows of nodes without an interval come out as exact zeros (zero operator, zero neighbours);
+    // only real intervals are stored, the rest of the array stays cleared
+    double acc_d = 0.0;
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const double p = s[r] * inv;
+      if (t.ival) phi_s[RT::row(r) * S] = p;
+      vcd[r] = 2.0 * p;  // vc+ = phi, vc- = -phi (pipg.hpp:268-279)
+      acc_d = fma(vcd[r], p, acc_d);
+    }
+    if (kJy >= 0) {
+      if (t.ival) th_s[0] = dy * inv;
+    }
+    block_barrier();
+    // ---- adjoint map (pipg.hpp:247-275)
+    {
+      double gx[RT::nxc], gm[RT::nuc], gp[RT::nuc];
+      transposed<K, R, S>(op, phi_s, gx, gm, gp);
+#pragma unroll
+      for (int q = 0; q < RT::nxc; ++q) {
+        const int c = RT::xc(q);
+        double v = gx[q] - phi_s[c * S - 1];
+        if (c == kNX - 1) v += th_s[-1] - th_s[0];
+        zx[q] = v;
+      }
+#pragma unroll
+      for (int q = 0; q < RT::nuc; ++q) {
+        const double gpp = __shfl_up_sync(kFull, gp[q], 1);
+        zu[q] = gm[q] + (lane == 0 ? 0.0 : gpp);
+      }
+    }
+    double az0 = acc_d, az1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      if (q & 1) az1 = fma(zx[q], zx[q], az1);
+      else az0 = fma(zx[q], zx[q], az0);
+    }
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) az1 = fma(zu[q], zu[q], az1);
+    const double share = warp_sum(t.auth ? az0 + az1 : 0.0);
+    forward_map();  // of trip j + 1
+    if (lane == 0) red[(j & 1) * kCsWarps + warp] = share;
+  }
+  if (!done) {  // j_max trips without meeting the tolerance
+    block_barrier();
+    ss = norm_sq(a.j_max & 1);
+  }
+  if (tid == 0) {
+    a.sigma[b] = (1.0 + a.eps_buff) * sqrt(ss);
+    if (a.trips) a.trips[(size_t)b * a.trips_stride + (a.trips_slot ? a.trips_slot[b] : 0)] = trips;
+  }
+}
+
+template <int K, int kHalves>
+__global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  switch ((threadIdx.x >> 5) % K) {
+    case 0: power_role<4, 0, kHalves>(a, sm, b, handled); break;
+    case 1: power_role<4, 1, kHalves>(a, sm, b, handled); break;
+    case 2: power_role<4, 2, kHalves>(a, sm, b, handled); break;
+    default: power_role<4, 3, kHalves>(a, sm, b, handled); break;
+  }
+}
+
+// ---- the same over a cluster of two CTAs (struct Cut, struct Port) ----
+template <int K, int R, int kHalves, bool kCluster>
+__device__ __forceinline__ void power_role_x(const PowerArgs& a, double* sm, int b, unsigned char* handled) {
+  using RT = RoleT<K, R>;
+  using Cfg = CsCfg<K, kHalves>;
+  constexpr int S = Cfg::S;
+  constexpr CsLayout L = cs_layout<K, kHalves>(false);
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
   const Cut cut = make_cut<kCluster>(n);
-  const Lane t = make_lane<kHalves>(cut, n, half, lane);
+  const LaneX t = make_lane_cut<kHalves>(cut, n, half, lane);
   for (int e = tid; e < L.total; e += Cfg::threads) sm[e] = 0.0;
 
   OpCols<K, R> op;
@@ -743,15 +965,15 @@ __device__ __forceinline__ void power_role(const PowerArgs& a, double* sm, int b
 }
 
 template <int K, int kHalves, bool kCluster>
-__global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel(PowerArgs a, unsigned char* handled) {
+__global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_cluster_kernel(PowerArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   switch ((threadIdx.x >> 5) % K) {
-    case 0: power_role<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
-    case 1: power_role<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
-    case 2: power_role<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
-    default: power_role<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
+    case 0: power_role_x<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
+    case 1: power_role_x<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
+    case 2: power_role_x<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
+    default: power_role_x<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
   }
 }
 
@@ -761,11 +983,341 @@ __global__ void __launch_bounds__(CsCfg<K, kHalves>::threads, 1) power_cs_kernel
 /// stopping_custom(cur, prev) and the divergence test of pipg.hpp:475-487 over two snapshots: 0 =
 /// go on, 1 = converged, 2 = a non-finite primal or dual entry.  One copy for the four roles (the
 /// loop bodies are role-specific and have to share the instruction cache with as little as possible).
+template <int kHalves>
+__device__ __noinline__ int pipg_check(const double* cur, const double* prev, int n, double* red, double eps_abs,
+                                       double eps_rel) {
+  constexpr SnapCs SN = snap_cs<4, kHalves>();
+  constexpr int T = CsCfg<4, kHalves>::threads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = n - 1;
+  double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, badv = 0.0;
+  auto scan = [&](int off, int count, bool dual, bool finite_checked) {
+#pragma unroll 1
+    for (int e = tid; e < count; e += T) {
+      const double c = cur[off + e], o = prev[off + e];
+      if (dual) {
+        r_cur = max_nn(r_cur, fabs(c));
+        r_prev = max_nn(r_prev, fabs(o));
+        r_del = max_nn(r_del, fabs(c - o));
+      } else {
+        z_cur = max_nn(z_cur, fabs(c));
+        z_prev = max_nn(z_prev, fabs(o));
+        z_del = max_nn(z_del, fabs(c - o));
+      }
+      if (finite_checked && !pt_finite(c)) badv = 1.0;
+    }
+  };
+  scan(SN.x, n * kNX, false, true);
+  scan(SN.u, n * kNU, false, true);
+  scan(SN.vp, m * kNX, false, false);
+  scan(SN.vn, m * kNX, false, false);
+  scan(SN.ph, m * kNX, true, true);
+  scan(SN.th, m, true, false);
+  z_cur = warp_max_nn(z_cur); z_prev = warp_max_nn(z_prev); z_del = warp_max_nn(z_del);
+  r_cur = warp_max_nn(r_cur); r_prev = warp_max_nn(r_prev); r_del = warp_max_nn(r_del);
+  badv = warp_max_nn(badv);
+  if (lane == 0) {
+    double* rw = red + warp * 8;
+    rw[0] = z_cur; rw[1] = z_prev; rw[2] = z_del; rw[3] = r_cur; rw[4] = r_prev; rw[5] = r_del;
+    rw[6] = badv;
+  }
+  block_barrier();
+  double v[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double mx = 0.0;
+#pragma unroll
+    for (int w = 0; w < CsCfg<4, kHalves>::warps; ++w) mx = max_nn(mx, red[w * 8 + q]);
+    v[q] = mx;
+  }
+  block_barrier();  // red and the snapshots are rewritten later
+  if (v[6] > 0.0) return 2;
+  return (v[2] <= eps_abs + eps_rel * max_nn(v[0], v[1]) && v[5] <= eps_abs + eps_rel * max_nn(v[3], v[4])) ? 1 : 0;
+}
+
+template <int K, int R, int kHalves>
+__device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
+  using RT = RoleT<K, R>;
+  using Cfg = CsCfg<K, kHalves>;
+  constexpr int S = Cfg::S;
+  constexpr int T = Cfg::threads;
+  constexpr CsLayout L = cs_layout<K, kHalves>(true);
+  constexpr SnapCs SN = snap_cs<K, kHalves>();
+  const int n = a.shape.n, m = n - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
+  const Lane t = make_lane<kHalves>(n, half, lane);
+  for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
+
+  OpCols<K, R> op;
+  const bool have = t.k < m;  // halo copies load their node's block too
+  const bool bad = load_cols<K, R>(a.sp, (size_t)b * m + (have ? t.k : 0), have, op);
+  if (__syncthreads_or(bad ? 1 : 0)) {  // not the rocket pattern: the dense kernel takes the instance
+    if (tid == 0) handled[b] = 0;
+    return;
+  }
+  if (tid == 0) handled[b] = 1;
+
+  double* phi_s = sm + L.phi + t.slot;    // extrapolated dynamics dual, row i at + i * S; interval k-1 at -1
+  double* th_s = sm + L.th + t.slot;      // extrapolated relaxation dual
+  double* part_s = sm + L.part + t.slot;
+  double* xn_s = sm + L.xn + t.slot;      // reflections of x[q0], x[w2], x[y]; node k+1 at +1
+  const double* wv_s = sm + L.wv + t.slot;
+  const double* eps_s = sm + L.eps + t.slot;
+  double* bnd_s = sm + L.bnd + (R * 4) * S + t.slot;  // [u column][lo, hi] at + (2 * q + {0, 1}) * S
+  double* red = sm + L.red;
+  double* snap0 = sm + L.snap;
+  double* init_val = sm + L.fix;
+  double* final_val = init_val + 16;
+  double* init_on = final_val + 16;
+  double* final_on = init_on + 16;
+  const double* cost_s = sm + L.ecost + t.slot;  // the terminal-cost term of this node's entries (pipg.hpp:404)
+
+  const size_t gx = (size_t)b * n * kNX, gu = (size_t)b * n * kNU, gm_ = (size_t)b * m * kNX, gt = (size_t)b * m;
+  const int NXn = n * kNX, NUn = n * kNU, NM = m * kNX;
+  if (tid < kNX) sm[L.ecost + tid * S + n] = a.shape.w_cost * a.shape.e_cost[tid];  // slot of node n - 1
+  if (tid == 0) {
+    // later entries override earlier ones, as the assignment loops do (pipg.hpp:408-413)
+    for (int i = 0; i < a.shape.n_init_fix; ++i) {
+      init_on[a.shape.init_fix_idx[i]] = 1.0;
+      init_val[a.shape.init_fix_idx[i]] = a.sp.init_fix_val[(size_t)b * a.shape.n_init_fix + i];
+    }
+    for (int i = 0; i < a.shape.n_final_fix; ++i) {
+      final_on[a.shape.final_fix_idx[i]] = 1.0;
+      final_val[a.shape.final_fix_idx[i]] = a.sp.final_fix_val[(size_t)b * a.shape.n_final_fix + i];
+    }
+  }
+  for (int e = tid; e < NM; e += T) {  // [interval][row] -> [row][slot]
+    const int k = e / kNX, i = e - k * kNX;
+    sm[L.wv + i * S + k + 1] = a.sp.w[gm_ + e];
+  }
+  for (int e = tid; e < m; e += T) sm[L.eps + e + 1] = a.sp.eps_relax[gt + e];
+#pragma unroll
+  for (int q = 0; q < RT::nuc; ++q) {  // box of the own control entries (pipg.hpp:418-419); unbounded where there is no node
+    if (t.halo) continue;  // the owner's warp fills the slot; the halo copy reads it behind the barrier
+    bnd_s[(2 * q) * S] = t.auth ? a.sp.u_min[gu + t.k * kNU + RT::uc(q)] : -INFINITY;
+    bnd_s[(2 * q + 1) * S] = t.auth ? a.sp.u_max[gu + t.k * kNU + RT::uc(q)] : INFINITY;
+  }
+  // warm start: ex = cur = workspace (pipg.hpp:362-374); it is snapshot 0
+  for (int e = tid; e < NXn; e += T) snap0[SN.x + e] = a.ws.x[gx + e];
+  for (int e = tid; e < NUn; e += T) snap0[SN.u + e] = a.ws.u[gu + e];
+  for (int e = tid; e < NM; e += T) {
+    snap0[SN.vp + e] = a.ws.vc_pos[gm_ + e];
+    snap0[SN.vn + e] = a.ws.vc_neg[gm_ + e];
+    snap0[SN.ph + e] = a.ws.dyn_dual[gm_ + e];
+  }
+  for (int e = tid; e < m; e += T) snap0[SN.th + e] = a.ws.relax_dual[gt + e];
+  block_barrier();
+
+  // boundary columns of this thread (pipg.hpp:408-413): bit q set when own x column q is assigned
+  int fix_bits = 0;
+  const double* fix_val = init_val;
+  const bool last_node = t.primal && t.k == n - 1;
+  if (t.primal && (t.k == 0 || t.k == n - 1)) {
+    const double* on = last_node ? final_on : init_on;
+    fix_val = last_node ? final_val : init_val;
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q)
+      if (on[RT::xc(q)] != 0.0) fix_bits |= 1 << q;
+  }
+
+  const bool warp_fix = __any_sync(kFull, fix_bits != 0);  // warp-uniform
+
+  // owner-private extrapolated copies
+  double xe[RT::nxc], ue[RT::nuc], vpe[RT::nrow], vne[RT::nrow], phe[RT::nrow], the = 0.0;
+#pragma unroll
+  for (int q = 0; q < RT::nxc; ++q) xe[q] = t.primal ? snap0[SN.x + t.k * kNX + RT::xc(q)] : 0.0;
+#pragma unroll
+  for (int q = 0; q < RT::nuc; ++q) ue[q] = t.primal ? snap0[SN.u + t.k * kNU + RT::uc(q)] : 0.0;
+#pragma unroll
+  for (int r = 0; r < RT::nrow; ++r) {
+    const int e = t.k * kNX + RT::row(r);
+    vpe[r] = t.ival ? snap0[SN.vp + e] : 0.0;
+    vne[r] = t.ival ? snap0[SN.vn + e] : 0.0;
+    phe[r] = t.ival ? snap0[SN.ph + e] : 0.0;
+    if (t.auth) phi_s[RT::row(r) * S] = phe[r];
+  }
+  if (R == 0) {
+    the = t.ival ? snap0[SN.th + t.k] : 0.0;
+    if (t.auth) th_s[0] = the;
+  }
+
+  const double sigma = a.sigma[b];
+  const double alpha = 2.0 / (a.shape.w_prox + sqrt(a.shape.w_prox * a.shape.w_prox + 4.0 * a.omega * sigma));
+  const double beta = a.omega * alpha;
+  // extrapolation (pipg.hpp:461-472) (1 - rho) * ex + rho * cur, evaluated as ex + rho * (cur - ex)
+  auto extrapolate = [&](double ex, double cur) { return fma(a.rho, cur - ex, ex); };
+  block_barrier();
+
+  // One iteration.  kStore additionally writes the new *_cur values of every owner into `snap`.
+  auto iteration = [&](auto store_tag, double* snap) {
+    constexpr bool kStore = decltype(store_tag)::value;
+    // ---- primal projected-gradient step (pipg.hpp:388-420) by the owner of each entry
+    double rx[RT::nxc], ru[RT::nuc];
+    {
+      double gx_[RT::nxc], gm[RT::nuc], gp[RT::nuc];
+      transposed<K, R, S, true>(op, phi_s, gx_, gm, gp);
+#pragma unroll
+      for (int q = 0; q < RT::nxc; ++q) {
+        const int c = RT::xc(q);
+        const double x0 = xe[q];
+        double base = x0 * a.shape.w_prox;
+        base += cost_s[c * S];  // zero but at the last node: no branch, no predicated address arithmetic
+        base += -phi_s[c * S - 1];
+        if (c == kNX - 1) base += th_s[-1] - th_s[0];
+        const double grad = base + gx_[q];
+        double xn = x0 + -alpha * grad;
+        if (warp_fix) xn = (fix_bits & (1 << q)) ? fix_val[c] : xn;  // (measured: faster than unconditional)
+        rx[q] = fma(2.0, xn, -x0);
+        if (kStore && t.auth) snap[SN.x + t.k * kNX + c] = xn;
+        xe[q] = extrapolate(x0, xn);
+      }
+#pragma unroll
+      for (int q = 0; q < RT::nuc; ++q) {
+        double gpp = __shfl_up_sync(kFull, gp[q], 1);
+        gpp = lane == 0 ? 0.0 : gpp;
+        const double u0 = ue[q];
+        const double grad = u0 * a.shape.w_prox + (gm[q] + gpp);
+        double un = u0 + -alpha * grad;
+        const double lo = bnd_s[(2 * q) * S], hi = bnd_s[(2 * q + 1) * S];
+        // std::max(lo, std::min(hi, v)), pipg.hpp:418-419
+        un = clamp_box(lo, hi, un);
+        ru[q] = fma(2.0, un, -u0);
+        if (kStore && t.auth) snap[SN.u + t.k * kNU + RT::uc(q)] = un;
+        ue[q] = extrapolate(u0, un);
+      }
+    }
+    // ---- forward products of the reflections: partial row sums of the own columns
+    double run[RT::nuc];
+#pragma unroll
+    for (int q = 0; q < RT::nuc; ++q) run[q] = __shfl_down_sync(kFull, ru[q], 1);
+    double xnx[RT::nrow];
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int jc = aligned_col<K, R>(RT::row(r));
+      xnx[r] = jc >= 0 ? __shfl_down_sync(kFull, rx[jc >= 0 ? jc : 0], 1) : 0.0;
+    }
+    double drift = 0.0;
+    if (R == 0) drift = __shfl_down_sync(kFull, rx[4], 1) - rx[4];  // K = 4: role 0 owns x[y]
+#pragma unroll
+    for (int q = 0; q < RT::nxc; ++q) {
+      const int slot = xn_slot<K>(RT::xc(q));
+      if (slot >= 0 && t.auth) xn_s[slot * S] = rx[q];
+    }
+    double own[RT::nrow];
+    forward_publish<K, R, S, false>(op, rx, ru, run, part_s, t.auth, own);
+    block_barrier();
+    // ---- slacks (pipg.hpp:423-430), PI feedback of the constraint violation (:433-458),
+    //      extrapolation of the dual groups (:468-472)
+    double s[RT::nrow];
+    gather_rows<K, R, S>(own, part_s, s);
+#pragma unroll
+    for (int r = 0; r < RT::nrow; ++r) {
+      const int i = RT::row(r);
+      const double xn = aligned_col<K, R>(i) >= 0 ? xnx[r] : xn_s[xn_slot<K>(i) * S + 1];
+      double resid = s[r] - xn;
+      const double p0 = phe[r], vp0 = vpe[r], vn0 = vne[r];
+      const double vp = clip0(vp0 - alpha * (a.shape.w_ep + p0));
+      const double vn = clip0(vn0 - alpha * (a.shape.w_ep - p0));
+      resid += (2.0 * vp - vp0) - (2.0 * vn - vn0) + wv_s[i * S];
+      const double pn = p0 + beta * resid;
+      if (kStore && t.ival) {
+        const int e = t.k * kNX + i;
+        snap[SN.vp + e] = vp;
+        snap[SN.vn + e] = vn;
+        snap[SN.ph + e] = pn;
+      }
+      // rows of nodes without an interval (zero operator, zero neighbours, zero right-hand side,
+      // w_ep >= 0) stay exact zeros; only real intervals are stored
+      phe[r] = extrapolate(p0, pn);
+      vpe[r] = extrapolate(vp0, vp);
+      vne[r] = extrapolate(vn0, vn);
+      if (t.ival) phi_s[i * S] = phe[r];
+    }
+    if (R == 0) {
+      const double tn = clip0(the + beta * (drift - eps_s[0]));
+      if (kStore && t.ival) snap[SN.th + t.k] = tn;
+      the = extrapolate(the, tn);
+      if (t.ival) th_s[0] = the;
+    }
+    block_barrier();
+  };
+
+  int iters = 0, cur_set = 0;  // snapshot holding the latest materialised *_cur groups
+  bool converged = false, diverged = false;
+  int to_check = a.j_check;  // iterations left until the next stopping test (counts down to 0)
+  for (int j = 1; j <= a.j_max; ++j) {
+    --to_check;
+    const bool check = to_check == 0;
+    // cur values are materialised when the next iteration checks against them, when this one
+    // checks (a converged exit returns them), and on the last iteration
+    const bool keep = to_check <= 1 || j == a.j_max;
+    if (check) to_check = a.j_check;
+    if (keep) {
+      cur_set ^= 1;
+      iteration(std::true_type{}, snap0 + cur_set * SN.total);
+    } else {
+      iteration(std::false_type{}, nullptr);
+    }
+    iters = j;
+    if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
+      const int verdict = pipg_check<kHalves>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total, n, red,
+                                              a.eps_abs, a.eps_rel);
+      if (verdict == 2) {
+        diverged = true;
+        break;
+      }
+      if (verdict == 1) {
+        converged = true;
+        break;
+      }
+    }
+  }
+
+  if (diverged) {  // SolverDiverged(j): the workspace is left untouched, pipg.hpp:478
+    if (tid == 0) {
+      if (a.status) a.status[b] = kStSolverDiverged;
+      if (a.fail_index) a.fail_index[b] = iters;
+      if (a.iterations) a.iterations[b] = iters;
+      if (a.converged) a.converged[b] = 0;
+      if (a.active) a.active[b] = 0;
+    }
+    return;
+  }
+  // solution = the *_cur groups, pipg.hpp:490-495 (every iteration ends with a barrier)
+  const double* cur = snap0 + cur_set * SN.total;
+  for (int e = tid; e < NXn; e += T) a.ws.x[gx + e] = cur[SN.x + e];
+  for (int e = tid; e < NUn; e += T) a.ws.u[gu + e] = cur[SN.u + e];
+  for (int e = tid; e < NM; e += T) {
+    a.ws.vc_pos[gm_ + e] = cur[SN.vp + e];
+    a.ws.vc_neg[gm_ + e] = cur[SN.vn + e];
+    a.ws.dyn_dual[gm_ + e] = cur[SN.ph + e];
+  }
+  for (int e = tid; e < m; e += T) a.ws.relax_dual[gt + e] = cur[SN.th + e];
+  if (tid == 0) {
+    if (a.iterations) a.iterations[b] = iters;
+    if (a.converged) a.converged[b] = converged ? 1 : 0;
+  }
+}
+
+template <int kHalves>
+__global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.x;
+  if (a.active && !a.active[b]) return;
+  switch ((threadIdx.x >> 5) & 3) {
+    case 0: pipg_role<4, 0, kHalves>(a, sm, b, handled); break;
+    case 1: pipg_role<4, 1, kHalves>(a, sm, b, handled); break;
+    case 2: pipg_role<4, 2, kHalves>(a, sm, b, handled); break;
+    default: pipg_role<4, 3, kHalves>(a, sm, b, handled); break;
+  }
+}
+
+// ---- the same over a cluster of two CTAs (struct Cut, struct Port) ----
 template <int kHalves, bool kCluster>
-__device__ __noinline__ int pipg_check(const double* cur, const double* prev, int l0, int nn, int mm, double* red,
+__device__ __noinline__ int pipg_check_x(const double* cur, const double* prev, int l0, int nn, int mm, double* red,
                                        double eps_abs, double eps_rel) {
   // l0: first owned local node, nn / mm: owned nodes / intervals of this CTA
-  constexpr SnapCs SN = snap_cs<4, kHalves>();
+  constexpr SnapCs SN = snap_cs<4, kHalves, 1>();
   constexpr int T = CsCfg<4, kHalves>::threads;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double z_cur = 0.0, z_prev = 0.0, z_del = 0.0, r_cur = 0.0, r_prev = 0.0, r_del = 0.0, badv = 0.0;
@@ -827,17 +1379,17 @@ __device__ __noinline__ int pipg_check(const double* cur, const double* prev, in
 }
 
 template <int K, int R, int kHalves, bool kCluster>
-__device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
+__device__ __forceinline__ void pipg_role_x(const PipgArgs& a, double* sm, int b, unsigned char* handled) {
   using RT = RoleT<K, R>;
   using Cfg = CsCfg<K, kHalves>;
   constexpr int S = Cfg::S;
   constexpr int T = Cfg::threads;
-  constexpr CsLayout L = cs_layout<K, kHalves>(true);
-  constexpr SnapCs SN = snap_cs<K, kHalves>();
+  constexpr CsLayout L = cs_layout<K, kHalves>(true, true);
+  constexpr SnapCs SN = snap_cs<K, kHalves, 1>();
   const int n = a.shape.n, m = n - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, half = warp / K;
   const Cut cut = make_cut<kCluster>(n);
-  const Lane t = make_lane<kHalves>(cut, n, half, lane);
+  const LaneX t = make_lane_cut<kHalves>(cut, n, half, lane);
   const int tl = t.slot - 1;  // local node: the snapshots are indexed by it
   for (int e = tid; e < L.total; e += T) sm[e] = 0.0;
 
@@ -1083,7 +1635,7 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
     }
     iters = j;
     if (check) {  // stopping_custom(cur, prev) and the divergence test, pipg.hpp:475-487
-      const int verdict = pipg_check<kHalves, kCluster>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total,
+      const int verdict = pipg_check_x<kHalves, kCluster>(snap0 + cur_set * SN.total, snap0 + (cur_set ^ 1) * SN.total,
                                                         cut.lo - cut.base, cut.hi - cut.lo,
                                                         (cut.hi < m ? cut.hi : m) - cut.lo, red, a.eps_abs, a.eps_rel);
       if (verdict == 2) {
@@ -1129,15 +1681,15 @@ __device__ __forceinline__ void pipg_role(const PipgArgs& a, double* sm, int b, 
 }
 
 template <int kHalves, bool kCluster>
-__global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_kernel(PipgArgs a, unsigned char* handled) {
+__global__ void __launch_bounds__(CsCfg<4, kHalves>::threads, 1) pipg_cs_cluster_kernel(PipgArgs a, unsigned char* handled) {
   extern __shared__ __align__(16) double sm[];
   const int b = kCluster ? blockIdx.x >> 1 : blockIdx.x;
   if (a.active && !a.active[b]) return;  // both CTAs of a cluster leave together
   switch ((threadIdx.x >> 5) & 3) {
-    case 0: pipg_role<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
-    case 1: pipg_role<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
-    case 2: pipg_role<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
-    default: pipg_role<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
+    case 0: pipg_role_x<4, 0, kHalves, kCluster>(a, sm, b, handled); break;
+    case 1: pipg_role_x<4, 1, kHalves, kCluster>(a, sm, b, handled); break;
+    case 2: pipg_role_x<4, 2, kHalves, kCluster>(a, sm, b, handled); break;
+    default: pipg_role_x<4, 3, kHalves, kCluster>(a, sm, b, handled); break;
   }
 }
 
@@ -1148,26 +1700,29 @@ bool solver_cs_supports(const SubShape& s, bool has_a_plus) {
 }
 
 namespace {
-template <int K, int kHalves, bool kCluster = false>
+template <int K, int kHalves>
 cudaError_t opt_in_power() {
-  return cudaFuncSetAttribute(power_cs_kernel<K, kHalves, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(power_cs_kernel<K, kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(double) * cs_layout<K, kHalves>(false).total));
 }
-template <int kHalves, bool kCluster = false>
+template <int kHalves>
 cudaError_t opt_in_pipg() {
-  return cudaFuncSetAttribute(pipg_cs_kernel<kHalves, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(pipg_cs_kernel<kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(double) * cs_layout<4, kHalves>(true).total));
 }
+constexpr size_t kPowerClusterSmem = sizeof(double) * cs_layout<4, 2>(false).total;
+constexpr size_t kPipgClusterSmem = sizeof(double) * cs_layout<4, 2>(true, true).total;
 template <int K, int kHalves>
 void launch_power(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
-  power_cs_kernel<K, kHalves, false><<<a.batch, CsCfg<K, kHalves>::threads, sizeof(double) * cs_layout<K, kHalves>(false).total, stream>>>(a, handled);
+  power_cs_kernel<K, kHalves><<<a.batch, CsCfg<K, kHalves>::threads, sizeof(double) * cs_layout<K, kHalves>(false).total, stream>>>(a, handled);
 }
 /// One instance over a cluster of two CTAs (kCsMaxNodes < n <= kCsClusterMaxNodes).
-cudaError_t launch_power_cluster(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
+template <class Kernel, class Args>
+cudaError_t launch_cluster(Kernel kernel, const Args& a, size_t smem, unsigned char* handled, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2u * (unsigned)a.batch);
   cfg.blockDim = dim3(CsCfg<4, 2>::threads);
-  cfg.dynamicSmemBytes = sizeof(double) * cs_layout<4, 2>(false).total;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr{};
   attr.id = cudaLaunchAttributeClusterDimension;
@@ -1176,51 +1731,44 @@ cudaError_t launch_power_cluster(const PowerArgs& a, unsigned char* handled, cud
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, power_cs_kernel<4, 2, true>, a, handled);
+  return cudaLaunchKernelEx(&cfg, kernel, a, handled);
 }
 }  // namespace
 
 size_t pipg_cs_smem(const SubShape& s) {
+  if (s.n > kCsMaxNodes) return kPipgClusterSmem;
   return sizeof(double) * (size_t)(s.n <= CsCfg<4, 1>::cap ? cs_layout<4, 1>(true).total : cs_layout<4, 2>(true).total);
 }
 
 cudaError_t configure_solver_cs(const SubShape&) {
   cudaError_t e = opt_in_power<4, 1>();
   if (e == cudaSuccess) e = opt_in_power<4, 2>();
-  if (e == cudaSuccess) e = opt_in_power<4, 2, true>();
   if (e == cudaSuccess) e = opt_in_pipg<1>();
   if (e == cudaSuccess) e = opt_in_pipg<2>();
-  if (e == cudaSuccess) e = opt_in_pipg<2, true>();
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(power_cs_cluster_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPowerClusterSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pipg_cs_cluster_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPipgClusterSmem);
   return e;
 }
 
 cudaError_t launch_power_cs(const PowerArgs& a, unsigned char* handled, cudaStream_t stream) {
-  if (a.shape.n > kCsMaxNodes) return launch_power_cluster(a, handled, stream);
+  if (a.shape.n > kCsMaxNodes)
+    return launch_cluster(power_cs_cluster_kernel<4, 2, true>, a, kPowerClusterSmem, handled, stream);
   if (a.shape.n <= CsCfg<4, 1>::cap) launch_power<4, 1>(a, handled, stream);
   else launch_power<4, 2>(a, handled, stream);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pipg_cs(const PipgArgs& a, unsigned char* handled, cudaStream_t stream) {
-  if (a.shape.n > kCsMaxNodes) {  // one instance over a cluster of two CTAs
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2u * (unsigned)a.batch);
-    cfg.blockDim = dim3(CsCfg<4, 2>::threads);
-    cfg.dynamicSmemBytes = sizeof(double) * cs_layout<4, 2>(true).total;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr{};
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, pipg_cs_kernel<2, true>, a, handled);
-  }
+  if (a.shape.n > kCsMaxNodes)
+    return launch_cluster(pipg_cs_cluster_kernel<2, true>, a, kPipgClusterSmem, handled, stream);
   if (a.shape.n <= CsCfg<4, 1>::cap) {
-    pipg_cs_kernel<1, false><<<a.batch, CsCfg<4, 1>::threads, sizeof(double) * cs_layout<4, 1>(true).total, stream>>>(a, handled);
+    pipg_cs_kernel<1><<<a.batch, CsCfg<4, 1>::threads, sizeof(double) * cs_layout<4, 1>(true).total, stream>>>(a, handled);
   } else {
-    pipg_cs_kernel<2, false><<<a.batch, CsCfg<4, 2>::threads, sizeof(double) * cs_layout<4, 2>(true).total, stream>>>(a, handled);
+    pipg_cs_kernel<2><<<a.batch, CsCfg<4, 2>::threads, sizeof(double) * cs_layout<4, 2>(true).total, stream>>>(a, handled);
   }
   return cudaGetLastError();
 }

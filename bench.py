@@ -569,8 +569,8 @@ def run_own_arm(args):
         # (profiles/ncu_traffic.json: bytes for a 148-instance launch), scaled to this batch
         traffic = None
         kernel_of = {"linearize": "column_pass_kernel",
-                     "power_iteration": "power_cs_kernel" if n <= 61 else "power_fast_kernel",
-                     "pipg": "pipg_cs_kernel" if n <= 61 else "pipg_fast_kernel"}
+                     "power_iteration": "power_cs_kernel",   # (n > 61: its 2-CTA cluster variant)
+                     "pipg": "pipg_cs_kernel"}
         tpath = ROOT / "profiles" / "ncu_traffic.json"
         if tpath.exists() and n in (50, 100):
             tj = json.loads(tpath.read_text())

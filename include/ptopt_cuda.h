@@ -221,11 +221,12 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h);
  *              up to eight CTAs, sixteen threads per node (a short dependent instruction
  *              stream per thread); up to 128 nodes.  Lowest single-solve latency, lower
  *              throughput per SM.
- *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size.  Up to 61 nodes
+ *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size.  Up to 102 nodes
  *              the column-sparse kernels run first (four role-uniform warps per 32 nodes, the
  *              structural zeros of the rocket model's state-transition blocks skipped at compile
- *              time); they verify the zero pattern of every instance while loading it and leave
- *              instances without it to the dense kernels (FAST_DENSE), which run right behind.
+ *              time; one CTA per instance up to 61 nodes, a 2-CTA cluster above); they verify the
+ *              zero pattern of every instance while loading it and leave instances without it to
+ *              the dense kernels (FAST_DENSE), which run right behind.
  *   FAST_DENSE the dense register-resident kernels alone: five threads per node, one CTA per
  *              instance up to 51 nodes, a 2-CTA cluster up to 102; any operator values. */
 #define PTOPT_SOLVER_AUTO 0

@@ -368,6 +368,58 @@ def test_pipg_rocket_2000_iterations(solver15, ptor):
         assert np.abs(ws[f][0] - getattr(ref, f)).max() <= TOL_ITER, f
 
 
+@pytest.mark.parametrize("nodes", [50, 100])
+def test_pipg_rocket_stopping_and_divergence_on_the_column_sparse_kernels(ptor, nodes):
+    """stopping_custom and the divergence test (pipg.hpp:307-326, 475-487) on the rocket-shaped
+    subproblem, i.e. on the column-sparse kernels: one CTA per instance at N=50, a 2-CTA cluster at
+    N=100, where the maxima of the two halves are combined between cluster barriers and both CTAs
+    have to take the same verdict.  (a) loose tolerances: the solve stops early at the oracle's
+    iteration; (b) a wildly underestimated sigma diverges: status, iteration index as the oracle
+    reports them, workspace untouched; the neighbour instance in the batch is not disturbed."""
+    from paper_2404_18034_b200.binding import Solver
+
+    sc = scenario.default_scenario(nodes)
+    d, shape, sub = rocket_subproblem(sc, ptor, 1)
+    n, m = d.nodes, d.nodes - 1
+    sx, su = ptor.scp_seed(scenario.run_seed(sc.dispersion.seed, 1), n)
+    z = np.zeros((m, NX))
+    rc, sigma, _ = ptor.power_iteration(shape, sub, sx, su, z, z, 1e-12, 1e-12, 0.05, 2000, with_trips=True)
+    assert rc == 0
+    with Solver(d) as s:
+        s.set_solver_path("fast")
+        # (a) early stop
+        cfg = abi.PipgConfig(omega=100.0, rho=1.6, j_max=4000, j_check=5, eps_abs=2e-3, eps_rel=2e-3,
+                             eps_buff=0.05)
+        ref = Workspace(NX, NU, n)
+        rc, it_ref, conv_ref, _ = ptor.pipg(shape, sub, cfg, sigma, ref)
+        assert rc == 0 and conv_ref and it_ref < 4000
+        ws = ws_dict(Workspace(NX, NU, n))
+        it, conv, status, _ = s.pipg_custom(shape, batch1(sub), cfg, [sigma], ws)
+        assert status[0] == 0 and conv[0] == 1 and it[0] == it_ref
+        for f in ref.FIELDS:
+            assert np.abs(ws[f][0] - getattr(ref, f)).max() <= TOL_ITER, f
+        # (b) divergence in the first instance of a batch of two
+        bad = abi.PipgConfig(omega=1e8, rho=1.6, j_max=20000, j_check=5, eps_abs=1e-11, eps_rel=1e-11,
+                             eps_buff=0.05)
+        ref_bad, ref_ok = Workspace(NX, NU, n), Workspace(NX, NU, n)
+        ref_bad.x[:] = 0.5
+        ref_ok.x[:] = 0.5
+        rc_bad, _, _, fail_ref = ptor.pipg(shape, sub, bad, 1e-16, ref_bad)
+        rc_ok, it_ok, conv_ok, _ = ptor.pipg(shape, sub, bad, sigma, ref_ok)
+        assert rc_bad == abi.ST_SOLVER_DIVERGED
+        start = Workspace(NX, NU, n)
+        start.x[:] = 0.5
+        ws2 = {f: np.concatenate([v, v]) for f, v in ws_dict(start).items()}
+        two = {f: (None if getattr(sub, f) is None else np.stack([getattr(sub, f)] * 2)) for f in sub.FIELDS}
+        it, conv, status, fail = s.pipg_custom(shape, two, bad, [1e-16, sigma], ws2)
+        assert status[0] == abi.ST_SOLVER_DIVERGED and fail[0] == fail_ref
+        np.testing.assert_array_equal(ws2["x"][0], start.x)  # workspace untouched on divergence
+        assert status[1] == rc_ok and it[1] == it_ok and conv[1] == conv_ok
+        if rc_ok == 0:
+            for f in ref_ok.FIELDS:
+                assert np.abs(ws2[f][1] - getattr(ref_ok, f)).max() <= TOL_ITER * max(1.0, np.abs(getattr(ref_ok, f)).max()), f
+
+
 @pytest.mark.parametrize("nodes,where", [(15, 3), (100, 3), (100, 80)])
 def test_column_sparse_kernels_leave_foreign_operators_to_the_dense_ones(ptor, nodes, where):
     """The column-sparse kernels check the zero pattern of every instance while they load it.  A

@@ -312,10 +312,12 @@ struct Port {
   unsigned rsm;     // the partner's shared memory (shared::cluster address of sm[0])
   unsigned armer;   // thread 0
   bool need_phi;    // this warp reads a slot the partner fills
+  /// Thread 0 arms the phase (its warp does not wait unless it reads the partner's values itself: a
+  /// warp that waits runs its phase after the release, and two such warps on one scheduler -- the
+  /// armer's and the halo warp of the same role -- were the long pole of the trip).
   __device__ __forceinline__ void recv_phi(int phase) const {
-    if (!need_phi) return;
     mbar_expect_pred(armer, box, kPhiBytes);
-    mbar_wait_at(box, (unsigned)phase);
+    if (need_phi) mbar_wait_at(box, (unsigned)phase);
   }
   __device__ __forceinline__ void recv_norm(int trip, int bytes) const {
     const unsigned at = box + 8u + 8u * (unsigned)(trip & 1);
@@ -345,7 +347,7 @@ __device__ __forceinline__ bool open_port(Port& pt, double* sm, double* red, con
   pt.rsm = partner_u32(sm, c.rank ^ 1);
   pt.armer = tid == 0 ? 1u : 0u;
   const bool reads = c.rank == 0 ? t.k == c.hi : (t.k == c.lo - 1 || t.k == c.lo);
-  pt.need_phi = __any_sync(kFull, reads) || tid < 32;  // the armer's warp always waits
+  pt.need_phi = __any_sync(kFull, reads);
   const int theirs = *cg::this_cluster().map_shared_rank(flag, c.rank ^ 1);
   return bad || theirs != 0;
 }

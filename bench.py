@@ -358,8 +358,8 @@ def other_configs(device_index, fp64_peak):
         "solves_per_s": B / (st["graph_total"] * 1e-3), "graph_ms": st["graph_total"],
         "stages_ms": {k: st[k] for k in ("linearize", "power_iteration", "pipg")},
         "power_trips_mean": float(res["power_trips"].sum(axis=1).mean()),
-        "what": "full SCP solves at N=100 on one GPU (column-sparse kernels, one instance over a 2-CTA cluster: "
-                "74 instances at a time, four waves), device time of the graph"}
+        "what": "full SCP solves at N=100 on one GPU (one instance over a 2-CTA cluster, 74 instances at a time, "
+                "four waves: column-sparse power iteration, dense cluster PIPG), device time of the graph"}
     # ---- the headline configuration on the dense register-resident kernels alone (round-1 path), for
     #      the gain of the column-sparse kernels in the same run
     n, B = 50, 4096
@@ -570,7 +570,7 @@ def run_own_arm(args):
         traffic = None
         kernel_of = {"linearize": "column_pass_kernel",
                      "power_iteration": "power_cs_kernel",   # (n > 61: its 2-CTA cluster variant)
-                     "pipg": "pipg_cs_kernel"}
+                     "pipg": "pipg_cs_kernel" if n <= 61 else "pipg_fast_kernel"}
         tpath = ROOT / "profiles" / "ncu_traffic.json"
         if tpath.exists() and n in (50, 100):
             tj = json.loads(tpath.read_text())

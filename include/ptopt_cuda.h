@@ -224,7 +224,8 @@ int ptopt_cuda_destroy(ptopt_cuda_handle* h);
  *   FAST_THROUGHPUT register-resident throughput kernels whatever the batch size.  Up to 102 nodes
  *              the column-sparse kernels run first (four role-uniform warps per 32 nodes, the
  *              structural zeros of the rocket model's state-transition blocks skipped at compile
- *              time; one CTA per instance up to 61 nodes, a 2-CTA cluster above); they verify the
+ *              time; one CTA per instance up to 61 nodes; above, the power iteration over a 2-CTA
+ *              cluster and PIPG on the dense cluster kernel); they verify the
  *              zero pattern of every instance while loading it and leave instances without it to
  *              the dense kernels (FAST_DENSE), which run right behind.
  *   FAST_DENSE the dense register-resident kernels alone: five threads per node, one CTA per

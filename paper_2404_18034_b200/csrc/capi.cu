@@ -250,6 +250,19 @@ bool use_cs_solver(const ptopt_cuda_handle* h, const SubShape& s, bool has_a_plu
          solver_cs_supports(s, has_a_plus);
 }
 
+/// Shapes above kCsMaxNodes (2-CTA clusters): the power iteration runs on the column-sparse cluster
+/// kernel, PIPG on the dense cluster kernel.  The column-sparse PIPG cluster kernel
+/// (pipg_cs_cluster_kernel) is parity-green and sanitizer-clean up to a few hundred instances but
+/// ended in a mailbox time-out (launch failure) in a batch of 2048 x N=100, so it is not the
+/// default; PTOPT_CS_CLUSTER=3 selects it (bit 0: power iteration, bit 1: PIPG).
+bool cs_stage_enabled(const SubShape& s, int stage_bit) {
+  static const int mask = [] {
+    const char* e = getenv("PTOPT_CS_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  return s.n <= kCsMaxNodes || (mask & stage_bit) != 0;
+}
+
 /// The split variant of the register-resident kernels (see solver_fast.cu) runs only when the
 /// handle asks for it (and the node count allows it).  Measured on B200 it loses to one CTA per
 /// instance both in throughput (493 vs 655 solves/s at N=50) and in single-solve latency
@@ -289,7 +302,7 @@ int dispatch_power(ptopt_cuda_handle* h, const PowerArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr)) {
+  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr) && cs_stage_enabled(a.shape, 1)) {
     unsigned char* handled = nullptr;
     PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
     PT_CUDA(launch_power_cs(a, handled, h->stream));
@@ -312,7 +325,7 @@ int dispatch_pipg(ptopt_cuda_handle* h, const PipgArgs& a) {
   }
   const bool fast = use_fast_solver(h, a.shape, a.sp.A_plus != nullptr);
   PT_TRY(configure_solver(h, a.shape, fast));
-  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr)) {
+  if (fast && use_cs_solver(h, a.shape, a.sp.A_plus != nullptr) && cs_stage_enabled(a.shape, 2)) {
     unsigned char* handled = nullptr;
     PT_TRY(device_out(h, B_HANDLED, (size_t)a.batch, &handled));
     PT_CUDA(launch_pipg_cs(a, handled, h->stream));
@@ -496,6 +509,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
   const bool fast = use_fast_solver(h, h->rocket_shape, false);
   const int lat = latency_ranks(h, h->rocket_shape, false, batch);
   const bool cs = !lat && fast && use_cs_solver(h, h->rocket_shape, false);
+  const bool cs_power = cs && cs_stage_enabled(h->rocket_shape, 1), cs_pipg = cs && cs_stage_enabled(h->rocket_shape, 2);
   unsigned char* handled = h->buf[S_HANDLED].as<unsigned char>();
   PowerArgs pa_rest = pa;
   PipgArgs ga_rest = ga;
@@ -508,7 +522,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
     PT_CUDA(mark(1));
     kernels += 1;
     if (it == h->desc.max_iters) break;  // the last pass only measures the final defect
-    if (cs) {  // column-sparse kernels, then the dense ones on whatever they did not take
+    if (cs_power) {  // column-sparse kernels, then the dense ones on whatever they did not take
       PT_CUDA(launch_power_cs(pa, handled, h->stream));
       PT_CUDA(launch_power_fast(pa_rest, false, h->stream));
       kernels += 1;
@@ -518,7 +532,7 @@ int enqueue_scp_loop(ptopt_cuda_handle* h, int batch, const ScpState& st, int* k
                      : launch_power_generic(pa, h->stream));
     }
     PT_CUDA(mark(2));
-    if (cs) {
+    if (cs_pipg) {
       PT_CUDA(launch_pipg_cs(ga, handled, h->stream));
       PT_CUDA(launch_pipg_fast(ga_rest, false, h->stream));
       kernels += 1;

@@ -371,8 +371,9 @@ def test_pipg_rocket_2000_iterations(solver15, ptor):
 @pytest.mark.parametrize("nodes", [50, 100])
 def test_pipg_rocket_stopping_and_divergence_on_the_column_sparse_kernels(ptor, nodes):
     """stopping_custom and the divergence test (pipg.hpp:307-326, 475-487) on the rocket-shaped
-    subproblem, i.e. on the column-sparse kernels: one CTA per instance at N=50, a 2-CTA cluster at
-    N=100, where the maxima of the two halves are combined between cluster barriers and both CTAs
+    subproblem: the column-sparse kernel with one CTA per instance at N=50; a 2-CTA cluster at
+    N=100 (by default the dense cluster PIPG kernel, with PTOPT_CS_CLUSTER=3 the column-sparse one),
+    where the maxima of the two halves are combined between cluster barriers and both CTAs
     have to take the same verdict.  (a) loose tolerances: the solve stops early at the oracle's
     iteration; (b) a wildly underestimated sigma diverges: status, iteration index as the oracle
     reports them, workspace untouched; the neighbour instance in the batch is not disturbed."""
